@@ -1,0 +1,120 @@
+/* agile_b200.h — C-ABI of the B200-native AGILE async page-I/O hot path.
+ *
+ * One context per GPU (one process per rank under torch.distributed).  The context owns the HBM
+ * page cache (tag words + 4 KiB lines), the SQ/CQ rings and side tables, the completion service
+ * and device-engine state, and one host-pinned GPU-mapped page store per emulated device.
+ * Workload entry points launch one fused kernel on the caller's stream: its first CTAs become
+ * the device engine (K4) and the completion service (K3), the rest run the workload against the
+ * device library (K1 cache, K2 queue engine).
+ *
+ * Every function returns 0 on success or a negative code; agile_last_error() has the message.
+ * Codes -101.. map to the reference exception types:
+ *   AGILE_E_PROTOCOL     ProtocolViolation   (nvme_queue.py:23)
+ *   AGILE_E_UNKNOWN_CID  UnknownCid          (agile_service.py:27)
+ *   AGILE_E_OUT_OF_RANGE OutOfRange          (ssd_model.py:24)
+ *   AGILE_E_ILLEGAL      IllegalState        (software_cache.py:26)
+ *   AGILE_E_LIVELOCK     LivelockSuspected   (sim_core.py:23)
+ *   AGILE_E_BUFFER_BUSY  BufferBusy          (gpu_api.py:21)
+ * Config errors (unknown key / bad value) return AGILE_E_CONFIG (ValueError/KeyError in Python).
+ */
+#ifndef AGILE_B200_H
+#define AGILE_B200_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct agile_ctx agile_ctx;
+
+#define AGILE_OK 0
+#define AGILE_E_CUDA (-1)
+#define AGILE_E_ARG (-2)
+#define AGILE_E_CONFIG (-3)
+#define AGILE_E_PROTOCOL (-101)
+#define AGILE_E_UNKNOWN_CID (-102)
+#define AGILE_E_OUT_OF_RANGE (-103)
+#define AGILE_E_ILLEGAL (-104)
+#define AGILE_E_LIVELOCK (-105)
+#define AGILE_E_BUFFER_BUSY (-106)
+
+/* stats slots (agile_stats) — software_cache.py:166-170, agile_service.py:75-87, ssd_model.py:125-128 */
+enum {
+  AGILE_S_HITS = 0, AGILE_S_MISSES, AGILE_S_FILLS, AGILE_S_WRITEBACKS, AGILE_S_RESETS, AGILE_S_ATTACHES,
+  AGILE_S_COMPLETIONS, AGILE_S_WINDOWS, AGILE_S_DRAIN_ENTRIES, AGILE_S_BYTES_READ, AGILE_S_BYTES_WRITTEN,
+  AGILE_S_FETCHED, AGILE_S_DOORBELLS, AGILE_S_SQ_FULL, AGILE_S_CQE_STALLS, AGILE_S_BARRIER_COUNT,
+  AGILE_S_BARRIER_NS, AGILE_S_RETRIES, AGILE_S_ENQUEUES, AGILE_S_LOOKUPS, AGILE_S_WAITS, AGILE_S_NUM
+};
+
+/* Replaces AgileSystem.__init__ (system.py:35-90): geometry comes from the resolved config text
+ * (config.py:220-230 `config_text`, key = value lines).  Keys read here: num_devices, seed,
+ * device.{num_blocks,block_size,read_latency_ns,write_latency_ns,parallelism,jitter,jitter_ns,
+ * per_channel_rate,emulation}, queues.{pairs_per_device,sq_depth,cq_depth},
+ * cache.{lines,bytes,ways,policy,busy_choice}, share_table.enabled, service.{warps,poll_ns,
+ * idle_max_ns}, engine.warps, timing.fetch_ns, debug_locks, livelock_budget. */
+int agile_create(const char* config_text, int cuda_device, agile_ctx** out);
+int agile_destroy(agile_ctx* ctx);
+const char* agile_last_error(agile_ctx* ctx);
+/* geometry[0..9] = num_devices, pairs_per_device, sq_depth, cq_depth, lines, ways, sets,
+ * engine_warps, service_warps, infra_ctas */
+int agile_geometry(agile_ctx* ctx, uint64_t* out, int n);
+
+/* Backing store (BlockStore, ssd_model.py:61-101): pinned + GPU-mapped host memory, caller-owned
+ * when host_ptr != NULL (registered), else context-owned and zeroed.  image_path (optional) is a
+ * raw little-endian block image, offset = blk * 4096, short tail zero-padded (load_image). */
+int agile_store_attach(agile_ctx* ctx, int dev, void* host_ptr, uint64_t num_blocks, const char* image_path);
+int agile_store_ptr(agile_ctx* ctx, int dev, void** host_ptr, uint64_t* num_blocks);
+/* synthetic page contents (oracle/pages.py): kind 0 = u64 word k of block b is
+ * page_word(seed, dev, b, k); kind 1 = fp32 table values, each 32-bit half h of that word stored
+ * as (h >> 8) * 2^-23 - 1 (page_floats) */
+int agile_store_fill(agile_ctx* ctx, int dev, uint64_t seed, uint64_t first_blk, uint64_t nblk, int kind);
+int agile_store_save_image(agile_ctx* ctx, int dev, const char* path);
+
+/* reset flags: 1 cache (tags/hands/locks), 2 queues + service/engine state, 4 stats */
+int agile_reset(agile_ctx* ctx, int flags);
+int agile_stats(agile_ctx* ctx, uint64_t* out, int n);
+/* K10 event log: enable with capacity (records of 64 B); read back rendered by the host */
+int agile_trace_enable(agile_ctx* ctx, uint64_t capacity);
+int agile_event_log(agile_ctx* ctx, void* out, uint64_t cap, uint64_t* n);
+/* wait for the stream and surface device-side protocol errors */
+int agile_sync(agile_ctx* ctx, void* stream);
+
+/* Serialized async_read + wait stream (one task): golden hit/miss/eviction sequence and page
+ * bytes under a fixed issue order.  Host arrays.  outcome: 0 hit, 1 miss, 2 attach; victim: key
+ * (dev << 36 | blk) of the READY line evicted by the access, or UINT64_MAX. */
+int agile_run_seq(agile_ctx* ctx, const uint32_t* dev, const uint64_t* blk, int64_t n, int8_t* outcome,
+                  uint64_t* victim, void* pages_out);
+
+/* CTC epochs (bench/ctc.py:27-111): device pointers.  keys[epochs][tasks][reads] (dev<<36|blk),
+ * bufs = tasks*2*reads*4096 bytes, digest[tasks], epoch_t[epochs+1] (globaltimer ns). */
+int agile_run_reads(agile_ctx* ctx, const uint64_t* keys, uint32_t tasks, uint32_t reads, uint32_t epochs,
+                    int async_mode, uint64_t compute_ns, void* bufs, uint64_t* digest, uint64_t* epoch_t,
+                    void* stream);
+
+/* Closed-loop 4 KiB reads (bench/bandwidth.py:20-68): conc requesters, one outstanding each.
+ * counters[0] = completions inside [warmup, warmup+measure), counters[1..2] = window (ns). */
+int agile_run_loop(agile_ctx* ctx, uint32_t conc, uint64_t warmup_ns, uint64_t measure_ns,
+                   uint64_t max_per_task, void* bufs, uint64_t* counters, void* stream);
+
+/* Gather epochs (bench/sweeps.py:39-88): keys[tasks][epochs][gathers]; values = u32 element 0
+ * of every gathered block; epoch_t[2] = start/end. */
+int agile_run_gather(agile_ctx* ctx, const uint64_t* keys, uint32_t tasks, uint32_t epochs, uint32_t gathers,
+                     int async_mode, uint64_t compute_ns, uint32_t* values, uint64_t* epoch_t, void* stream);
+
+/* DLRM embedding-bag (K5), device pointers: idx[B][T][L] int64 rows, table_key0[T] first page
+ * key of each table, table_rows[T], out[b*out_b_stride + t*out_t_stride + d] fp32 (sum pooling),
+ * counters[2] += {lookups, miss-path lookups}.  prefetch_distance 0 = sync mode. */
+int agile_embbag(agile_ctx* ctx, const int64_t* idx, const uint64_t* table_key0, const int64_t* table_rows,
+                 float* out, uint64_t* counters, uint32_t B, uint32_t T, uint32_t L, uint32_t D,
+                 uint32_t out_b_stride, uint32_t out_t_stride, uint32_t prefetch_distance, void* stream);
+/* Same, host buffers (end-to-end through the C-ABI: H2D of indices, kernel, D2H of pooled out). */
+int agile_embbag_host(agile_ctx* ctx, const int64_t* idx, const uint64_t* table_key0, const int64_t* table_rows,
+                      float* out, uint64_t* counters, uint32_t B, uint32_t T, uint32_t L, uint32_t D,
+                      uint32_t prefetch_distance);
+/* number of user CTAs the embbag launch uses (for roofline accounting) */
+int agile_embbag_grid(agile_ctx* ctx, uint32_t* user_ctas, uint32_t* infra_ctas);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,630 @@
+// agile_b200.cu — host side of the C-ABI (include/agile_b200.h): context construction from the
+// reference's config text, HBM layout, pinned/mapped page stores, fused launches, error surfacing.
+#include <cuda_runtime.h>
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "../../include/agile_b200.h"
+#include "agile_work.cuh"
+
+using namespace agile;
+
+struct agile_ctx {
+  int device = 0;
+  DevCtx d{};
+  std::vector<void*> dev_allocs;
+  void* host_store[kMaxDevices] = {};
+  bool store_owned[kMaxDevices] = {};
+  uint64_t store_blocks[kMaxDevices] = {};
+  std::string err;
+  int sms = 148;
+  uint64_t seed = 0;
+  // pinned staging for agile_embbag_host
+  void* h_stage = nullptr;
+  size_t h_stage_bytes = 0;
+  void* d_stage = nullptr;
+  size_t d_stage_bytes = 0;
+  cudaStream_t stream = nullptr;
+};
+
+namespace {
+
+int fail(agile_ctx* c, int code, const std::string& msg) {
+  if (c) c->err = msg;
+  return code;
+}
+
+#define CK(call)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return fail(ctx, AGILE_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+std::map<std::string, std::string> parse_kv(const char* text) {
+  std::map<std::string, std::string> kv;
+  std::istringstream in(text ? text : "");
+  std::string line;
+  while (std::getline(in, line)) {
+    const size_t hash = line.find('#');
+    if (hash != std::string::npos) line = line.substr(0, hash);
+    const size_t eq = line.find('=');
+    if (eq == std::string::npos) continue;
+    auto trim = [](std::string s) {
+      const size_t a = s.find_first_not_of(" \t\r\n");
+      const size_t b = s.find_last_not_of(" \t\r\n");
+      return a == std::string::npos ? std::string() : s.substr(a, b - a + 1);
+    };
+    kv[trim(line.substr(0, eq))] = trim(line.substr(eq + 1));
+  }
+  return kv;
+}
+
+struct Cfg {
+  std::map<std::string, std::string> kv;
+  std::string bad;
+  uint64_t u(const char* k, uint64_t def) {
+    auto it = kv.find(k);
+    if (it == kv.end() || it->second.empty()) return def;
+    char* end = nullptr;
+    const double v = strtod(it->second.c_str(), &end);
+    if (end == it->second.c_str() || v < 0) { bad = k; return def; }
+    return (uint64_t)llround(v);
+  }
+  double f(const char* k, double def) {
+    auto it = kv.find(k);
+    if (it == kv.end() || it->second.empty()) return def;
+    return atof(it->second.c_str());
+  }
+  std::string s(const char* k, const char* def) {
+    auto it = kv.find(k);
+    return it == kv.end() ? std::string(def) : it->second;
+  }
+  bool b(const char* k, bool def) {
+    auto it = kv.find(k);
+    if (it == kv.end()) return def;
+    std::string v = it->second;
+    for (auto& ch : v) ch = (char)tolower(ch);
+    return v == "true" || v == "1" || v == "yes" || v == "on";
+  }
+};
+
+bool pow2(uint64_t x) { return x && !(x & (x - 1)); }
+
+template <class T>
+int dalloc(agile_ctx* ctx, T** p, size_t count) {
+  void* q = nullptr;
+  const size_t bytes = std::max<size_t>(count * sizeof(T), 64);
+  CK(cudaMalloc(&q, bytes));
+  CK(cudaMemset(q, 0, bytes));
+  ctx->dev_allocs.push_back(q);
+  *p = reinterpret_cast<T*>(q);
+  return 0;
+}
+
+int device_error(agile_ctx* ctx) {
+  PersistWords pw;
+  CK(cudaMemcpy(&pw, ctx->d.pw, sizeof(pw), cudaMemcpyDeviceToHost));
+  if (!pw.error_code) return 0;
+  static const char* names[] = {"ok", "ProtocolViolation", "UnknownCid", "OutOfRange", "IllegalState",
+                                "LivelockSuspected", "BufferBusy"};
+  char buf[256];
+  snprintf(buf, sizeof buf, "%s (device) a=%llu b=%llu", pw.error_code < 7 ? names[pw.error_code] : "?",
+           (unsigned long long)pw.error_a, (unsigned long long)pw.error_b);
+  ctx->err = buf;
+  const int code = -(100 + (int)pw.error_code);
+  // clear so the context can be reset and reused
+  PersistWords z{};
+  z.outstanding = pw.outstanding;
+  cudaMemcpy(ctx->d.pw, &z, sizeof(z), cudaMemcpyHostToDevice);
+  return code;
+}
+
+template <class W>
+int launch(agile_ctx* ctx, const W& work, uint32_t n_user_ctas, cudaStream_t st) {
+  if (n_user_ctas == 0) n_user_ctas = 1;
+  CK(cudaMemsetAsync(ctx->d.run, 0, sizeof(RunWords), st));
+  Launch L;
+  L.n_user_ctas = n_user_ctas;
+  L.pad = 0;
+  const uint32_t grid = ctx->d.n_engine_ctas + ctx->d.n_service_ctas + n_user_ctas;
+  agile_kernel<W><<<grid, kCtaThreads, 0, st>>>(ctx->d, L, work);
+  CK(cudaGetLastError());
+  return 0;
+}
+
+template <class W>
+uint32_t resident_ctas(agile_ctx* ctx) {
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, agile_kernel<W>, kCtaThreads, 0);
+  if (per_sm < 1) per_sm = 1;
+  return (uint32_t)per_sm * (uint32_t)ctx->sms;
+}
+
+__global__ void fill_store_kernel(uint8_t* base, uint64_t seed, uint32_t dev, uint64_t first, uint64_t nblk, int kind) {
+  // page_word(seed, dev, blk, k) = splitmix64(seed ^ dev<<56 ^ blk<<9 ^ k)  (oracle/pages.py)
+  const uint64_t nwords = nblk * 512;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nwords; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t blk = first + i / 512, k = i % 512;
+    uint64_t x = seed ^ ((uint64_t)dev << 56) ^ (blk << 9) ^ k;
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    x ^= x >> 31;
+    if (kind == 1) {
+      const float lo = (float)((uint32_t)x >> 8) * (1.0f / 8388608.0f) - 1.0f;
+      const float hi = (float)((uint32_t)(x >> 32) >> 8) * (1.0f / 8388608.0f) - 1.0f;
+      x = (uint64_t)__float_as_uint(lo) | ((uint64_t)__float_as_uint(hi) << 32);
+    }
+    reinterpret_cast<uint64_t*>(base)[first * 512 + i] = x;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* agile_last_error(agile_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int agile_create(const char* config_text, int cuda_device, agile_ctx** out) {
+  if (!out) return AGILE_E_ARG;
+  *out = nullptr;
+  agile_ctx* ctx = new agile_ctx();
+  ctx->device = cuda_device;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    ctx->err = "no CUDA device visible: the B200 path has no CPU fallback";
+    *out = ctx;
+    return AGILE_E_CUDA;
+  }
+  CK(cudaSetDevice(cuda_device));
+  int sms = 0;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cuda_device));
+  ctx->sms = sms;
+  Cfg cfg;
+  cfg.kv = parse_kv(config_text);
+  DevCtx& d = ctx->d;
+  d.num_devices = (uint32_t)cfg.u("num_devices", 1);
+  const uint64_t block = cfg.u("device.block_size", 4096);
+  const uint64_t nblocks = cfg.u("device.num_blocks", 1 << 16);
+  d.pairs_per_device = (uint32_t)cfg.u("queues.pairs_per_device", 128);
+  d.sq_depth = (uint32_t)cfg.u("queues.sq_depth", 256);
+  d.cq_depth = (uint32_t)cfg.u("queues.cq_depth", 256);
+  uint64_t lines = cfg.u("cache.lines", 512);
+  const uint64_t cbytes = cfg.u("cache.bytes", 0);
+  if (cbytes) lines = std::max<uint64_t>(1, cbytes / block);   // config.py:64-67
+  uint64_t ways = cfg.u("cache.ways", 32);
+  if (ways == 0 || ways > lines) ways = lines;   // 0 = fully associative (reference-exact clock)
+  const std::string policy = cfg.s("cache.policy", "clock");
+  const std::string busy = cfg.s("cache.busy_choice", "wait");
+  d.service_warps = (uint32_t)std::max<uint64_t>(1, cfg.u("service.warps", 4));
+  d.poll_ns = (uint32_t)cfg.u("service.poll_ns", 400);
+  d.idle_max_ns = (uint32_t)std::max<uint64_t>(d.poll_ns, cfg.u("service.idle_max_ns", 3200));
+  d.engine_warps = (uint32_t)std::max<uint64_t>(1, cfg.u("engine.warps", 16));
+  const std::string emu = cfg.s("device.emulation", "model");
+  const std::string jitter = cfg.s("device.jitter", "none");
+  ctx->seed = cfg.u("seed", 0);
+  if (!cfg.bad.empty()) return fail(ctx, AGILE_E_CONFIG, "bad numeric value for " + cfg.bad), *out = ctx, AGILE_E_CONFIG;
+  *out = ctx;
+  if (block != kBlockBytes) return fail(ctx, AGILE_E_CONFIG, "device.block_size must be 4096 on the B200 path");
+  if (d.num_devices < 1 || d.num_devices > (uint32_t)kMaxDevices) return fail(ctx, AGILE_E_CONFIG, "num_devices out of range [1,16]");
+  if (!pow2(d.sq_depth) || d.sq_depth < 2 || d.sq_depth > 65536 || !pow2(d.cq_depth) || d.cq_depth < 2 || d.cq_depth > 65536)
+    return fail(ctx, AGILE_E_CONFIG, "depth must be a power of two in [2, 65536]");   // nvme_queue.py:100-103
+  if (d.pairs_per_device < 1) return fail(ctx, AGILE_E_CONFIG, "queues.pairs_per_device must be >= 1");
+  if ((uint64_t)d.num_devices * d.pairs_per_device > 65535) return fail(ctx, AGILE_E_CONFIG, "too many queue pairs");
+  if (lines % ways) return fail(ctx, AGILE_E_CONFIG, "cache.lines must be a multiple of cache.ways");
+  if (lines >= (1ull << 32) - 1) return fail(ctx, AGILE_E_CONFIG, "cache too large");
+  if (policy != "clock") return fail(ctx, AGILE_E_CONFIG, "cache.policy: only 'clock' (set-associative clock) on the B200 path");
+  if (busy != "wait" && busy != "find_another") return fail(ctx, AGILE_E_CONFIG, "cache.busy_choice must be wait|find_another");
+  if (cfg.b("share_table.enabled", false)) return fail(ctx, AGILE_E_CONFIG, "share_table.enabled=true is not supported on the B200 path (SURVEY 8(f))");
+  if (cfg.u("device.parallelism", 16) > 32 * kMaxChanPerLane) return fail(ctx, AGILE_E_CONFIG, "device.parallelism must be <= 256");
+  if (emu != "model" && emu != "link") return fail(ctx, AGILE_E_CONFIG, "device.emulation must be model|link");
+  if (jitter != "none" && jitter != "uniform" && jitter != "exponential") return fail(ctx, AGILE_E_CONFIG, "unknown jitter kind");
+  d.num_qp = d.num_devices * d.pairs_per_device;
+  d.cq_window = std::min<uint32_t>(32, d.cq_depth);
+  d.num_lines = (uint32_t)lines;
+  d.ways = (uint32_t)ways;
+  d.num_sets = (uint32_t)(lines / ways);
+  d.sets_pow2 = pow2(d.num_sets) ? 1u : 0u;
+  d.n_engine_ctas = (d.engine_warps + kCtaWarps - 1) / kCtaWarps;
+  d.n_service_ctas = (d.service_warps + kCtaWarps - 1) / kCtaWarps;
+  d.trace = 0;
+  const uint64_t budget = cfg.u("livelock_budget", 5000000);
+  d.watchdog_ns = std::max<uint64_t>(budget, 1000000) * 4000ull;   // events -> ~ns budget (>= 4 s)
+  if (d.watchdog_ns > 60ull * 1000000000ull) d.watchdog_ns = 60ull * 1000000000ull;
+  Model& m = d.model;
+  m.link_mode = emu == "link" ? 1u : 0u;
+  m.parallelism = (uint32_t)std::max<uint64_t>(1, cfg.u("device.parallelism", 16));
+  m.read_ns = cfg.u("device.read_latency_ns", 17712);
+  m.write_ns = cfg.u("device.write_latency_ns", 29789);
+  m.fetch_ns = cfg.u("timing.fetch_ns", 300);
+  m.jitter = jitter == "none" ? 0u : (jitter == "uniform" ? 1u : 2u);
+  m.jitter_ns = cfg.u("device.jitter_ns", 0);
+  const double rate = cfg.f("device.per_channel_rate", 0.0);
+  m.occupancy_ns = rate > 0 ? (uint64_t)std::max(1.0, std::floor(1e9 / rate)) : 0;   // ssd_model.py:55-58
+  m.seed = ctx->seed;
+  int rc;
+  if ((rc = dalloc(ctx, &d.tags, lines))) return rc;
+  if ((rc = dalloc(ctx, &d.set_lock, d.num_sets))) return rc;
+  if ((rc = dalloc(ctx, &d.hand, d.num_sets))) return rc;
+  if ((rc = dalloc(ctx, &d.lines, lines * kBlockBytes))) return rc;
+  const size_t nsq = (size_t)d.num_qp * d.sq_depth;
+  if ((rc = dalloc(ctx, &d.sqe, nsq * 4))) return rc;
+  if ((rc = dalloc(ctx, &d.sq_state, nsq))) return rc;
+  if ((rc = dalloc(ctx, &d.sq_done_v, nsq))) return rc;
+  if ((rc = dalloc(ctx, &d.sqw, d.num_qp))) return rc;
+  if ((rc = dalloc(ctx, &d.cmd, nsq))) return rc;
+  if ((rc = dalloc(ctx, &d.cqe, (size_t)d.num_qp * d.cq_depth))) return rc;
+  if ((rc = dalloc(ctx, &d.cqw, d.num_qp))) return rc;
+  if ((rc = dalloc(ctx, &d.chan_free, (size_t)d.num_devices * m.parallelism))) return rc;
+  if ((rc = dalloc(ctx, &d.dev_lock, d.num_devices))) return rc;
+  if ((rc = dalloc(ctx, &d.dev_seq, d.num_devices))) return rc;
+  if ((rc = dalloc(ctx, &d.run, 1))) return rc;
+  if ((rc = dalloc(ctx, &d.pw, 1))) return rc;
+  if ((rc = dalloc(ctx, &d.stats, S_NUM))) return rc;
+  if ((rc = dalloc(ctx, &d.log_count, 1))) return rc;
+  d.log = nullptr;
+  d.log_cap = 0;
+  // attach zeroed stores of the configured size for every device (callers may re-attach)
+  for (uint32_t dv = 0; dv < d.num_devices; ++dv) {
+    if ((rc = agile_store_attach(ctx, (int)dv, nullptr, nblocks, nullptr))) return rc;
+  }
+  CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+  return 0;
+}
+
+int agile_destroy(agile_ctx* ctx) {
+  if (!ctx) return 0;
+  cudaSetDevice(ctx->device);
+  cudaDeviceSynchronize();
+  for (void* p : ctx->dev_allocs) cudaFree(p);
+  for (int i = 0; i < kMaxDevices; ++i) {
+    if (!ctx->host_store[i]) continue;
+    if (ctx->store_owned[i]) cudaFreeHost(ctx->host_store[i]);
+    else cudaHostUnregister(ctx->host_store[i]);
+  }
+  if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
+  if (ctx->d_stage) cudaFree(ctx->d_stage);
+  if (ctx->d.log) cudaFree(ctx->d.log);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return 0;
+}
+
+int agile_geometry(agile_ctx* ctx, uint64_t* out, int n) {
+  if (!ctx || !out) return AGILE_E_ARG;
+  const DevCtx& d = ctx->d;
+  const uint64_t g[10] = {d.num_devices, d.pairs_per_device, d.sq_depth, d.cq_depth, d.num_lines,
+                          d.ways, d.num_sets, d.engine_warps, d.service_warps, d.n_engine_ctas + d.n_service_ctas};
+  for (int i = 0; i < n && i < 10; ++i) out[i] = g[i];
+  return 0;
+}
+
+int agile_store_attach(agile_ctx* ctx, int dev, void* host_ptr, uint64_t num_blocks, const char* image_path) {
+  if (!ctx || dev < 0 || dev >= (int)ctx->d.num_devices || num_blocks == 0) return fail(ctx, AGILE_E_ARG, "bad store args");
+  CK(cudaSetDevice(ctx->device));
+  if (num_blocks > BLK_MASK) return fail(ctx, AGILE_E_ARG, "num_blocks exceeds the 36-bit block space");
+  // drop the previous store
+  if (ctx->host_store[dev]) {
+    CK(cudaDeviceSynchronize());
+    if (ctx->store_owned[dev]) cudaFreeHost(ctx->host_store[dev]);
+    else cudaHostUnregister(ctx->host_store[dev]);
+    ctx->host_store[dev] = nullptr;
+  }
+  const size_t bytes = (size_t)num_blocks * kBlockBytes;
+  void* h = host_ptr;
+  if (h) {
+    CK(cudaHostRegister(h, bytes, cudaHostRegisterMapped | cudaHostRegisterPortable));
+    ctx->store_owned[dev] = false;
+  } else {
+    CK(cudaHostAlloc(&h, bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+    ctx->store_owned[dev] = true;
+  }
+  void* dptr = nullptr;
+  CK(cudaHostGetDevicePointer(&dptr, h, 0));
+  ctx->host_store[dev] = h;
+  ctx->store_blocks[dev] = num_blocks;
+  ctx->d.store[dev] = reinterpret_cast<const uint8_t*>(dptr);
+  ctx->d.store_w[dev] = reinterpret_cast<uint8_t*>(dptr);
+  ctx->d.store_blocks[dev] = num_blocks;
+  if (!host_ptr) {
+    // zero-default store (BlockStore: unwritten blocks read back as zeros); written by the GPU
+    // through the mapping at link speed
+    CK(cudaMemset(dptr, 0, bytes));
+    CK(cudaDeviceSynchronize());
+  }
+  if (image_path && image_path[0]) {
+    FILE* f = fopen(image_path, "rb");
+    if (!f) return fail(ctx, AGILE_E_ARG, std::string("cannot open image ") + image_path);
+    const size_t got = fread(h, 1, bytes, f);
+    fclose(f);
+    if (got < bytes) memset(reinterpret_cast<uint8_t*>(h) + got, 0, bytes - got);   // short tail zero-padded
+  }
+  return 0;
+}
+
+int agile_store_ptr(agile_ctx* ctx, int dev, void** host_ptr, uint64_t* num_blocks) {
+  if (!ctx || dev < 0 || dev >= (int)ctx->d.num_devices) return AGILE_E_ARG;
+  if (host_ptr) *host_ptr = ctx->host_store[dev];
+  if (num_blocks) *num_blocks = ctx->store_blocks[dev];
+  return 0;
+}
+
+int agile_store_fill(agile_ctx* ctx, int dev, uint64_t seed, uint64_t first_blk, uint64_t nblk, int kind) {
+  if (!ctx || dev < 0 || dev >= (int)ctx->d.num_devices) return AGILE_E_ARG;
+  if (first_blk + nblk > ctx->store_blocks[dev]) return fail(ctx, AGILE_E_OUT_OF_RANGE, "fill beyond store");
+  CK(cudaSetDevice(ctx->device));
+  fill_store_kernel<<<ctx->sms * 8, 256>>>(ctx->d.store_w[dev], seed, (uint32_t)dev, first_blk, nblk, kind);
+  CK(cudaGetLastError());
+  CK(cudaDeviceSynchronize());
+  return 0;
+}
+
+int agile_store_save_image(agile_ctx* ctx, int dev, const char* path) {
+  if (!ctx || dev < 0 || dev >= (int)ctx->d.num_devices || !path) return AGILE_E_ARG;
+  CK(cudaDeviceSynchronize());
+  const uint8_t* h = reinterpret_cast<const uint8_t*>(ctx->host_store[dev]);
+  // top = last block holding a non-zero byte (+1): the dense analogue of save_image's
+  // max(written)+1 (ssd_model.py:97-101)
+  uint64_t top = ctx->store_blocks[dev];
+  while (top > 0) {
+    const uint64_t* w = reinterpret_cast<const uint64_t*>(h + (top - 1) * kBlockBytes);
+    bool nz = false;
+    for (int k = 0; k < 512 && !nz; ++k) nz = w[k] != 0;
+    if (nz) break;
+    --top;
+  }
+  FILE* f = fopen(path, "wb");
+  if (!f) return fail(ctx, AGILE_E_ARG, std::string("cannot open ") + path);
+  fwrite(h, 1, top * kBlockBytes, f);
+  fclose(f);
+  return 0;
+}
+
+int agile_reset(agile_ctx* ctx, int flags) {
+  if (!ctx) return AGILE_E_ARG;
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaDeviceSynchronize());
+  DevCtx& d = ctx->d;
+  if (flags & 1) {
+    CK(cudaMemset(d.tags, 0, (size_t)d.num_lines * 8));
+    CK(cudaMemset(d.hand, 0, (size_t)d.num_sets * 4));
+    CK(cudaMemset(d.set_lock, 0, (size_t)d.num_sets * 4));
+  }
+  if (flags & 2) {
+    const size_t nsq = (size_t)d.num_qp * d.sq_depth;
+    CK(cudaMemset(d.sqe, 0, nsq * 64));
+    CK(cudaMemset(d.sq_state, 0, nsq * 4));
+    CK(cudaMemset(d.sq_done_v, 0, nsq * 8));
+    CK(cudaMemset(d.sqw, 0, (size_t)d.num_qp * sizeof(SqWords)));
+    CK(cudaMemset(d.cmd, 0, nsq * sizeof(CmdCtx)));
+    CK(cudaMemset(d.cqe, 0, (size_t)d.num_qp * d.cq_depth * 16));
+    CK(cudaMemset(d.cqw, 0, (size_t)d.num_qp * sizeof(CqWords)));
+    CK(cudaMemset(d.chan_free, 0, (size_t)d.num_devices * d.model.parallelism * 8));
+    CK(cudaMemset(d.dev_seq, 0, (size_t)d.num_devices * 8));
+    CK(cudaMemset(d.pw, 0, sizeof(PersistWords)));
+  }
+  if (flags & 4) {
+    CK(cudaMemset(d.stats, 0, S_NUM * 8));
+    CK(cudaMemset(d.log_count, 0, 8));
+  }
+  CK(cudaDeviceSynchronize());
+  return 0;
+}
+
+int agile_stats(agile_ctx* ctx, uint64_t* out, int n) {
+  if (!ctx || !out) return AGILE_E_ARG;
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaDeviceSynchronize());
+  uint64_t s[S_NUM];
+  CK(cudaMemcpy(s, ctx->d.stats, sizeof s, cudaMemcpyDeviceToHost));
+  for (int i = 0; i < n && i < S_NUM; ++i) out[i] = s[i];
+  return 0;
+}
+
+int agile_trace_enable(agile_ctx* ctx, uint64_t capacity) {
+  if (!ctx) return AGILE_E_ARG;
+  CK(cudaSetDevice(ctx->device));
+  if (ctx->d.log) { cudaFree(ctx->d.log); ctx->d.log = nullptr; }
+  ctx->d.log_cap = 0;
+  ctx->d.trace = 0;
+  if (capacity) {
+    void* p = nullptr;
+    CK(cudaMalloc(&p, capacity * 64));
+    ctx->d.log = reinterpret_cast<uint4*>(p);
+    ctx->d.log_cap = capacity;
+    ctx->d.trace = 1;
+  }
+  CK(cudaMemset(ctx->d.log_count, 0, 8));
+  return 0;
+}
+
+int agile_event_log(agile_ctx* ctx, void* out, uint64_t cap, uint64_t* n) {
+  if (!ctx || !n) return AGILE_E_ARG;
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaDeviceSynchronize());
+  uint64_t cnt = 0;
+  CK(cudaMemcpy(&cnt, ctx->d.log_count, 8, cudaMemcpyDeviceToHost));
+  *n = cnt;
+  if (cnt > ctx->d.log_cap) return fail(ctx, AGILE_E_ARG, "event log overflow: raise the trace capacity");
+  if (out && cap) CK(cudaMemcpy(out, ctx->d.log, std::min(cnt, cap) * 64, cudaMemcpyDeviceToHost));
+  return 0;
+}
+
+int agile_sync(agile_ctx* ctx, void* stream) {
+  if (!ctx) return AGILE_E_ARG;
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaStreamSynchronize(reinterpret_cast<cudaStream_t>(stream)));
+  return device_error(ctx);
+}
+
+int agile_run_seq(agile_ctx* ctx, const uint32_t* dev, const uint64_t* blk, int64_t n, int8_t* outcome,
+                  uint64_t* victim, void* pages_out) {
+  if (!ctx || n < 0 || (n && (!dev || !blk || !outcome || !victim))) return fail(ctx, AGILE_E_ARG, "bad seq args");
+  CK(cudaSetDevice(ctx->device));
+  for (int64_t i = 0; i < n; ++i) {
+    if (dev[i] >= ctx->d.num_devices) return fail(ctx, AGILE_E_OUT_OF_RANGE, "no such device");
+    if (blk[i] >= ctx->store_blocks[dev[i]]) return fail(ctx, AGILE_E_OUT_OF_RANGE, "block out of range");
+  }
+  if (n == 0) return 0;
+  uint32_t* d_dev; uint64_t* d_blk; int8_t* d_out; uint64_t* d_vic; uint4* d_pages = nullptr; uint4* d_scr;
+  CK(cudaMalloc(&d_dev, n * 4));
+  CK(cudaMalloc(&d_blk, n * 8));
+  CK(cudaMalloc(&d_out, n));
+  CK(cudaMalloc(&d_vic, n * 8));
+  CK(cudaMalloc(&d_scr, kBlockBytes));
+  if (pages_out) CK(cudaMalloc(&d_pages, (size_t)n * kBlockBytes));
+  CK(cudaMemcpy(d_dev, dev, n * 4, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(d_blk, blk, n * 8, cudaMemcpyHostToDevice));
+  SeqWork w;
+  w.dev = d_dev; w.blk = reinterpret_cast<const u64*>(d_blk); w.n = n;
+  w.outcome = reinterpret_cast<signed char*>(d_out); w.victim = reinterpret_cast<u64*>(d_vic);
+  w.pages = d_pages; w.scratch = d_scr;
+  int rc = launch(ctx, w, 1, ctx->stream);
+  if (!rc) rc = agile_sync(ctx, ctx->stream);
+  if (!rc) {
+    CK(cudaMemcpy(outcome, d_out, n, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(victim, d_vic, n * 8, cudaMemcpyDeviceToHost));
+    if (pages_out) CK(cudaMemcpy(pages_out, d_pages, (size_t)n * kBlockBytes, cudaMemcpyDeviceToHost));
+  }
+  cudaFree(d_dev); cudaFree(d_blk); cudaFree(d_out); cudaFree(d_vic); cudaFree(d_scr);
+  if (d_pages) cudaFree(d_pages);
+  return rc;
+}
+
+int agile_run_reads(agile_ctx* ctx, const uint64_t* keys, uint32_t tasks, uint32_t reads, uint32_t epochs,
+                    int async_mode, uint64_t compute_ns, void* bufs, uint64_t* digest, uint64_t* epoch_t,
+                    void* stream) {
+  if (!ctx || !keys || !bufs || !digest || !epoch_t || !tasks || !reads || !epochs) return fail(ctx, AGILE_E_ARG, "bad reads args");
+  if (reads > (uint32_t)ReadsWork::MAXR) return fail(ctx, AGILE_E_ARG, "reads_per_task > 64");
+  CK(cudaSetDevice(ctx->device));
+  ReadsWork w;
+  w.keys = reinterpret_cast<const u64*>(keys);
+  w.bufs = reinterpret_cast<uint4*>(bufs);
+  w.digest = reinterpret_cast<u64*>(digest);
+  w.epoch_t = reinterpret_cast<u64*>(epoch_t);
+  w.tasks = tasks; w.reads = reads; w.epochs = epochs; w.async_mode = async_mode ? 1u : 0u;
+  w.compute_ns = compute_ns;
+  const uint32_t users = (tasks + kCtaThreads - 1) / kCtaThreads;
+  const uint32_t cap = resident_ctas<ReadsWork>(ctx);
+  if (users + ctx->d.n_engine_ctas + ctx->d.n_service_ctas > cap)
+    return fail(ctx, AGILE_E_ARG, "tasks exceed co-resident capacity for the epoch barrier");
+  return launch(ctx, w, users, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int agile_run_loop(agile_ctx* ctx, uint32_t conc, uint64_t warmup_ns, uint64_t measure_ns,
+                   uint64_t max_per_task, void* bufs, uint64_t* counters, void* stream) {
+  if (!ctx || !conc || !bufs || !counters) return fail(ctx, AGILE_E_ARG, "bad loop args");
+  CK(cudaSetDevice(ctx->device));
+  LoopWork w;
+  w.bufs = reinterpret_cast<uint4*>(bufs);
+  w.counters = reinterpret_cast<unsigned long long*>(counters);
+  w.conc = conc;
+  w.ndev = ctx->d.num_devices;
+  uint64_t nb = ctx->store_blocks[0];
+  for (uint32_t i = 1; i < ctx->d.num_devices; ++i) nb = std::min<uint64_t>(nb, ctx->store_blocks[i]);
+  w.num_blocks = nb;
+  w.warmup_ns = warmup_ns;
+  w.measure_ns = measure_ns;
+  w.max_per_task = max_per_task ? max_per_task : ~0ull;
+  const uint32_t users = (conc + kCtaThreads - 1) / kCtaThreads;
+  return launch(ctx, w, users, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int agile_run_gather(agile_ctx* ctx, const uint64_t* keys, uint32_t tasks, uint32_t epochs, uint32_t gathers,
+                     int async_mode, uint64_t compute_ns, uint32_t* values, uint64_t* epoch_t, void* stream) {
+  if (!ctx || !keys || !values || !epoch_t || !tasks || !epochs || !gathers) return fail(ctx, AGILE_E_ARG, "bad gather args");
+  CK(cudaSetDevice(ctx->device));
+  GatherWork w;
+  w.keys = reinterpret_cast<const u64*>(keys);
+  w.values = values;
+  w.epoch_t = reinterpret_cast<u64*>(epoch_t);
+  w.tasks = tasks; w.epochs = epochs; w.gathers = gathers; w.async_mode = async_mode ? 1u : 0u;
+  w.compute_ns = compute_ns;
+  const uint32_t users = (tasks + kCtaThreads - 1) / kCtaThreads;
+  const uint32_t cap = resident_ctas<GatherWork>(ctx);
+  if (users + ctx->d.n_engine_ctas + ctx->d.n_service_ctas > cap)
+    return fail(ctx, AGILE_E_ARG, "tasks exceed co-resident capacity for the epoch barrier");
+  return launch(ctx, w, users, reinterpret_cast<cudaStream_t>(stream));
+}
+
+static uint32_t embbag_users(agile_ctx* ctx) {
+  const uint32_t cap = resident_ctas<EmbBagWork>(ctx);
+  const uint32_t infra = ctx->d.n_engine_ctas + ctx->d.n_service_ctas;
+  return cap > infra + 1 ? cap - infra : 1;
+}
+
+int agile_embbag_grid(agile_ctx* ctx, uint32_t* user_ctas, uint32_t* infra_ctas) {
+  if (!ctx) return AGILE_E_ARG;
+  if (user_ctas) *user_ctas = embbag_users(ctx);
+  if (infra_ctas) *infra_ctas = ctx->d.n_engine_ctas + ctx->d.n_service_ctas;
+  return 0;
+}
+
+int agile_embbag(agile_ctx* ctx, const int64_t* idx, const uint64_t* table_key0, const int64_t* table_rows,
+                 float* out, uint64_t* counters, uint32_t B, uint32_t T, uint32_t L, uint32_t D,
+                 uint32_t out_b_stride, uint32_t out_t_stride, uint32_t prefetch_distance, void* stream) {
+  if (!ctx || !idx || !table_key0 || !table_rows || !out || !counters) return fail(ctx, AGILE_E_ARG, "null embbag arg");
+  if (L == 0 || L > 32) return fail(ctx, AGILE_E_ARG, "pooling factor L must be in [1, 32]");
+  if (D == 0 || D > 128 || D % 4 || (1024u % D) != 0) return fail(ctx, AGILE_E_ARG, "D must divide 1024, be a multiple of 4 and <= 128");
+  if ((uint64_t)B * T >= (1ull << 31)) return fail(ctx, AGILE_E_ARG, "too many bags");
+  CK(cudaSetDevice(ctx->device));
+  EmbBagWork w;
+  w.idx = reinterpret_cast<const long long*>(idx);
+  w.table_key0 = reinterpret_cast<const u64*>(table_key0);
+  w.table_rows = reinterpret_cast<const long long*>(table_rows);
+  w.out = out;
+  w.lookups_miss = reinterpret_cast<u64*>(counters);
+  w.B = B; w.T = T; w.L = L; w.D = D;
+  w.pd = prefetch_distance;
+  uint32_t rpp = kBlockBytes / (D * 4), sh = 0;
+  while ((1u << sh) < rpp) ++sh;
+  w.rows_per_page_shift = sh;
+  w.out_b_stride = out_b_stride ? out_b_stride : T * D;
+  w.out_t_stride = out_t_stride ? out_t_stride : D;
+  const uint32_t users = embbag_users(ctx);
+  w.nwarps_total = users * kCtaWarps;
+  return launch(ctx, w, users, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int agile_embbag_host(agile_ctx* ctx, const int64_t* idx, const uint64_t* table_key0, const int64_t* table_rows,
+                      float* out, uint64_t* counters, uint32_t B, uint32_t T, uint32_t L, uint32_t D,
+                      uint32_t prefetch_distance) {
+  if (!ctx || !idx || !out) return fail(ctx, AGILE_E_ARG, "null embbag_host arg");
+  CK(cudaSetDevice(ctx->device));
+  const size_t n_idx = (size_t)B * T * L * 8, n_out = (size_t)B * T * D * 4, n_tab = (size_t)T * 8;
+  const size_t need = n_idx + n_out + 2 * n_tab + 16 + 256;
+  if (ctx->d_stage_bytes < need) {
+    if (ctx->d_stage) cudaFree(ctx->d_stage);
+    CK(cudaMalloc(&ctx->d_stage, need));
+    ctx->d_stage_bytes = need;
+  }
+  uint8_t* base = reinterpret_cast<uint8_t*>(ctx->d_stage);
+  int64_t* d_idx = reinterpret_cast<int64_t*>(base);
+  float* d_out = reinterpret_cast<float*>(base + n_idx);
+  uint64_t* d_key = reinterpret_cast<uint64_t*>(base + n_idx + n_out);
+  int64_t* d_rows = reinterpret_cast<int64_t*>(base + n_idx + n_out + n_tab);
+  uint64_t* d_cnt = reinterpret_cast<uint64_t*>(base + n_idx + n_out + 2 * n_tab);
+  cudaStream_t st = ctx->stream;
+  CK(cudaMemcpyAsync(d_idx, idx, n_idx, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_key, table_key0, n_tab, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_rows, table_rows, n_tab, cudaMemcpyHostToDevice, st));
+  CK(cudaMemsetAsync(d_cnt, 0, 16, st));
+  int rc = agile_embbag(ctx, d_idx, d_key, d_rows, d_out, d_cnt, B, T, L, D, 0, 0, prefetch_distance, st);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(out, d_out, n_out, cudaMemcpyDeviceToHost, st));
+  uint64_t cnt[2] = {0, 0};
+  CK(cudaMemcpyAsync(cnt, d_cnt, 16, cudaMemcpyDeviceToHost, st));
+  rc = agile_sync(ctx, st);
+  if (!rc && counters) { counters[0] += cnt[0]; counters[1] += cnt[1]; }
+  return rc;
+}
+
+}  // extern "C"

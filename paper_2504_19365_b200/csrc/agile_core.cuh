@@ -1,0 +1,1231 @@
+// agile_core.cuh — cache (K1), SQ submit (K2), completion service (K3), device engine (K4).
+// All user-facing functions are warp-collective: every lane of the warp calls them, each lane
+// carrying its own request (or none); the warp coalesces, probes and submits cooperatively.
+#pragma once
+#include "agile_dev.cuh"
+#undef SPIN_FILE_ID
+#define SPIN_FILE_ID 1
+
+namespace agile {
+
+constexpr u32 FULL = 0xffffffffu;
+constexpr u32 NONE = 0xffffffffu;
+
+// access outcomes (software_cache.py:37-41)
+enum : int { R_NONE = -1, R_HIT = 0, R_FILLING = 1, R_MISS = 2, R_RETRY = 3 };
+
+struct Launch {
+  u32 n_user_ctas;
+  u32 pad;
+};
+
+// position of the n-th (0-based) set bit of m (n < popc(m))
+__device__ __forceinline__ u32 nth_set_bit(u32 m, u32 n) {
+  u32 pos = 0;
+#pragma unroll
+  for (int w = 16; w; w >>= 1) {
+    const u32 lowmask = (1u << w) - 1u;
+    const u32 lo = __popc(m & lowmask);
+    if (n >= lo) { n -= lo; m >>= w; pos += w; }
+    else m &= lowmask;
+  }
+  return pos;
+}
+
+// ======================================================================= K1: cache
+
+// Probe one key (warp-uniform) across all ways of its set.  Relaxed loads; callers that act
+// on the result re-validate (seqlock) or hold the set lock.
+__device__ __forceinline__ bool probe_key_warp(const DevCtx& c, u64 key, u32& line, u64& word) {
+  const u32 lane = lane_id();
+  const u64 base = (u64)set_of(c, key) * c.ways;
+  for (u32 w0 = 0; w0 < c.ways; w0 += 32) {
+    const u32 w = w0 + lane;
+    u64 tw = 0;
+    bool m = false;
+    if (w < c.ways) {
+      tw = ld_relaxed(&c.tags[base + w]);
+      m = tw_live(tw) && tw_key(tw) == key;
+    }
+    const u32 b = __ballot_sync(FULL, m);
+    if (b) {
+      const int src = __ffs(b) - 1;
+      line = (u32)(base + w0 + src);
+      word = __shfl_sync(FULL, tw, src);
+      return true;
+    }
+  }
+  return false;
+}
+
+// Batched warp-cooperative probe: every active lane carries a key; lanes are split into groups
+// of W (one lane per way) and each group resolves one key per round with a ballot.  Returns per
+// lane the matching (line, word) or line = NONE.  Used for W <= 32; larger W falls back to the
+// per-key probe.
+__device__ __forceinline__ void probe_lanes(const DevCtx& c, bool active, u64 key, u32& line, u64& word) {
+  const u32 lane = lane_id();
+  line = NONE;
+  word = 0;
+  const u32 act = __ballot_sync(FULL, active);
+  if (!act) return;
+  const u32 W = c.ways;
+  if (W > 32 || (W & (W - 1))) {
+    // generic path: one key at a time
+    u32 todo = act;
+    while (todo) {
+      const int src = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const u64 k = __shfl_sync(FULL, key, src);
+      u32 l; u64 w;
+      const bool f = probe_key_warp(c, k, l, w);
+      if (lane == (u32)src && f) { line = l; word = w; }
+    }
+    return;
+  }
+  const u32 G = 32 / W;                // keys per round
+  const u32 g = lane / W, way = lane % W;
+  const u32 nact = __popc(act);
+  const u32 my_rank = __popc(act & lanemask_lt());
+  const u32 rounds = (nact + G - 1) / G;
+  const u32 gmask = (W == 32) ? FULL : ((1u << W) - 1);
+  for (u32 r0 = 0; r0 < rounds; r0 += 8) {
+    u64 tw[8];
+    u64 sb[8];
+#pragma unroll
+    for (u32 j = 0; j < 8; ++j) {
+      const u32 rank = (r0 + j) * G + g;
+      tw[j] = 0;
+      sb[j] = 0;
+      // source lane of this rank (rank-th set bit of act)
+      u32 src = 0;
+      const bool valid = rank < nact;
+      if (valid) src = nth_set_bit(act, rank);
+      const u64 k = __shfl_sync(FULL, key, valid ? src : 0);
+      if (valid && r0 + j < rounds) {
+        sb[j] = (u64)set_of(c, k) * W;
+        const u64 t = ld_relaxed(&c.tags[sb[j] + way]);
+        tw[j] = (tw_live(t) && tw_key(t) == k) ? t : 0;
+      }
+    }
+#pragma unroll
+    for (u32 j = 0; j < 8; ++j) {
+      const u32 b = __ballot_sync(FULL, tw[j] != 0);
+      // the lane owning rank (r0+j)*G + g' reads group g' bits
+      const bool mine = active && (my_rank / G) == (r0 + j);
+      const u32 mg = my_rank % G;
+      const u32 bits = (b >> (mg * W)) & gmask;
+      const int hw = bits ? __ffs(bits) - 1 : 0;
+      const u64 wv = __shfl_sync(FULL, tw[j], mg * W + hw);
+      const u64 base = __shfl_sync(FULL, sb[j], mg * W + hw);
+      if (mine && bits) { line = (u32)(base + hw); word = wv; }
+    }
+  }
+}
+
+// Clock victim choice over one set held under its lock (ClockPolicy.map semantics,
+// software_cache.py:109-126, per set; SURVEY A.2 plug-in).  Lane w holds way w's word (W<=32).
+// Returns victim way or -1; fills the swept-and-cleared way mask and the new hand.
+__device__ __forceinline__ int clock_pick_vec(u32 W, u32 hand, u32 avail, u32 ref1, u32& cleared, u32& new_hand) {
+  const u32 fullw = (W == 32) ? FULL : ((1u << W) - 1);
+  auto rot = [&](u32 m) -> u32 { return hand ? (((m >> hand) | (m << (W - hand))) & fullw) : (m & fullw); };
+  auto unrot = [&](u32 m) -> u32 { return hand ? (((m << hand) | (m >> (W - hand))) & fullw) : (m & fullw); };
+  const u32 A = rot(avail), R = rot(ref1);
+  const u32 Z = A & ~R;
+  int p;
+  u32 clr;
+  if (Z) {
+    p = __ffs(Z) - 1;
+    clr = A & R & ((1u << p) - 1u);
+  } else if (A) {
+    p = __ffs(A) - 1;
+    clr = A & R;
+  } else {
+    cleared = 0;
+    new_hand = hand;
+    return -1;
+  }
+  const int v = (int)((hand + (u32)p) % W);
+  // the victim's own ref bit is re-set by on_insert (software_cache.py:106-107): never clear it
+  cleared = unrot(clr) & ~(1u << v);
+  new_hand = (u32)(v + 1) % W;
+  return v;
+}
+
+// Serial exact sweep for W > 32 (fully associative parity mode), run by one lane.
+__device__ __forceinline__ int clock_pick_serial(const DevCtx& c, u64 base, u32 W, u32 hand, u32& new_hand,
+                                                 u64* cleared_list, u32& ncleared, u32 max_cleared) {
+  u32 h = hand;
+  ncleared = 0;
+  for (u32 scanned = 0; scanned < 2 * W; ++scanned) {
+    const u32 idx = h;
+    const u64 w = ld_relaxed(&c.tags[base + idx]);
+    h = (idx + 1) % W;
+    if (tw_state(w) == ST_BUSY || tw_pins(w)) continue;
+    if (tw_ref(w)) {
+      atomicAnd(&c.tags[base + idx], ~REF_BIT);
+      continue;
+    }
+    new_hand = h;
+    return (int)idx;
+  }
+  new_hand = hand;
+  return -1;
+}
+
+__device__ __forceinline__ bool lock_set(const DevCtx& c, u32 set) {
+  int ok = 1;
+  if (lane_id() == 0) {
+    Spin sp;
+    while (atom_cas_acquire(&c.set_lock[set], 0u, 1u) != 0u) {
+      if (!sp.again(c, 256, __LINE__ + 100000 * SPIN_FILE_ID)) { ok = 0; break; }
+    }
+  }
+  return __shfl_sync(FULL, ok, 0) != 0;
+}
+__device__ __forceinline__ void unlock_set(const DevCtx& c, u32 set) {
+  __syncwarp();
+  if (lane_id() == 0) st_release(&c.set_lock[set], 0u);
+}
+
+__device__ __forceinline__ void log_state(const DevCtx& c, u32 who, u32 line, u32 from, u32 to, u64 key) {
+  log_ev(c, who, M_CACHE, A_STATE, line, from, to, key_dev(key), key_blk(key));
+}
+
+// Miss path for one key (warp-uniform), under the set lock: re-probe (in-flight dedup), else pick
+// a clock victim, CAS it to BUSY(key) and return R_MISS with the line to fill.  pin_n pins are
+// added atomically to the resulting line (async_read waiters).  victim_key gets the evicted READY
+// key (evict_reset, software_cache.py:339-346) or ~0.
+__device__ int claim_key_warp(const DevCtx& c, u64 key, u32 pin_n, u32 who, u32& line, u64& word, u64& victim_key) {
+  const u32 lane = lane_id();
+  const u32 set = set_of(c, key);
+  const u64 base = (u64)set * c.ways;
+  const u32 W = c.ways;
+  victim_key = ~0ull;
+  if (lane == 0) log_ev(c, who, M_CACHE, A_MISS, key_dev(key), key_blk(key));
+  if (!lock_set(c, set)) return R_RETRY;
+  for (int attempt = 0;; ++attempt) {
+    if (aborted(c)) { unlock_set(c, set); return R_RETRY; }
+    u32 l; u64 w;
+    if (probe_key_warp(c, key, l, w)) {
+      int kind = tw_state(w) == ST_BUSY ? R_FILLING : R_HIT;
+      if (lane == 0) {
+        if (pin_n) w = atomicAdd(&c.tags[l], (u64)pin_n * PIN_ONE) + (u64)pin_n * PIN_ONE;
+        if (kind == R_HIT && !tw_ref(w)) atomicOr(&c.tags[l], REF_BIT);
+        kind = tw_state(w) == ST_BUSY ? R_FILLING : R_HIT;
+      }
+      kind = __shfl_sync(FULL, kind, 0);
+      w = __shfl_sync(FULL, w, 0);
+      unlock_set(c, set);
+      line = l; word = w;
+      return kind;
+    }
+    int v;
+    u32 new_hand;
+    u64 old = 0;
+    u32 cleared = 0;
+    const u32 hand = ld_relaxed(&c.hand[set]);
+    if (W <= 32) {
+      u64 tw = 0;
+      if (lane < W) tw = ld_relaxed(&c.tags[base + lane]);
+      const u32 avail = __ballot_sync(FULL, lane < W && tw_state(tw) != ST_BUSY && tw_pins(tw) == 0);
+      const u32 ref1 = __ballot_sync(FULL, lane < W && tw_ref(tw));
+      v = clock_pick_vec(W, hand, avail, ref1, cleared, new_hand);
+      if (v >= 0) old = __shfl_sync(FULL, tw, v);
+    } else {
+      int vv = -1;
+      u32 nh = hand;
+      u32 ncl = 0;
+      if (lane == 0) vv = clock_pick_serial(c, base, W, hand, nh, nullptr, ncl, 0);
+      v = __shfl_sync(FULL, vv, 0);
+      new_hand = __shfl_sync(FULL, nh, 0);
+      if (v >= 0) old = ld_relaxed(&c.tags[base + v]);
+    }
+    if (v < 0) {  // every way busy/pinned: caller waits (any_free_wait, software_cache.py:364-365)
+      unlock_set(c, set);
+      return R_RETRY;
+    }
+    const u64 nw = tw_make(ST_BUSY, key, tw_ver(old) + 1, true, pin_n);
+    u64 prev = 0;
+    if (lane == 0) prev = atomicCAS(&c.tags[base + v], old, nw);
+    prev = __shfl_sync(FULL, prev, 0);
+    if (prev != old) continue;   // a hitter touched ref/pins: re-evaluate
+    if (W <= 32 && lane < W && ((cleared >> lane) & 1u)) atomicAnd(&c.tags[base + lane], ~REF_BIT);
+    if (lane == 0) {
+      st_relaxed(&c.hand[set], new_hand);
+      const u32 ost = tw_state(old);
+      if (ost == ST_READY || ost == ST_MODIFIED) {
+        victim_key = tw_key(old);
+        atomicAdd(&c.stats[S_RESETS], 1ull);
+        log_ev(c, who, M_CACHE, A_EVICT_RESET, base + v, key_dev(victim_key), key_blk(victim_key));
+        log_state(c, who, (u32)(base + v), ost, ST_INVALID, victim_key);
+      }
+      log_state(c, who, (u32)(base + v), ST_INVALID, ST_BUSY, key);
+      atomicAdd(&c.stats[S_FILLS], 1ull);
+    }
+    victim_key = __shfl_sync(FULL, victim_key, 0);
+    unlock_set(c, set);
+    line = (u32)(base + v);
+    word = nw;
+    return R_MISS;
+  }
+}
+
+// Lane-parallel miss path (W <= 32): every lane with `want` claims its own key under its set's
+// lock, so the claims of one warp overlap instead of running one after another.  The loop is
+// convergent — each pass, every waiting lane tries its set lock once and the winners run the
+// O(W) claim — so no lane ever spins inside divergent code; lanes sharing a set are serialised
+// by the lock.  Same semantics as claim_key_warp (re-probe for in-flight dedup, clock victim,
+// CAS to BUSY(key)).  Returns per lane R_HIT / R_FILLING / R_MISS / R_RETRY (R_NONE if !want).
+__device__ int claim_lanes(const DevCtx& c, bool want, u64 key, u32 pin_n, u32 who, u32& line, u64& word,
+                           u64& victim_key) {
+  const u32 lane = lane_id();
+  const u32 W = c.ways;
+  int kind = R_NONE;
+  victim_key = ~0ull;
+  const u32 set = want ? set_of(c, key) : 0u;
+  const u64 base = (u64)set * W;
+  if (want) log_ev(c, who, M_CACHE, A_MISS, key_dev(key), key_blk(key));
+  u32 pending = __ballot_sync(FULL, want);
+  u32 fills = 0, resets = 0;
+  Spin sp;
+  while (pending) {
+    const bool mine = (pending >> lane) & 1u;
+    bool got = false;
+    bool settled = false;
+    if (mine) got = atom_cas_acquire(&c.set_lock[set], 0u, 1u) == 0u;
+    if (got) {
+      u32 avail = 0, ref1 = 0;
+      int found = -1;
+      u64 fw = 0;
+      for (u32 w = 0; w < W; ++w) {
+        const u64 t = ld_relaxed(&c.tags[base + w]);
+        if (tw_live(t) && tw_key(t) == key) { found = (int)w; fw = t; }
+        if (tw_state(t) != ST_BUSY && tw_pins(t) == 0) avail |= 1u << w;
+        if (tw_ref(t)) ref1 |= 1u << w;
+      }
+      if (found >= 0) {
+        u64 w2 = fw;
+        if (pin_n) w2 = atomicAdd(&c.tags[base + found], (u64)pin_n * PIN_ONE) + (u64)pin_n * PIN_ONE;
+        kind = tw_state(w2) == ST_BUSY ? R_FILLING : R_HIT;
+        if (kind == R_HIT && !tw_ref(w2)) atomicOr(&c.tags[base + found], REF_BIT);
+        line = (u32)(base + found);
+        word = w2;
+        settled = true;
+      } else {
+        const u32 hand = ld_relaxed(&c.hand[set]);
+        u32 cleared = 0, nh = hand;
+        const int v = clock_pick_vec(W, hand, avail, ref1, cleared, nh);
+        if (v < 0) {
+          kind = R_RETRY;   // every way busy/pinned: wait (any_free_wait, software_cache.py:364-365)
+          settled = true;
+        } else {
+          const u64 old = ld_relaxed(&c.tags[base + v]);
+          if (tw_state(old) != ST_BUSY && tw_pins(old) == 0) {
+            const u64 nw = tw_make(ST_BUSY, key, tw_ver(old) + 1, true, pin_n);
+            if (atomicCAS(&c.tags[base + v], old, nw) == old) {
+              for (u32 m = cleared; m; m &= m - 1) atomicAnd(&c.tags[base + (__ffs(m) - 1)], ~REF_BIT);
+              st_relaxed(&c.hand[set], nh);
+              const u32 ost = tw_state(old);
+              if (ost == ST_READY || ost == ST_MODIFIED) {
+                victim_key = tw_key(old);
+                ++resets;
+                log_ev(c, who, M_CACHE, A_EVICT_RESET, base + v, key_dev(victim_key), key_blk(victim_key));
+                log_state(c, who, (u32)(base + v), ost, ST_INVALID, victim_key);
+              }
+              log_state(c, who, (u32)(base + v), ST_INVALID, ST_BUSY, key);
+              ++fills;
+              kind = R_MISS;
+              line = (u32)(base + v);
+              word = nw;
+              settled = true;
+            }
+          }
+          // else: a hitter pinned/touched the victim between scan and CAS: re-evaluate next pass
+        }
+      }
+      st_release(&c.set_lock[set], 0u);
+    }
+    const u32 progressed = __ballot_sync(FULL, got);
+    pending &= ~__ballot_sync(FULL, settled);
+    if (pending && !progressed) {
+      if (!sp.again(c, 512, __LINE__ + 100000 * SPIN_FILE_ID)) {
+        if ((pending >> lane) & 1u) kind = R_RETRY;
+        break;
+      }
+    }
+  }
+  const u32 nf = __popc(__ballot_sync(FULL, fills != 0));
+  const u32 nr = __popc(__ballot_sync(FULL, resets != 0));
+  if (lane == 0) {
+    if (nf) atomicAdd(&c.stats[S_FILLS], (u64)nf);
+    if (nr) atomicAdd(&c.stats[S_RESETS], (u64)nr);
+  }
+  return kind;
+}
+
+// Pin a line found by a lock-free probe; returns the post-pin word, or 0 if the line no longer
+// holds `key` (caller retries through the miss path).
+__device__ __forceinline__ u64 pin_line(const DevCtx& c, u32 line, u64 key, u32 n) {
+  const u64 old = atomicAdd(&c.tags[line], (u64)n * PIN_ONE);
+  if (!tw_live(old) || tw_key(old) != key || tw_pins(old) > 900) {
+    atomicAdd(&c.tags[line], (u64)0 - (u64)n * PIN_ONE);
+    return 0;
+  }
+  return old + (u64)n * PIN_ONE;
+}
+__device__ __forceinline__ void unpin_line(const DevCtx& c, u32 line, u32 n) {
+  atomicAdd(&c.tags[line], (u64)0 - (u64)n * PIN_ONE);
+}
+
+// ======================================================================= K2: SQ submit
+
+__device__ __forceinline__ u32 sq_slot_index(const DevCtx& c, u32 q, u64 v) { return q * c.sq_depth + (u32)(v & (c.sq_depth - 1)); }
+
+// Doorbell protocol (attempt_sqdb, nvme_queue.py:293-311): whoever wins the doorbell lock flips
+// the contiguous UPDATED run after the published doorbell to ISSUED (32 lanes per pass) and
+// publishes once; everyone loops until the doorbell passed `target`.
+__device__ bool ring_doorbell_until(const DevCtx& c, u32 q, u64 target, u32 who) {
+  const u32 lane = lane_id();
+  SqWords* s = &c.sqw[q];
+  const u32 D = c.sq_depth;
+  Spin sp;
+  while (true) {
+    const u64 db = ld_acquire(&s->db);
+    if (db >= target) return true;
+    int got = 0;
+    if (lane == 0) got = atom_cas_acquire(&s->db_lock, 0u, 1u) == 0u;
+    got = __shfl_sync(FULL, got, 0);
+    if (got) {
+      const u64 old = ld_relaxed(&s->db);
+      u64 v = old;
+      while (true) {
+        const u64 vi = v + lane;
+        const u32 idx = sq_slot_index(c, q, vi);
+        bool upd = false;
+        if (vi < old + D) upd = ld_acquire(&c.sq_state[idx]) == SQ_UPDATED;
+        const u32 b = __ballot_sync(FULL, upd);
+        const u32 prefix = (~b) ? (u32)(__ffs(~b) - 1) : 32u;
+        if (lane < prefix) {
+          if (atom_cas_acqrel(&c.sq_state[idx], SQ_UPDATED, SQ_ISSUED) != SQ_UPDATED)
+            set_error(c, E_PROTOCOL, q, vi);
+          log_ev(c, who, M_NVME, A_SQE_ISSUED, q, vi & (D - 1), vi & (D - 1));
+        }
+        v += prefix;
+        if (prefix < 32) break;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        if (v > old) {
+          st_relaxed(&s->db_time, gtimer());
+          log_ev(c, who, M_NVME, A_DOORBELL, q, old, v, D);
+          st_release(&s->db, v);   // the doorbell is a release fence
+          atomicAdd(&c.stats[S_DOORBELLS], 1ull);
+        }
+        st_release(&s->db_lock, 0u);
+      }
+      __syncwarp();
+      continue;
+    }
+    if (!sp.again(c, 256, __LINE__ + 100000 * SPIN_FILE_ID)) return false;
+  }
+}
+
+// Warp-aggregated submission (submit_command/attempt_enqueue, nvme_queue.py:314-354).
+// Lanes with `has` place one command each.  Lanes targeting the same device elect a leader
+// (__match_any_sync) that reserves popc slots with a capacity-checked CAS on the SQ tail
+// (tail - head <= depth - 1, nvme_queue.py:131-144); partial grants leave the remainder pending
+// and the next round rotates to the following SQ; a full lap backs off until the service frees
+// entries.  Returns false only when the run is aborting.
+__device__ bool submit_warp(const DevCtx& c, bool has, u32 dev, u64 blk, u32 line, u32 kind, u32 op, u64 buf,
+                            u64 key, u32 who, u32 sq_start) {
+  const u32 lane = lane_id();
+  const u32 D = c.sq_depth, P = c.pairs_per_device;
+  u32 pending = __ballot_sync(FULL, has);
+  u32 rot = 0;
+  Spin sp;
+  while (pending) {
+    const bool mine = (pending >> lane) & 1u;
+    u32 grp = __match_any_sync(FULL, mine ? dev : 0xffffffffu);
+    if (!mine) grp = 0;
+    const u32 rank = __popc(grp & lanemask_lt());
+    const u32 n = __popc(grp);
+    u32 q = 0, m = 0;
+    u64 t = 0;
+    if (mine && rank == 0) {
+      for (u32 k = 0; k < P && m == 0; ++k) {
+        const u32 qq = dev * P + (sq_start + rot + k) % P;
+        SqWords* s = &c.sqw[qq];
+        u64 tt = ld_relaxed(&s->tail);
+        while (true) {
+          const u64 hh = ld_acquire(&s->head);
+          const u64 used = tt - hh;
+          if (used >= (u64)(D - 1)) break;
+          const u32 take = (u32)min((u64)n, (u64)(D - 1) - used);
+          const u64 prev = atomicCAS(&s->tail, tt, tt + take);
+          if (prev == tt) { q = qq; t = tt; m = take; break; }
+          tt = prev;
+        }
+        if (m == 0) atomicAdd(&c.stats[S_SQ_FULL], 1ull);
+      }
+      if (m) atomicAdd(&c.pw->outstanding, (u64)m);
+    }
+    const u32 leader = grp ? (u32)(__ffs(grp) - 1) : lane;
+    q = __shfl_sync(FULL, q, leader);
+    t = __shfl_sync(FULL, t, leader);
+    m = __shfl_sync(FULL, m, leader);
+    const bool got = mine && rank < m;
+    if (got) {
+      const u64 v = t + rank;
+      const u32 slot = (u32)(v & (D - 1));
+      const u32 idx = q * D + slot;
+      uint4* e = c.sqe + (u64)idx * 4;
+      const u64 prp = kind == K_RAW ? buf : (u64)(uintptr_t)line_ptr(c, line);
+      // 64 B NVMe SQE: CDW0 opcode|CID, NSID, PRP1 (dw6-7), SLBA (dw10-11), NLB (dw12, 0-based)
+      e[0] = make_uint4((op == OP_READ ? 0x02u : 0x01u) | (slot << 16), dev + 1, 0u, 0u);
+      e[1] = make_uint4(0u, 0u, (u32)prp, (u32)(prp >> 32));
+      e[2] = make_uint4(0u, 0u, (u32)blk, (u32)(blk >> 32));
+      e[3] = make_uint4(0u, 0u, 0u, 0u);
+      CmdCtx* x = &c.cmd[idx];
+      x->key = key;
+      x->vidx = v;
+      x->t_submit = gtimer();
+      x->line = kind == K_RAW ? NONE : line;
+      x->kind = kind;
+      x->buf = buf;
+      log_ev(c, who, M_NVME, A_ENQUEUE, q, slot, slot, op, dev, blk);
+      if (atom_cas_acqrel(&c.sq_state[idx], SQ_EMPTY, SQ_UPDATED) != SQ_EMPTY)
+        set_error(c, E_PROTOCOL, q, v);   // mark_updated on a non-EMPTY entry (nvme_queue.py:160-162)
+      log_ev(c, who, M_NVME, A_SQE_UPDATED, q, slot);
+    }
+    __syncwarp();
+    u32 lead_b = __ballot_sync(FULL, mine && rank == 0 && m > 0);
+    while (lead_b) {
+      const int L = __ffs(lead_b) - 1;
+      lead_b &= lead_b - 1;
+      const u32 qL = __shfl_sync(FULL, q, L);
+      const u64 endL = __shfl_sync(FULL, t + m, L);
+      if (!ring_doorbell_until(c, qL, endL, who)) return false;
+    }
+    const u32 gb = __ballot_sync(FULL, got);
+    if (lane == 0 && gb) atomicAdd(&c.stats[S_ENQUEUES], (u64)__popc(gb));
+    pending &= ~gb;
+    if (pending && !gb) {
+      ++rot;
+      if (!sp.again(c, 1024, __LINE__ + 100000 * SPIN_FILE_ID)) return false;
+    }
+  }
+  return true;
+}
+
+// ======================================================================= user-side verbs
+// (AgileApi, gpu_api.py:139-278; paper Listing 1 naming: prefetch / asyncRead / wait)
+
+struct Req {        // per-lane result of an access
+  u32 line;
+  int kind;         // R_HIT / R_FILLING / R_MISS / R_NONE
+  u64 word;
+  u64 victim;       // key evicted by this miss (evict_reset) or ~0
+};
+
+// Warp-collective cache access.  Lanes with the same key coalesce (__match_any_sync, lowest lane
+// leads: warp_coalesce, gpu_api.py:40-54).  pin: every requesting lane holds one pin on the
+// resulting line until it has consumed it (async_read); !pin: prefetch semantics.
+// count_followers_as_attach: async_read keeps one outcome per caller (hit/miss/attach).
+__device__ Req access_warp(const DevCtx& c, bool active, u64 key, bool pin, u32 who, u32 sq_start,
+                           bool drop_followers) {
+  const u32 lane = lane_id();
+  Req r;
+  r.line = NONE; r.kind = R_NONE; r.word = 0; r.victim = ~0ull;
+  if (active) {   // AgileApi._check_block (gpu_api.py:328-332): OutOfRange before the cache is touched
+    const u32 dv = key_dev(key);
+    if (dv >= c.num_devices || key_blk(key) >= c.store_blocks[dv]) {
+      set_error(c, E_OUT_OF_RANGE, dv, key_blk(key));
+      active = false;
+    }
+  }
+  u32 grp = __match_any_sync(FULL, active ? key : ~0ull);
+  if (!active) grp = 0;
+  const bool leader = active && (grp & lanemask_lt()) == 0;
+  const u32 gsize = __popc(grp);
+  const u32 lead_lane = grp ? (u32)(__ffs(grp) - 1) : lane;
+  u32 todo = __ballot_sync(FULL, leader);
+  u32 hits = 0, attaches = 0, misses = 0;
+  Spin sp;
+  while (true) {
+    // lock-free probe for all unresolved leaders
+    const bool want = (todo >> lane) & 1u;
+    u32 l; u64 w;
+    probe_lanes(c, want, key, l, w);
+    bool resolved = false;
+    if (want && l != NONE) {
+      u64 pw = w;
+      if (pin) pw = pin_line(c, l, key, gsize);
+      if (pw) {
+        r.line = l;
+        r.word = pw;
+        r.kind = tw_state(pw) == ST_BUSY ? R_FILLING : R_HIT;
+        if (r.kind == R_HIT && !tw_ref(pw)) atomicOr(&c.tags[l], REF_BIT);   // on_hit
+        resolved = true;
+      }
+    }
+    todo &= ~__ballot_sync(FULL, resolved);
+    // misses: lane-parallel claims under per-set locks (W <= 32); one key at a time otherwise
+    u32 retry = 0;
+    u32 mb = todo;
+    bool need_submit = false;
+    if (c.ways <= 32 && mb) {
+      u32 cl = NONE; u64 cw = 0, vk = ~0ull;
+      const bool w = (mb >> lane) & 1u;
+      const int kind = claim_lanes(c, w, key, pin ? gsize : 0u, who, cl, cw, vk);
+      if (w) {
+        if (kind == R_RETRY || kind == R_NONE) retry |= 1u;
+        else { r.line = cl; r.word = cw; r.kind = kind; r.victim = vk; need_submit = kind == R_MISS; }
+      }
+      mb = 0;
+    }
+    while (mb) {
+      const int src = __ffs(mb) - 1;
+      mb &= mb - 1;
+      const u64 k = __shfl_sync(FULL, key, src);
+      const u32 pn = pin ? __shfl_sync(FULL, gsize, src) : 0u;
+      u32 cl; u64 cw, vk;
+      const int kind = claim_key_warp(c, k, pn, __shfl_sync(FULL, who, src), cl, cw, vk);
+      if (lane == (u32)src) {
+        if (kind == R_RETRY) retry |= 1u;
+        else { r.line = cl; r.word = cw; r.kind = kind; r.victim = vk; need_submit = kind == R_MISS; }
+      }
+    }
+    const u32 rb = __ballot_sync(FULL, retry != 0);
+    todo = rb;
+    // submit fills (warp-aggregated)
+    const u32 dev = key_dev(key);
+    if (!submit_warp(c, need_submit, dev, key_blk(key), r.line, K_FILL, OP_READ, 0, key, who, sq_start)) {
+      r.kind = R_NONE;
+      break;
+    }
+    if (!todo) break;
+    if (!sp.again(c, 2048, __LINE__ + 100000 * SPIN_FILE_ID)) break;
+  }
+  // accounting + trace
+  if (leader) {
+    if (r.kind == R_HIT) hits = 1;
+    else if (r.kind == R_MISS) misses = 1;
+    else if (r.kind == R_FILLING) attaches = 1;
+    if (r.kind == R_HIT) log_ev(c, who, M_CACHE, A_HIT, key_dev(key), key_blk(key));
+    if (r.kind == R_FILLING) log_ev(c, who, M_CACHE, A_ATTACH, r.line, 1);
+  }
+  // broadcast to followers
+  const u32 bl = __shfl_sync(FULL, r.line, lead_lane);
+  const int bk = __shfl_sync(FULL, r.kind, lead_lane);
+  const u64 bw = __shfl_sync(FULL, r.word, lead_lane);
+  if (active && !leader) {
+    if (drop_followers) {
+      r.line = NONE; r.kind = R_NONE;
+    } else {
+      r.line = bl; r.word = bw;
+      r.kind = (bk == R_HIT) ? R_HIT : (bk == R_NONE ? R_NONE : R_FILLING);
+      if (r.kind == R_HIT) hits = 1; else if (r.kind == R_FILLING) { attaches = 1; log_ev(c, who, M_CACHE, A_ATTACH, r.line, 1); }
+    }
+  }
+  const u32 h = __popc(__ballot_sync(FULL, hits != 0));
+  const u32 a = __popc(__ballot_sync(FULL, attaches != 0));
+  const u32 mm = __popc(__ballot_sync(FULL, misses != 0));
+  if (lane == 0) {
+    if (h) atomicAdd(&c.stats[S_HITS], (u64)h);
+    if (a) atomicAdd(&c.stats[S_ATTACHES], (u64)a);
+    if (mm) atomicAdd(&c.stats[S_MISSES], (u64)mm);
+  }
+  return r;
+}
+
+// Wait until each active lane's pinned line is READY, then copy the 4 KiB line into the lane's
+// destination buffer warp-cooperatively (the waiter drains itself: per-page state instead of
+// waiter lists, software_cache.py:563-570) and drop the pin.
+// One poll pass: every active lane whose pinned line is READY gets its 4 KiB line copied into
+// its destination buffer warp-cooperatively (the waiter drains itself: per-page state instead of
+// waiter lists, software_cache.py:563-570) and drops its pin.  Returns the mask of lanes served.
+__device__ u32 try_copy_warp(const DevCtx& c, bool active, u32 line, u64 key, uint4* dst) {
+  const u32 lane = lane_id();
+  bool ready = false;
+  if (active && line != NONE) {
+    const u64 w = ld_acquire(&c.tags[line]);
+    if (!tw_live(w) || tw_key(w) != key) set_error(c, E_ILLEGAL_STATE, line, key);
+    ready = tw_state(w) == ST_READY || tw_state(w) == ST_MODIFIED;
+  }
+  const u32 rb = __ballot_sync(FULL, ready);
+  if (!rb) return 0;
+  __syncwarp();
+  u32 todo = rb;
+  while (todo) {
+    const int l0 = __ffs(todo) - 1;
+    todo &= todo - 1;
+    const uint4* src = reinterpret_cast<const uint4*>(line_ptr(c, __shfl_sync(FULL, line, l0)));
+    uint4* d = reinterpret_cast<uint4*>(__shfl_sync(FULL, (u64)(uintptr_t)dst, l0));
+    uint4 v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = __ldcg(src + lane + 32 * k);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) d[lane + 32 * k] = v[k];
+  }
+  __syncwarp();
+  if ((rb >> lane) & 1u) unpin_line(c, line, 1);
+  return rb;
+}
+
+// Wait until every active lane's pinned line is READY and copied (AgileApi.wait, gpu_api.py:233-248:
+// nothing is held while waiting but the page's own pin).
+__device__ bool wait_copy_warp(const DevCtx& c, bool active, u32 line, u64 key, uint4* dst) {
+  const u32 lane = lane_id();
+  u32 pending = __ballot_sync(FULL, active && line != NONE);
+  Spin sp;
+  bool ok = true;
+  while (pending) {
+    const u32 rb = try_copy_warp(c, (pending >> lane) & 1u, line, key, dst);
+    pending &= ~rb;
+    if (pending && !rb) {
+      if (!sp.again(c, 1024, __LINE__ + 100000 * SPIN_FILE_ID)) { ok = false; break; }
+    }
+  }
+  // abort path: release the pins we still hold so the cache stays consistent
+  if ((pending >> lane) & 1u) unpin_line(c, line, 1);
+  return ok;
+}
+
+// Wait (without pinning) until the line holds `key` READY.  Returns false if the line was
+// reassigned meanwhile (caller re-accesses).
+__device__ __forceinline__ bool wait_ready_lane(const DevCtx& c, u32 line, u64 key, Spin& sp, bool& alive) {
+  const u64 w = ld_acquire(&c.tags[line]);
+  if (!tw_live(w) || tw_key(w) != key) { alive = false; return false; }
+  alive = true;
+  return tw_state(w) == ST_READY || tw_state(w) == ST_MODIFIED;
+}
+
+// ======================================================================= K3: completion service
+
+__device__ __forceinline__ void advance_head(const DevCtx& c, u32 q, u32 who) {
+  SqWords* s = &c.sqw[q];
+  const u32 D = c.sq_depth;
+  u64 h = ld_acquire(&s->head);
+  bool moved = false;
+  while (true) {
+    const u64 dv = ld_acquire(&c.sq_done_v[q * D + (u32)(h & (D - 1))]);
+    if (dv != h + 1) break;
+    const u64 prev = atomicCAS(&s->head, h, h + 1);
+    if (prev == h) { h = h + 1; moved = true; }
+    else h = prev;
+  }
+  if (moved) log_ev(c, who, M_NVME, A_HEAD, q, h);
+}
+
+// One window pass over a CQ (cq_polling, agile_service.py:147-171 + process_cqe 173-199).
+__device__ u32 cq_poll(const DevCtx& c, u32 cq, u32 who) {
+  const u32 lane = lane_id();
+  CqWords* cw = &c.cqw[cq];
+  int got = 0;
+  if (lane == 0) got = atom_cas_acquire(&cw->claim, 0u, 1u) == 0u;
+  got = __shfl_sync(FULL, got, 0);
+  if (!got) return 0;
+  const u64 offset = ld_relaxed(&cw->poll_offset);
+  u32 mask = ld_relaxed(&cw->poll_mask);
+  const u32 window = c.cq_window;
+  const u32 Dq = c.cq_depth;
+  const u32 Ds = c.sq_depth;
+  bool valid = false;
+  u32 sq = 0, slot = 0;
+  u64 v = offset + lane;
+  if (lane < window && !((mask >> lane) & 1u)) {
+    const u64 w = ld_acquire(reinterpret_cast<const u64*>(c.cqe + (u64)cq * Dq + (u32)(v & (Dq - 1))) + 1);
+    const u32 phase = (u32)(w >> 48) & 1u;
+    const u32 expect = 1u - (u32)((v / Dq) & 1u);   // lap 0 writes 1 (nvme_queue.py:262-264)
+    if (phase == expect) {
+      valid = true;
+      sq = (u32)(w >> 16) & 0xffffu;
+      slot = (u32)(w >> 32) & 0xffffu;   // CID == SQE slot
+    }
+  }
+  u64 lat = 0;
+  if (valid) {
+    const u32 idx = sq * Ds + slot;
+    if (sq >= c.num_qp || slot >= Ds) { set_error(c, E_UNKNOWN_CID, cq, v); valid = false; }
+    else {
+      const CmdCtx x = c.cmd[idx];
+      // release the SQE first so stuck producers can move (agile_service.py:188-195)
+      if (atom_cas_acqrel(&c.sq_state[idx], SQ_ISSUED, SQ_EMPTY) != SQ_ISSUED)
+        set_error(c, E_UNKNOWN_CID, sq, slot);
+      log_ev(c, who, M_NVME, A_SQE_RELEASE, sq, slot, slot);
+      log_ev(c, who, M_SVC, A_CQE_PROCESS, cq, v, slot, sq);
+      atomicExch(&c.sq_done_v[idx], x.vidx + 1);
+      if (x.line != NONE && (x.kind == K_FILL || x.kind == K_WB_KEEP)) {
+        // BUSY -> READY: one release-add on the state field preserves ref/pins/version
+        const u64 old = atom_add_release(&c.tags[x.line], 1ull << ST_SHIFT);
+        if (tw_state(old) != ST_BUSY) set_error(c, E_ILLEGAL_STATE, x.line, old);
+        log_state(c, who, x.line, ST_BUSY, ST_READY, x.key);
+      }
+      lat = gtimer() - x.t_submit;
+      fence_sc();
+    }
+  }
+  __syncwarp();
+  // head advance: one leader per SQ among completed lanes
+  u32 grp = __match_any_sync(FULL, valid ? sq : 0xffffffffu);
+  if (valid && (grp & lanemask_lt()) == 0) advance_head(c, sq, who);
+  const u32 vb = __ballot_sync(FULL, valid);
+  mask |= vb;
+  // stats (warp-aggregated)
+  u64 lsum = lat;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) lsum += __shfl_xor_sync(FULL, lsum, o);
+  const u32 k = __popc(vb);
+  const u32 fullw = window == 32 ? FULL : ((1u << window) - 1u);
+  if (lane == 0) {
+    if (k) {
+      atomicAdd(&c.stats[S_COMPLETIONS], (u64)k);
+      atomicAdd(&c.stats[S_BARRIER_COUNT], (u64)k);
+      atomicAdd(&c.stats[S_BARRIER_NS], lsum);
+    }
+    u64 off = offset;
+    if (mask == fullw) {
+      log_ev(c, who, M_SVC, A_WINDOW_RING, cq, off, off + window);
+      st_release(&cw->host_db, off + window);   // ring only full windows
+      atomicAdd(&c.stats[S_WINDOWS], 1ull);
+      off += window;
+      mask = 0;
+    }
+    st_relaxed(&cw->poll_offset, off);
+    st_relaxed(&cw->poll_mask, mask);
+    if (k) atom_add_release(&c.pw->outstanding, (u64)0 - (u64)k);
+    st_release(&cw->claim, 0u);
+  }
+  __syncwarp();
+  return k;
+}
+
+__device__ void drain_partial_windows(const DevCtx& c, u32 who) {
+  // _drain_partial_windows, agile_service.py:224-236 (lane-parallel over CQs)
+  for (u32 cq0 = 0; cq0 < c.num_qp; cq0 += 32) {
+    const u32 cq = cq0 + lane_id();
+    if (cq < c.num_qp) {
+      CqWords* cw = &c.cqw[cq];
+      const u32 mask = ld_relaxed(&cw->poll_mask);
+      if (mask) {
+        const u32 k = (u32)(__ffs(~mask) - 1);
+        if (mask != ((k == 32) ? FULL : ((1u << k) - 1u))) set_error(c, E_PROTOCOL, cq, mask);
+        const u64 off = ld_relaxed(&cw->poll_offset);
+        log_ev(c, who, M_SVC, A_DRAIN_RING, cq, off, off + k);
+        st_release(&cw->host_db, off + k);
+        st_relaxed(&cw->poll_offset, off + k);
+        st_relaxed(&cw->poll_mask, 0u);
+        atomicAdd(&c.stats[S_DRAIN_ENTRIES], (u64)k);
+      }
+    }
+  }
+}
+
+__device__ void service_main(const DevCtx& c, const Launch& L, u32 sw) {
+  const u32 who = WHO_SVC | sw;
+  const u32 n = c.num_qp;
+  const u32 S = c.service_warps;
+  if (sw == 0 && lane_id() == 0) log_ev(c, who, M_SVC, A_START, S);
+  u32 pos = sw;
+  u32 idle = c.poll_ns;
+  u32 sweep = 0, since = 0;
+  const u32 per_sweep = (n + S - 1) / S;
+  while (true) {
+    const u32 got = cq_poll(c, pos % n, who);
+    pos += S;
+    sweep += got;
+    bool stop = false;
+    if (++since >= per_sweep) {
+      if (lane_id() == 0) {
+        const bool users = ld_acquire(&c.run->users_done) >= L.n_user_ctas;
+        const u64 out = ld_acquire(&c.pw->outstanding);
+        stop = (users && out == 0) || aborted(c);
+        if (users && atomicCAS(&c.run->stop_logged, 0u, 1u) == 0u) log_ev(c, who, M_SVC, A_STOP);
+      }
+      stop = __shfl_sync(FULL, (int)stop, 0) != 0;
+      if (stop) break;
+      if (sweep == 0) {
+        nap(idle);
+        idle = min(idle * 2, c.idle_max_ns);
+      } else {
+        idle = c.poll_ns;
+      }
+      sweep = 0;
+      since = 0;
+    }
+  }
+  // the last warp out rings residual partial windows (agile_service.py:141-145)
+  u32 order = 0;
+  if (lane_id() == 0) order = atomicAdd(&c.run->svc_exited, 1u);
+  order = __shfl_sync(FULL, order, 0);
+  if (order == S - 1) {
+    drain_partial_windows(c, who);
+    __syncwarp();
+    if (lane_id() == 0) st_release(&c.run->engine_stop, 1u);
+  }
+}
+
+// ======================================================================= K4: device engine
+
+__device__ __forceinline__ u64 splitmix64(u64 x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+// LatencyModel.service_ns (ssd_model.py:45-53) for draw number `seq` of device `dev`
+__device__ __forceinline__ u64 model_service_ns(const DevCtx& c, u32 op, u32 dev, u64 seq) {
+  const u64 base = op == OP_READ ? c.model.read_ns : c.model.write_ns;
+  if (c.model.jitter == 0 || c.model.jitter_ns == 0) return base;
+  const u64 r = splitmix64(c.model.seed ^ ((u64)dev << 48) ^ seq);
+  if (c.model.jitter == 1) return base + r % c.model.jitter_ns;
+  const double u = ((r >> 11) + 0.5) * (1.0 / 9007199254740992.0);
+  return base + (u64)(-log(u) * (double)c.model.jitter_ns);
+}
+
+// FIFO channel dispatch (_dispatch/_start/_free_channel, ssd_model.py:168-186) for every lane in
+// `mask` whose command targets `dev`, in lane order: start at the earliest free channel no sooner
+// than arrival; the channel is held for occupancy_ns.  One lock hold per (warp pass, device);
+// channel free-times live in registers (lane i holds channels i, i+32, ...).
+constexpr u32 kMaxChanPerLane = 8;   // parallelism <= 256
+__device__ void model_schedule_batch(const DevCtx& c, u32 dev, u32 mask, u32 op, u64 arrival, u64& due) {
+  const u32 lane = lane_id();
+  const u32 P = c.model.parallelism;
+  const u32 n = __popc(mask);
+  int ok = 1;
+  u64 seq0 = 0;
+  if (lane == 0) {
+    Spin sp;
+    while (atom_cas_acquire(&c.dev_lock[dev], 0u, 1u) != 0u)
+      if (!sp.again(c, 128, __LINE__ + 100000 * SPIN_FILE_ID)) { ok = 0; break; }
+    if (ok && c.model.jitter && c.model.jitter_ns) seq0 = atomicAdd(&c.dev_seq[dev], (u64)n);
+  }
+  ok = __shfl_sync(FULL, ok, 0);
+  seq0 = __shfl_sync(FULL, seq0, 0);
+  if (!ok) { if ((mask >> lane) & 1u) due = 0; return; }
+  u64* ch = c.chan_free + (u64)dev * P;
+  u64 cf[kMaxChanPerLane];
+#pragma unroll
+  for (u32 k = 0; k < kMaxChanPerLane; ++k) {
+    const u32 i = lane + 32 * k;
+    cf[k] = i < P ? ld_relaxed(&ch[i]) : ~0ull;
+  }
+  u32 todo = mask;
+  u32 rank = 0;
+  while (todo) {
+    const int l = __ffs(todo) - 1;
+    todo &= todo - 1;
+    const u64 arr = __shfl_sync(FULL, arrival, l);
+    const u32 opl = __shfl_sync(FULL, op, l);
+    const u64 svc = model_service_ns(c, opl, dev, seq0 + rank);
+    ++rank;
+    // warp argmin over channel free-times (ties -> lowest channel index)
+    u64 best = ~0ull;
+    u32 bi = 0;
+#pragma unroll
+    for (u32 k = 0; k < kMaxChanPerLane; ++k) {
+      if (cf[k] < best) { best = cf[k]; bi = lane + 32 * k; }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const u64 ob = __shfl_xor_sync(FULL, best, o);
+      const u32 oi = __shfl_xor_sync(FULL, bi, o);
+      if (ob < best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+    }
+    const u64 start = max(arr, best);
+    const u64 occ = c.model.occupancy_ns ? c.model.occupancy_ns : svc;
+#pragma unroll
+    for (u32 k = 0; k < kMaxChanPerLane; ++k)
+      if (lane + 32 * k == bi) cf[k] = start + occ;
+    if (lane == (u32)l) due = start + svc;
+  }
+#pragma unroll
+  for (u32 k = 0; k < kMaxChanPerLane; ++k) {
+    const u32 i = lane + 32 * k;
+    if (i < P) st_relaxed(&ch[i], cf[k]);
+  }
+  __syncwarp();
+  if (lane == 0) st_release(&c.dev_lock[dev], 0u);
+  __syncwarp();
+}
+
+// lane holding the smallest sequence number among lanes with `cand` (-1 if none)
+__device__ __forceinline__ int oldest_lane(bool cand, u32 seq) {
+  u32 best = cand ? seq : 0xffffffffu;
+  int bl = cand ? (int)lane_id() : 32;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const u32 ob = __shfl_xor_sync(FULL, best, o);
+    const int ol = __shfl_xor_sync(FULL, bl, o);
+    if (ob < best || (ob == best && ol < bl)) { best = ob; bl = ol; }
+  }
+  return bl < 32 ? bl : -1;
+}
+
+__device__ void engine_main(const DevCtx& c, u32 ew) {
+  const u32 lane = lane_id();
+  const u32 E = c.engine_warps;
+  const u32 Ds = c.sq_depth, Dq = c.cq_depth;
+  const u32 nq = c.num_qp > ew ? (c.num_qp - ew + E - 1) / E : 0;   // owned QPs: ew, ew+E, ...
+  // one in-service command per lane: fetched (pv), data moved (pcp), completion due at pdue
+  bool pv = false, pcp = false, plogged = false, pstalled = false;
+  u32 pq = 0, pslot = 0, pop = 0, pdev = 0;
+  u64 pdue = 0, pblk = 0, prp = 0;
+  u32 rr = 0, pass = 0, seq = 0, pseq = 0;
+  u32 idle = 32;
+  u64 bytes_r = 0, bytes_w = 0;
+  while (true) {
+    bool did = false;
+    const u64 now = gtimer();
+    // ---- post due completions (device_post / stall, nvme_queue.py:266-279, ssd_model.py:200-206)
+    const bool due = pv && pcp && pdue <= now;
+    if (__ballot_sync(FULL, due)) {
+      if (due && !plogged) {
+        // the completion is reported at its model time (the bytes moved earlier)
+        log_ev(c, WHO_DEV | pdev, M_SSD, A_COMPLETE, pdev, pq, pslot, pop, pblk);
+        if (pop == OP_READ) bytes_r += kBlockBytes; else bytes_w += kBlockBytes;
+        plogged = true;
+      }
+      u32 grp = __match_any_sync(FULL, due ? pq : 0xffffffffu);
+      if (!due) grp = 0;
+      const u32 rank = __popc(grp & lanemask_lt());
+      const u32 n = __popc(grp);
+      u64 tail = 0;
+      u32 take = 0;
+      if (due && rank == 0) {
+        CqWords* cw = &c.cqw[pq];
+        tail = cw->dev_tail;
+        const u64 hdb = ld_acquire(&cw->host_db);
+        const u64 room = (u64)Dq - (tail - hdb);
+        take = (u32)min((u64)n, room);
+        cw->dev_tail = tail + take;
+      }
+      const u32 leader = grp ? (u32)(__ffs(grp) - 1) : lane;
+      tail = __shfl_sync(FULL, tail, leader);
+      take = __shfl_sync(FULL, take, leader);
+      if (due) {
+        if (rank < take) {
+          const u64 v = tail + rank;
+          u64* cqe = reinterpret_cast<u64*>(c.cqe + (u64)pq * Dq + (u32)(v & (Dq - 1)));
+          const u64 phase = 1ull - ((v / Dq) & 1ull);
+          const u64 w1 = (u64)pq << 16 | (u64)pslot << 32 | phase << 48;   // SQID | CID | P
+          cqe[0] = 0ull;
+          st_release(cqe + 1, w1);
+          log_ev(c, WHO_DEV | pdev, M_SSD, A_CQE_POST, pq, v, pslot, pq);
+          pv = false;
+          did = true;
+        } else if (!pstalled) {
+          log_ev(c, WHO_DEV | pdev, M_SSD, A_CQE_STALL, pq, pslot, pq);
+          atomicAdd(&c.stats[S_CQE_STALLS], 1ull);
+          pstalled = true;
+        }
+      }
+    }
+    // ---- move the bytes of up to two fetched commands (two 4 KiB pages in flight per pass),
+    //      interleaved with posting so completions are never held behind a long copy batch
+    const u32 tocopy = __ballot_sync(FULL, pv && !pcp);
+    if (tocopy) {
+      did = true;
+      // oldest-fetched first (no lane starves behind newly fetched commands)
+      const int l0 = oldest_lane(pv && !pcp, pseq);
+      const int l1 = oldest_lane(pv && !pcp && (int)lane != l0, pseq);
+      const int s1l = l1 < 0 ? l0 : l1;
+      const u32 op0 = __shfl_sync(FULL, pop, l0), op1 = __shfl_sync(FULL, pop, s1l);
+      const u32 d0 = __shfl_sync(FULL, pdev, l0), d1 = __shfl_sync(FULL, pdev, s1l);
+      const u64 b0 = __shfl_sync(FULL, pblk, l0), b1 = __shfl_sync(FULL, pblk, s1l);
+      const u64 p0 = __shfl_sync(FULL, prp, l0), p1 = __shfl_sync(FULL, prp, s1l);
+      const uint4* s0 = op0 == OP_READ ? reinterpret_cast<const uint4*>(c.store[d0] + (b0 << kBlockShift))
+                                       : reinterpret_cast<const uint4*>(p0);
+      uint4* t0 = op0 == OP_READ ? reinterpret_cast<uint4*>(p0)
+                                 : reinterpret_cast<uint4*>(c.store_w[d0] + (b0 << kBlockShift));
+      const uint4* s1 = op1 == OP_READ ? reinterpret_cast<const uint4*>(c.store[d1] + (b1 << kBlockShift))
+                                       : reinterpret_cast<const uint4*>(p1);
+      uint4* t1 = op1 == OP_READ ? reinterpret_cast<uint4*>(p1)
+                                 : reinterpret_cast<uint4*>(c.store_w[d1] + (b1 << kBlockShift));
+      uint4 v0[8], v1[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v0[k] = __ldcg(s0 + lane + 32 * k);
+      if (l1 >= 0) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v1[k] = __ldcg(s1 + lane + 32 * k);
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) __stcg(t0 + lane + 32 * k, v0[k]);
+      if (l1 >= 0) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) __stcg(t1 + lane + 32 * k, v1[k]);
+      }
+      __threadfence();   // page bytes visible before the CQE release of these commands
+      __syncwarp();
+      if ((int)lane == l0 || (int)lane == l1) pcp = true;
+    }
+    // ---- fetch newly published SQEs into free lanes (on_sq_doorbell/_fetch, ssd_model.py:138-166);
+    //      while bytes are still to be moved only every 4th pass pays the doorbell round trips
+    const u32 freeb = __ballot_sync(FULL, !pv);
+    u32 nfree = __popc(freeb);
+    bool newcmd = false;
+    ++pass;
+    const bool fetch_now = !__ballot_sync(FULL, pv && !pcp) || (pass & 3u) == 0;
+    if (nfree && nq && fetch_now) {
+      u32 assigned = 0;   // free lanes handed out in earlier chunks
+      for (u32 b0 = 0; b0 < nq && nfree; b0 += 32) {
+        const u32 k = b0 + lane;
+        const bool own = k < nq;
+        u32 q = 0;
+        u64 f = 0, avail = 0;
+        if (own) {
+          q = ew + ((k + rr) % nq) * E;
+          f = c.sqw[q].fetched;
+          avail = ld_acquire(&c.sqw[q].db) - f;
+        }
+        const u32 a = (u32)min(avail, (u64)32);
+        u32 pre = a;   // inclusive scan
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const u32 t = __shfl_up_sync(FULL, pre, o);
+          if (lane >= (u32)o) pre += t;
+        }
+        pre -= a;   // exclusive
+        const u32 take = pre >= nfree ? 0u : min(a, nfree - pre);
+        if (take) c.sqw[q].fetched = f + take;
+        u32 tot = take;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(FULL, tot, o);
+        if (!tot) continue;
+        // distribute to free lanes in order
+        const u32 fr = __popc(freeb & lanemask_lt());
+        const bool isfree = !pv;
+        for (u32 s = 0; s < 32; ++s) {
+          const u32 ps = __shfl_sync(FULL, pre, s);
+          const u32 ts = __shfl_sync(FULL, take, s);
+          const u32 qs = __shfl_sync(FULL, q, s);
+          const u64 fs = __shfl_sync(FULL, f, s);
+          if (isfree && !newcmd && ts && fr >= assigned + ps && fr < assigned + ps + ts) {
+            newcmd = true;
+            pq = qs;
+            const u64 v = fs + (fr - assigned - ps);
+            pslot = (u32)(v & (Ds - 1));
+          }
+        }
+        nfree -= tot;
+        assigned += tot;
+      }
+      rr++;
+    }
+    const u32 nb = __ballot_sync(FULL, newcmd);
+    if (nb) {
+      did = true;
+      u64 arrival = 0;
+      if (newcmd) {
+        const u32 idx = pq * Ds + pslot;
+        if (ld_acquire(&c.sq_state[idx]) != SQ_ISSUED) set_error(c, E_PROTOCOL, pq, pslot);   // ssd_model.py:158-160
+        const uint4* e = c.sqe + (u64)idx * 4;
+        const uint4 e0 = e[0], e1 = e[1], e2 = e[2];
+        pop = (e0.x & 0xffu) == 0x02u ? OP_READ : OP_WRITE;
+        pdev = e0.y - 1;
+        prp = (u64)e1.z | ((u64)e1.w << 32);
+        pblk = (u64)e2.z | ((u64)e2.w << 32);
+        if (pdev >= c.num_devices || pblk >= c.store_blocks[pdev]) {
+          set_error(c, E_OUT_OF_RANGE, pdev, pblk);
+          pdev = 0;
+          pblk = 0;
+        }
+        log_ev(c, WHO_DEV | pdev, M_SSD, A_FETCH, pdev, pq, pslot, pslot);
+        arrival = ld_relaxed(&c.sqw[pq].db_time) + c.model.fetch_ns;
+      }
+      // completion time: link mode = as soon as the bytes moved; model mode replays the channels
+      if (c.model.link_mode) {
+        if (newcmd) pdue = 0;
+      } else {
+        u32 t2 = nb;
+        while (t2) {
+          const int l = __ffs(t2) - 1;
+          const u32 dl = __shfl_sync(FULL, pdev, l);
+          const u32 same = __ballot_sync(FULL, newcmd && pdev == dl) & t2;
+          t2 &= ~same;
+          model_schedule_batch(c, dl, same, pop, arrival, pdue);
+        }
+      }
+      if (newcmd) {
+        pv = true; pcp = false; plogged = false; pstalled = false;
+        pseq = seq + __popc(nb & lanemask_lt());
+      }
+      seq += __popc(nb);
+      if (lane == 0) atomicAdd(&c.stats[S_FETCHED], (u64)__popc(nb));
+    }
+    // ---- exit once the service is done and nothing is in service
+    const bool busy = __ballot_sync(FULL, pv) != 0;
+    if (!busy) {
+      int stop = 0;
+      if (lane == 0) stop = ld_acquire(&c.run->engine_stop) != 0 || aborted(c);
+      if (__shfl_sync(FULL, stop, 0)) break;
+    } else if (aborted(c)) {
+      break;
+    }
+    if (!did) {
+      nap(idle);
+      idle = min(idle * 2, 512u);
+    } else {
+      idle = 32;
+    }
+  }
+  u64 br = bytes_r, bw = bytes_w;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) { br += __shfl_xor_sync(FULL, br, o); bw += __shfl_xor_sync(FULL, bw, o); }
+  if (lane == 0) {
+    if (br) atomicAdd(&c.stats[S_BYTES_READ], br);
+    if (bw) atomicAdd(&c.stats[S_BYTES_WRITTEN], bw);
+  }
+}
+
+// ======================================================================= launch skeleton
+// Role by arrival ticket: the first CTAs to actually start become the device engine and the
+// completion service, so every spinning user CTA waits only on CTAs that are already resident
+// (forward progress by construction; PAPER.md:811-819 draft: the service is the first block).
+struct Role {
+  int kind;   // 0 engine, 1 service, 2 user
+  u32 idx;
+};
+
+__device__ __forceinline__ Role take_role(const DevCtx& c) {
+  __shared__ u32 s_ticket;
+  if (threadIdx.x == 0) s_ticket = atomicAdd(&c.run->ticket, 1u);
+  __syncthreads();
+  u32 t = s_ticket;
+  Role r;
+  if (t < c.n_engine_ctas) { r.kind = 0; r.idx = t; return r; }
+  t -= c.n_engine_ctas;
+  if (t < c.n_service_ctas) { r.kind = 1; r.idx = t; return r; }
+  r.kind = 2;
+  r.idx = t - c.n_service_ctas;
+  return r;
+}
+
+__device__ __forceinline__ void user_done(const DevCtx& c) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(&c.run->users_done, 1u);
+  }
+}
+
+template <class Work>
+__global__ void __launch_bounds__(kCtaThreads) agile_kernel(DevCtx c, Launch L, Work work) {
+  const Role r = take_role(c);
+  const u32 warp = threadIdx.x >> 5;
+  if (r.kind == 0) {
+    const u32 ew = r.idx * kCtaWarps + warp;
+    if (ew < c.engine_warps) engine_main(c, ew);
+    return;
+  }
+  if (r.kind == 1) {
+    const u32 sw = r.idx * kCtaWarps + warp;
+    if (sw < c.service_warps) service_main(c, L, sw);
+    return;
+  }
+  work.run(c, r.idx, L.n_user_ctas);
+  user_done(c);
+}
+
+}  // namespace agile

@@ -1,0 +1,405 @@
+// agile_work.cuh — user-side workloads (the consumers of the device library):
+//   SeqWork        serialized async_read+wait stream (golden hit/miss/eviction parity)
+//   ReadsWork      CTC sync/async epochs (bench/ctc.py:27-111)            — K8
+//   LoopWork       closed-loop 4 KiB random reads (bench/bandwidth.py:20-68) — K9
+//   GatherWork     prefetch + array_get gather epochs (bench/sweeps.py:39-88)
+//   EmbBagWork     DLRM embedding-bag over cached rows                    — K5
+#pragma once
+#include "agile_core.cuh"
+#undef SPIN_FILE_ID
+#define SPIN_FILE_ID 2
+
+namespace agile {
+
+// grid barrier among user CTAs (the epoch Rendezvous, sim_core.py:139-159). All user CTAs are
+// co-resident by construction (the host sizes the grid from occupancy for these workloads).
+__device__ __forceinline__ bool user_grid_barrier(const DevCtx& c, u32 n_user_ctas) {
+  __syncthreads();
+  __shared__ int s_ok;
+  if (threadIdx.x == 0) {
+    s_ok = 1;
+    const u32 gen = ld_acquire(&c.run->bar_gen);
+    __threadfence();
+    if (atomicAdd(&c.run->bar_count, 1u) == n_user_ctas - 1) {
+      st_relaxed(&c.run->bar_count, 0u);
+      st_release(&c.run->bar_gen, gen + 1);
+    } else {
+      Spin sp;
+      while (ld_acquire(&c.run->bar_gen) == gen)
+        if (!sp.again(c, 512, __LINE__ + 100000 * SPIN_FILE_ID)) { s_ok = 0; break; }
+    }
+  }
+  __syncthreads();
+  return s_ok != 0;
+}
+
+// compute phase of the benchmarks: time-calibrated busy loop (Delay(compute_ns) of the reference)
+__device__ __forceinline__ void compute_spin(u64 ns) {
+  if (!ns) return;
+  const u64 t0 = gtimer();
+  while (gtimer() - t0 < ns) { }
+}
+
+__device__ __forceinline__ u32 user_who(u32 uidx) { return WHO_USER | (uidx * kCtaThreads + threadIdx.x); }
+
+// ------------------------------------------------------------------ SeqWork
+struct SeqWork {
+  const u32* dev;
+  const u64* blk;
+  long long n;
+  signed char* outcome;   // 0 hit, 1 miss, 2 attach
+  u64* victim;            // evicted key or ~0
+  uint4* pages;           // optional n * 4 KiB
+  uint4* scratch;         // 4 KiB
+  __device__ void run(const DevCtx& c, u32 uidx, u32 nusers) {
+    if (uidx != 0 || threadIdx.x >= 32) return;
+    const u32 lane = lane_id();
+    const u32 who = user_who(0) & ~31u;   // task "u0"
+    for (long long i = 0; i < n; ++i) {
+      if (aborted(c)) return;
+      const bool act = lane == 0;
+      const u64 key = make_key(dev[i], blk[i]);
+      if (act) log_ev(c, who, M_API, A_ASYNC_READ, dev[i], blk[i]);
+      const Req r = access_warp(c, act, key, true, who, 0, false);
+      if (act) {
+        outcome[i] = r.kind == R_HIT ? 0 : (r.kind == R_MISS ? 1 : 2);
+        victim[i] = r.victim;
+      }
+      uint4* dst = pages ? pages + i * 256 : scratch;
+      wait_copy_warp(c, act && r.kind != R_NONE, r.line, key, dst);
+    }
+  }
+};
+
+// ------------------------------------------------------------------ ReadsWork (CTC)
+struct ReadsWork {
+  const u64* keys;        // [epochs][tasks][reads] request keys
+  uint4* bufs;            // [tasks][2][reads] 4 KiB buffers
+  u64* digest;            // [tasks] xor of the first 8 bytes of every page read
+  u64* epoch_t;           // [epochs + 1] barrier timestamps
+  u32 tasks, reads, epochs, async_mode;
+  u64 compute_ns;
+  static constexpr int MAXR = 64;
+  __device__ void issue(const DevCtx& c, u32 task, bool act, u32 e, u32 set, u32* lines, u64* ks, u32 who, u32 sq_start) {
+    for (u32 i = 0; i < reads; ++i) {
+      const u64 key = act ? keys[((u64)e * tasks + task) * reads + i] : 0ull;
+      const Req r = access_warp(c, act, key, true, who, sq_start + i + e * reads, false);
+      lines[set * MAXR + i] = (act && r.kind != R_NONE) ? r.line : NONE;
+      ks[set * MAXR + i] = key;
+    }
+  }
+  __device__ void wait_set(const DevCtx& c, u32 task, bool act, u32 set, const u32* lines, const u64* ks, u64& dg) {
+    for (u32 i = 0; i < reads; ++i) {
+      uint4* dst = bufs + (((u64)task * 2 + set) * reads + i) * 256;
+      wait_copy_warp(c, act, lines[set * MAXR + i], ks[set * MAXR + i], dst);
+      if (act && lines[set * MAXR + i] != NONE) {
+        const uint2 w = *reinterpret_cast<const uint2*>(dst);
+        dg ^= (u64)w.x | ((u64)w.y << 32);
+      }
+    }
+  }
+  __device__ void run(const DevCtx& c, u32 uidx, u32 nusers) {
+    const u32 task = uidx * kCtaThreads + threadIdx.x;
+    const bool act = task < tasks;
+    const u32 who = user_who(uidx);
+    const u32 sq_start = uidx * kCtaWarps + (threadIdx.x >> 5);
+    u32 lines[2 * MAXR];
+    u64 ks[2 * MAXR];
+    u64 dg = 0;
+    if (uidx == 0 && threadIdx.x == 0) epoch_t[0] = gtimer();
+    if (!async_mode) {
+      for (u32 e = 0; e < epochs; ++e) {
+        issue(c, task, act, e, 0, lines, ks, who, sq_start);
+        wait_set(c, task, act, 0, lines, ks, dg);
+        // compute starts only after every task's data arrived (bench/ctc.py:80-83)
+        if (!user_grid_barrier(c, nusers)) return;
+        if (uidx == 0 && threadIdx.x == 0) epoch_t[e + 1] = gtimer();
+        compute_spin(compute_ns);
+      }
+    } else {
+      issue(c, task, act, 0, 0, lines, ks, who, sq_start);
+      for (u32 e = 0; e < epochs; ++e) {
+        const u32 cur = e & 1u;
+        // the next epoch's fetches ride under this epoch's compute (bench/ctc.py:47-70)
+        if (e + 1 < epochs) issue(c, task, act, e + 1, cur ^ 1u, lines, ks, who, sq_start);
+        wait_set(c, task, act, cur, lines, ks, dg);
+        if (!user_grid_barrier(c, nusers)) return;
+        if (uidx == 0 && threadIdx.x == 0) epoch_t[e + 1] = gtimer();
+        compute_spin(compute_ns);
+      }
+    }
+    if (act) digest[task] = dg;
+    // final timestamp after the last compute
+    if (!user_grid_barrier(c, nusers)) return;
+    if (uidx == 0 && threadIdx.x == 0) epoch_t[epochs] = gtimer();
+  }
+};
+
+// ------------------------------------------------------------------ LoopWork (IOPS)
+// Each requester keeps exactly one 4 KiB read outstanding; requester idx issues
+// dev = (idx + j) % d, blk = (j * conc + idx) % num_blocks (bench/bandwidth.py:32-33).
+struct LoopWork {
+  uint4* bufs;            // [conc] 4 KiB
+  unsigned long long* counters;   // [0] completions in window, [1] window start, [2] window end
+  u32 conc, ndev;
+  u64 num_blocks;
+  u64 warmup_ns, measure_ns;
+  u64 max_per_task;
+  __device__ void run(const DevCtx& c, u32 uidx, u32 nusers) {
+    const u32 idx = uidx * kCtaThreads + threadIdx.x;
+    const bool act = idx < conc;
+    const u32 who = user_who(uidx);
+    const u32 sq_start = uidx * kCtaWarps + (threadIdx.x >> 5);
+    if (threadIdx.x == 0) atomicCAS(&c.run->t_first, 0ull, gtimer());
+    __syncthreads();
+    const u64 t0 = ld_acquire(&c.run->t_first);
+    const u64 ws = t0 + warmup_ns, we = ws + measure_ns;
+    u32 inwin = 0;
+    uint4* dst = bufs + (u64)(act ? idx : 0) * 256;
+    // requesters progress independently: a lane issues its next read as soon as its previous
+    // one completed (no warp lockstep), so the in-flight population stays at `conc`
+    const u32 lane = lane_id();
+    bool outst = false;
+    u32 line = NONE;
+    u64 key = 0, j = 0;
+    Spin sp;
+    while (true) {
+      const bool issue = act && !outst && j < max_per_task && gtimer() < we;
+      const u32 ib = __ballot_sync(FULL, issue);
+      if (ib) {
+        const u32 dev = (idx + (u32)j) % ndev;
+        const u64 blk = (j * conc + idx) % num_blocks;
+        const u64 k = make_key(dev, blk);
+        const Req r = access_warp(c, issue, k, true, who, sq_start + (u32)__shfl_sync(FULL, j, __ffs(ib) - 1), false);
+        if (issue) {
+          ++j;
+          if (r.kind != R_NONE) { outst = true; line = r.line; key = k; }
+        }
+      }
+      const u32 done = try_copy_warp(c, outst, line, key, dst);
+      if ((done >> lane) & 1u) {
+        outst = false;
+        const u64 t = gtimer();
+        if (t >= ws && t < we) ++inwin;
+      }
+      const bool more = outst || (act && j < max_per_task && gtimer() < we);
+      if (!__any_sync(FULL, more)) break;
+      if (!ib && !done) {
+        if (!sp.again(c, 512, __LINE__ + 100000 * SPIN_FILE_ID)) break;
+      } else {
+        sp = Spin();
+      }
+    }
+    if (outst) unpin_line(c, line, 1);   // abort path only
+    u32 s = inwin;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
+    if (lane_id() == 0 && s) atomicAdd(&counters[0], (u64)s);
+    if (uidx == 0 && threadIdx.x == 0) { counters[1] = ws; counters[2] = we; }
+  }
+};
+
+// ------------------------------------------------------------------ GatherWork (queue/cache sweeps)
+// One warp = 32 tasks in lockstep (run_workload(..., warp_size=32)). Per epoch each task
+// prefetches its gather set (warp-coalesced) and then array_gets element 0 of every block.
+struct GatherWork {
+  const u64* keys;        // [tasks][epochs][gathers]
+  u32* values;            // [tasks][epochs][gathers] little-endian u32 read
+  u64* epoch_t;
+  u32 tasks, epochs, gathers, async_mode;
+  u64 compute_ns;
+  __device__ void prefetch_epoch(const DevCtx& c, bool act, u32 task, u32 e, u32 who, u32 sq_start) {
+    for (u32 g = 0; g < gathers; ++g) {
+      const u64 key = act ? keys[((u64)task * epochs + e) * gathers + g] : 0ull;
+      access_warp(c, act, key, false, who, sq_start + g + e * gathers, true);
+    }
+  }
+  __device__ void get_epoch(const DevCtx& c, bool act, u32 task, u32 e, u32 who, u32 sq_start) {
+    for (u32 g = 0; g < gathers; ++g) {
+      const u64 key = act ? keys[((u64)task * epochs + e) * gathers + g] : 0ull;
+      // array_get = read_range loop (software_cache.py:212-219): access, wait READY, read, validate
+      bool pend = act;
+      u32 val = 0;
+      Spin sp;
+      while (__any_sync(FULL, pend)) {
+        const Req r = access_warp(c, pend, key, true, who, sq_start, false);
+        bool done = false;
+        if (pend && r.kind != R_NONE) {
+          Spin s2;
+          while (true) {
+            const u64 w = ld_acquire(&c.tags[r.line]);
+            if (tw_state(w) == ST_READY || tw_state(w) == ST_MODIFIED) break;
+            if (!s2.again(c, 512, __LINE__ + 100000 * SPIN_FILE_ID)) break;
+          }
+          val = __ldcg(reinterpret_cast<const unsigned int*>(line_ptr(c, r.line)));
+          unpin_line(c, r.line, 1);
+          done = true;
+        }
+        if (done) pend = false;
+        if (aborted(c)) break;
+      }
+      if (act) values[((u64)task * epochs + e) * gathers + g] = val;
+    }
+  }
+  __device__ void run(const DevCtx& c, u32 uidx, u32 nusers) {
+    const u32 task = uidx * kCtaThreads + threadIdx.x;
+    const bool act = task < tasks;
+    const u32 who = user_who(uidx);
+    const u32 sq_start = task / 32;   // thread_idx % nsq start SQ per warp (nvme_queue.py:91-93)
+    if (uidx == 0 && threadIdx.x == 0) epoch_t[0] = gtimer();
+    if (async_mode) prefetch_epoch(c, act, task, 0, who, sq_start);
+    for (u32 e = 0; e < epochs; ++e) {
+      if (!async_mode) prefetch_epoch(c, act, task, e, who, sq_start);
+      else if (e + 1 < epochs) prefetch_epoch(c, act, task, e + 1, who, sq_start);
+      get_epoch(c, act, task, e, who, sq_start);
+      if (!user_grid_barrier(c, nusers)) return;
+      compute_spin(compute_ns);
+    }
+    if (!user_grid_barrier(c, nusers)) return;
+    if (uidx == 0 && threadIdx.x == 0) epoch_t[1] = gtimer();
+  }
+};
+
+// ------------------------------------------------------------------ EmbBagWork (K5)
+// pooled[b, t, :] = sum_l table_t[idx[b, t, l], :] over 4 KiB pages of 8 rows x 128 fp32.
+// One warp per bag: lanes 0..L-1 map their index to (page, row slot), the warp probes all L
+// pages with the batched ballot probe, misses are claimed/submitted warp-aggregated, then every
+// lane loads one float4 of each row (16 B/lane, 512 B coalesced per row) and sums in registers.
+// Hits are validated seqlock-style against the tag word after a fence (no pin atomics on the
+// hot path).  Async mode prefetches the warp's bag `pd` positions ahead before processing.
+struct EmbBagWork {
+  const long long* idx;        // [B][T][L]
+  const u64* table_key0;       // [T] key of the table's first page (dev << 36 | page)
+  const long long* table_rows; // [T]
+  float* out;                  // [B][T][D]
+  u64* lookups_miss;           // [2] lookups, miss-path lookups
+  u32 B, T, L, D;
+  u32 pd;                      // prefetch distance in bags (0 = sync)
+  u32 rows_per_page_shift;     // log2(4096 / (D*4))
+  u32 out_b_stride, out_t_stride;   // in floats
+  u32 nwarps_total;
+
+  __device__ __forceinline__ bool bag_keys(u32 bag, bool lane_act, u64& key, u32& off) const {
+    const u32 b = bag / T, t = bag % T;
+    if (!lane_act) return false;
+    long long r = idx[((u64)b * T + t) * L + lane_id()];
+    const long long rows = table_rows[t];
+    if (r < 0 || r >= rows) r = 0;   // invalid index -> row 0 (callers validate on host)
+    const u64 page = (u64)r >> rows_per_page_shift;
+    const u32 slot = (u32)r & ((1u << rows_per_page_shift) - 1u);
+    key = table_key0[t] + page;
+    off = slot * D * 4;
+    return true;
+  }
+
+  __device__ void run(const DevCtx& c, u32 uidx, u32 nusers) {
+    const u32 lane = lane_id();
+    const u32 gw = uidx * kCtaWarps + (threadIdx.x >> 5);
+    const u32 nw = nusers * kCtaWarps;
+    const u32 nbags = B * T;
+    const u32 who = user_who(uidx);
+    const bool lact = lane < L;
+    u32 misses_local = 0, lookups_local = 0;
+    // prologue prefetch
+    if (pd) {
+      for (u32 k = 0; k < pd; ++k) {
+        const u32 bag = gw + k * nw;
+        if (bag >= nbags) break;
+        u64 key = 0; u32 off = 0;
+        const bool a = bag_keys(bag, lact, key, off);
+        access_warp(c, a, key, false, who, gw, true);
+      }
+    }
+    for (u32 bag = gw; bag < nbags; bag += nw) {
+      if (aborted(c)) break;
+      if (pd) {
+        const u32 nb = bag + pd * nw;
+        if (nb < nbags) {
+          u64 key = 0; u32 off = 0;
+          const bool a = bag_keys(nb, lact, key, off);
+          access_warp(c, a, key, false, who, gw, true);
+        }
+      }
+      u64 key = 0; u32 off = 0;
+      const bool a = bag_keys(bag, lact, key, off);
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      // rows still to be summed (one per lane l < L); rows are validated individually so a
+      // page evicted under us only costs that row a retry
+      u32 pend = __ballot_sync(FULL, a);
+      bool first = true;
+      u32 line = NONE;
+      u64 word = 0;
+      Spin rsp;
+      while (pend) {
+        const bool mine = (pend >> lane) & 1u;
+        // 1. resolve pending lookups to READY lines (probe, then miss path / wait)
+        probe_lanes(c, mine, key, line, word);
+        bool ready = mine && line != NONE && (tw_state(word) == ST_READY || tw_state(word) == ST_MODIFIED);
+        if (ready && !tw_ref(word)) atomicOr(&c.tags[line], REF_BIT);
+        u32 need = __ballot_sync(FULL, mine && !ready);
+        if (need) {
+          if (first) misses_local += __popc(need);
+          Spin sp;
+          while (need) {
+            const bool nm = (need >> lane) & 1u;
+            bool have = nm && line != NONE;   // found BUSY by the probe
+            const Req r = access_warp(c, nm && !have, key, false, who, gw, false);
+            if (nm && !have && r.kind != R_NONE) { line = r.line; word = r.word; have = true; }
+            bool done = false;
+            if (nm && have) {
+              const u64 w = ld_acquire(&c.tags[line]);
+              if (tw_live(w) && tw_key(w) == key) {
+                if (tw_state(w) == ST_READY || tw_state(w) == ST_MODIFIED) { word = w; done = true; }
+              } else {
+                line = NONE;   // reassigned before we saw it READY: miss path again
+              }
+            }
+            need &= ~__ballot_sync(FULL, done);
+            if (need && !sp.again(c, 1024, __LINE__ + 100000 * SPIN_FILE_ID)) break;
+          }
+          if (aborted(c)) break;
+          fence_acq_rel();
+        }
+        first = false;
+        // 2. gather pending rows in chunks of 8: lane owns dims [4*lane, 4*lane+4)
+        const u64 rowaddr = mine ? (u64)(uintptr_t)(line_ptr(c, line) + off) : 0ull;
+        u32 okall = 0;
+        for (u32 l0 = 0; l0 < L; l0 += 8) {
+          const u32 cm = (pend >> l0) & 0xffu;
+          if (!cm) continue;
+          float4 v[8];
+#pragma unroll
+          for (u32 j = 0; j < 8; ++j) {
+            const u64 ra = __shfl_sync(FULL, rowaddr, (l0 + j) & 31);
+            v[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (((cm >> j) & 1u) && lane * 4 < D) v[j] = __ldcg(reinterpret_cast<const float4*>(ra) + lane);
+          }
+          // 3. seqlock validation of this chunk: the line kept its identity while we read it
+          fence_acq_rel();
+          bool bad = false;
+          if (mine && lane >= l0 && lane < l0 + 8) {
+            const u64 w2 = ld_relaxed(&c.tags[line]);
+            bad = ((w2 ^ word) & IDENT_MASK) != 0;
+          }
+          const u32 ok = cm & ~(__ballot_sync(FULL, bad) >> l0);
+#pragma unroll
+          for (u32 j = 0; j < 8; ++j) {
+            if ((ok >> j) & 1u) { acc.x += v[j].x; acc.y += v[j].y; acc.z += v[j].z; acc.w += v[j].w; }
+          }
+          okall |= ok << l0;
+        }
+        pend &= ~okall;
+        if (pend && !rsp.again(c, 256, __LINE__ + 100000 * SPIN_FILE_ID)) break;
+      }
+      lookups_local += L;
+      const u32 b = bag / T, t = bag % T;
+      if (lane * 4 < D) reinterpret_cast<float4*>(out + (u64)b * out_b_stride + (u64)t * out_t_stride)[lane] = acc;
+    }
+    if (lane == 0) {
+      atomicAdd(&lookups_miss[0], (u64)lookups_local);
+      atomicAdd(&lookups_miss[1], (u64)misses_local);
+    }
+  }
+};
+
+}  // namespace agile

@@ -1,0 +1,36 @@
+"""Benchmark-shape checks on the GPU: CTC overlap (criterion 4 analogue) and the device model's
+rate ceiling parallelism*block/latency (test_ssd_model.py:153-164) with linear device scaling
+(criterion 5, test_acceptance.py:167-191)."""
+
+import numpy as np
+import pytest
+
+from paper_2504_19365_b200.system import make_key
+
+pytestmark = pytest.mark.gpu
+
+
+def test_ctc_async_overlaps_compute(gpu_system):
+    # async needs SQ slots and cache lines for ~2x the per-epoch demand
+    s = gpu_system(cache_lines=8192, ways=32, blocks=1 << 16, pairs=16, sq_depth=256, cq_depth=256,
+                   emulation="model", engine_warps=8, warps=4)
+    T, R, E = 128, 4, 16
+    keys = make_key(np.zeros(E * T * R), np.arange(E * T * R)).reshape(E, T, R)
+    base = s.run_reads(keys, T, R, E, False, 0)["t_ns"]
+    comm = base / E
+    s.reset()
+    ts = s.run_reads(keys, T, R, E, False, int(comm))["t_ns"]
+    s.reset()
+    ta = s.run_reads(keys, T, R, E, True, int(comm))["t_ns"]
+    speed = ts / ta
+    assert speed > 1.3, (ts, ta, speed)
+
+
+@pytest.mark.parametrize("ndev", [1, 2])
+def test_model_mode_rate_ceiling_and_scaling(gpu_system, ndev):
+    s = gpu_system(num_devices=ndev, pairs=8, sq_depth=256, cq_depth=256, cache_lines=4096, ways=32,
+                   blocks=1 << 16, emulation="model", engine_warps=8, warps=4)
+    r = s.run_loop(64 * ndev, warmup_ns=2_000_000, measure_ns=20_000_000)
+    gbps = r["completions"] * 4096 / r["window_ns"]
+    ceiling = ndev * 16 * 4096 / 17712
+    assert ceiling * 0.93 <= gbps <= ceiling * 1.02, (gbps, ceiling)
