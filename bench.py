@@ -1,0 +1,422 @@
+#!/usr/bin/env python
+"""bench.py — headline benchmark of the B200 AGILE hot path.
+
+Metric (BASELINE.json): DLRM lookups/s (and 4 KB-page IOPS) with the async-vs-sync overlap
+speedup.  A "step" is one DLRM embedding-bag batch (B=2048 x 26 tables x pooling 20, dim 128,
+fp32) gathered through the HBM page cache from the host-pinned page store:
+  * N=1  -> BASELINE configs[1]: tables 4x the HBM cache on one B200.
+  * N>1  -> BASELINE configs[4]: tables sharded by table over N ranks (one process per GPU,
+            torchrun), each with its own cache / queue pairs / store shard, pooled embeddings
+            exchanged with one NCCL all_to_all_single per step.  Per-GPU work is fixed
+            (weak scaling).
+Timing: W warm-up steps, then K timed steps on the launching stream with CUDA events,
+barrier + synchronize on both sides, max over ranks.  Inputs (index batches) are resident in
+HBM; every step uses a distinct batch; the working set (16 GiB cache + 64 GiB store per GPU)
+is far larger than L2.
+`--impl reference`: the CPU port of the same path (oracle/agile_oracle.c) on all host
+threads, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+B, T, L, D = 2048, 26, 20, 128
+SEED = 20260417
+ALPHA = 1.05
+
+
+def _args():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    p.add_argument("--cache-gib", type=float, default=16.0)
+    p.add_argument("--table-mult", type=float, default=4.0)
+    p.add_argument("--prefetch", type=int, default=1)
+    p.add_argument("--no-scatter", action="store_true")
+    p.add_argument("--quick", action="store_true", help="skip e2e / sync / hit / cpu legs")
+    p.add_argument("--cpu-seconds", type=float, default=12.0)
+    return p.parse_args()
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            pk = json.load(fh)
+        return float(pk["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def _link_peak():
+    try:
+        with open(os.path.join(ROOT, "profiles", "link_probe_r01.json")) as fh:
+            return float(json.load(fh)["zero_copy_4k_gather_gbs"])
+    except Exception:
+        return 51.4
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (the recipe's clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.path = tempfile.mktemp(suffix=".csv")
+
+    def start(self):
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "100", "-i", str(self.gpu)], stdout=self.fh,
+                                         stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.fh.close()
+        sm, mx, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def _plan(args, world):
+    """Per-rank sizes: cache bytes and store bytes, capped by host RAM (pinned store)."""
+    cache_bytes = int(args.cache_gib * (1 << 30))
+    table_bytes = int(cache_bytes * args.table_mult)
+    try:
+        mem = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES")
+        local = int(os.environ.get("LOCAL_WORLD_SIZE", world))
+        cap = int(0.55 * mem / max(1, local))
+        if table_bytes > cap:
+            table_bytes = cap
+            cache_bytes = int(table_bytes / args.table_mult)
+    except (ValueError, OSError):
+        pass
+    return cache_bytes, table_bytes
+
+
+def run_reference(args):
+    """CPU port of the same path on host threads (rank 0 only); bounded per-step samples."""
+    rank = int(os.environ.get("RANK", 0))
+    if rank != 0:
+        return
+    import numpy as np
+    from paper_2504_19365_b200.bench.dlrm import table_rows, layout, make_batch
+    from oracle.cpu import CpuEmbeddingCache
+    world = args.gpus
+    cache_bytes, table_bytes = _plan(args, world)
+    rows = table_rows(table_bytes * world, D, T)
+    key0, pages = layout(rows, D)
+    threads = os.cpu_count() or 1
+    cache = CpuEmbeddingCache(cache_bytes // 4096 - (cache_bytes // 4096) % 32, 32, SEED)
+    bs = 128   # bounded sample: 128 samples x 26 tables x 20 per step
+    times = []
+    for step in range(args.warmup + args.steps):
+        idx = make_batch(SEED, step, rows, B, L, ALPHA, not args.no_scatter)[:bs]
+        t0 = time.perf_counter()
+        cache.embbag(idx, key0, rows, D, threads=threads)
+        dt = time.perf_counter() - t0
+        if step >= args.warmup:
+            times.append(dt)
+    per = bs * T * L
+    value = per * len(times) / sum(times)
+    line = {"impl": "reference", "metric": "dlrm_lookups_per_s", "value": value, "unit": "lookups/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "dlrm_embbag", "tables": T, "dim": D, "batch": B, "pooling": L,
+                       "cache_bytes_per_gpu": cache_bytes, "table_bytes_per_gpu": table_bytes,
+                       "zipf": ALPHA, "scatter": not args.no_scatter},
+            "cpu_baseline": {"value": value, "unit": "lookups/s", "cores": threads, "kind": "port",
+                             "sample": f"{bs} samples x {T} tables x {L} lookups per step; set-assoc clock cache "
+                                       f"of {cache_bytes >> 30} GiB over {pages} synthetic pages"},
+            "e2e": {"value": value, "unit": "lookups/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = _args()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2504_19365_b200 import AgileSystem, SystemConfig
+    from paper_2504_19365_b200.bench.dlrm import table_rows, make_batch, shard_tables, build_shard
+
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    assert world == args.gpus or "RANK" not in os.environ, "--gpus must match WORLD_SIZE"
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cache_bytes, table_bytes = _plan(args, world)
+    rows_all = table_rows(table_bytes * world, D, T)
+    groups, owner = shard_tables(rows_all, world)
+    shard = build_shard(rows_all, groups[rank], D)
+    Tg = len(shard.tables)
+
+    cfg = SystemConfig()
+    cfg.seed = SEED
+    cfg.device.num_blocks = max(1, shard.pages)
+    cfg.device.emulation = "link"            # host-pinned page store at host-link speed
+    cfg.cache.bytes = cache_bytes
+    cfg.cache.ways = 32
+    cfg.queues.pairs_per_device = 128        # paper defaults: 128 QPs x 256 (config.py:49-51)
+    cfg.queues.sq_depth = 256
+    cfg.queues.cq_depth = 256
+    cfg.engine.warps = 64
+    cfg.service.warps = 16
+    cfg.service.idle_max_ns = 1600
+    cfg.debug_locks = False
+    t0 = time.time()
+    system = AgileSystem(cfg, device=local)
+    system.fill_store(0, SEED, kind="f32")
+    setup_s = time.time() - t0
+
+    scatter = not args.no_scatter
+    nb = args.warmup + args.steps
+    n_sync = max(2, args.steps // 2)
+    n_e2e = args.steps
+    host_batches = [make_batch(SEED, s, rows_all, B, L, ALPHA, scatter, shard.tables)
+                    for s in range(nb + n_sync + n_e2e + 1)]
+    dbat = [torch.from_numpy(x).to(dev) for x in host_batches[:nb + n_sync]]
+    key0 = torch.from_numpy(shard.key0.view(np.int64)).to(dev)
+    rows = torch.from_numpy(shard.rows).to(dev)
+    out = torch.empty((B, Tg, D), dtype=torch.float32, device=dev)
+    cnt = torch.zeros(2, dtype=torch.int64, device=dev)
+    recv = torch.empty((B // world, T, D), dtype=torch.float32, device=dev) if world > 1 else None
+    a2a_in = torch.empty((world, B // world, Tg, D), dtype=torch.float32, device=dev) if world > 1 else None
+    a2a_out = torch.empty((world, B // world, max(len(g) for g in groups), D), dtype=torch.float32, device=dev) \
+        if world > 1 else None
+    stream = torch.cuda.current_stream(dev)
+
+    def step(i, pd):
+        system.embbag(dbat[i], key0, rows, out, cnt, prefetch_distance=pd, stream=stream.cuda_stream)
+        if world > 1:
+            # pooled [B, Tg, D] is peer-major along B: one all-to-all moves every peer's slice
+            a2a_in.copy_(out.view(world, B // world, Tg, D))
+            if all(len(g) == Tg for g in groups):
+                dist.all_to_all_single(a2a_out[:, :, :Tg], a2a_in)
+            else:
+                pad = torch.zeros((world, B // world, a2a_out.shape[2], D), dtype=torch.float32, device=dev)
+                pad[:, :, :Tg] = a2a_in
+                dist.all_to_all_single(a2a_out, pad)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---------------- warm-up (fills the cache) ----------------
+    for i in range(args.warmup):
+        step(i, args.prefetch)
+    system.sync(stream.cuda_stream)
+    barrier()
+
+    # ---------------- timed region ----------------
+    clocks = Clocks(local)
+    clocks.start()
+    time.sleep(0.25)
+    cnt.zero_()
+    st0 = system.stats()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for k in range(args.steps):
+        ev[k][0].record(stream)
+        step(args.warmup + k, args.prefetch)
+        ev[k][1].record(stream)
+    e1.record(stream)
+    barrier()
+    clk = clocks.stop()
+    system.sync(stream.cuda_stream)
+    ms_local = e0.elapsed_time(e1)
+    ms = max_over_ranks(ms_local)
+    kern_ms = [a.elapsed_time(b) for a, b in ev]
+    st1 = system.stats()
+    c = cnt.cpu().numpy()
+    lookups_local, miss_lookups = int(c[0]), int(c[1])
+    fills = st1["fills"] - st0["fills"]
+    lookups_global = B * T * L * args.steps
+    value = lookups_global / (ms / 1e3)
+
+    hbm_peak, peak_kind = _peaks()
+    link_peak = _link_peak()
+    avg_kern_s = statistics.mean(kern_ms) / 1e3
+    bags_local = B * Tg
+    alg_bytes = bags_local * L * (D * 4 + 8) + bags_local * D * 4      # rows + indices + pooled out
+    roofline = {"bound": "hbm", "achieved": alg_bytes / avg_kern_s / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                "frac": alg_bytes / avg_kern_s / 1e9 / hbm_peak, "traffic": None,
+                "kernel": "agile_kernel<EmbBagWork> (fused engine+service+embbag)",
+                "bytes_per_launch": alg_bytes, "peak_kind": peak_kind}
+    miss_bytes = fills / args.steps * 4096
+    roofline_link = {"bound": "link", "achieved": miss_bytes / avg_kern_s / 1e9, "peak": link_peak, "unit": "GB/s",
+                     "frac": miss_bytes / avg_kern_s / 1e9 / link_peak,
+                     "iops": fills / args.steps / avg_kern_s, "page_fills_per_step": fills / args.steps,
+                     "peak_kind": "measured zero-copy 4 KiB gather (profiles/link_probe_r01.json)"}
+
+    line = {"metric": "dlrm_lookups_per_s", "value": value, "unit": "lookups/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (Criteo-Kaggle-shaped cardinalities scaled to 4x cache, bounded Zipf "
+                    f"{ALPHA} indices{' hashed over rows' if scatter else ''}, hash-generated fp32 rows)",
+            "config": {"workload": "dlrm_embbag" + ("_sharded_a2a" if world > 1 else ""), "tables": T, "dim": D,
+                       "global_batch": B, "pooling": L, "cache_bytes_per_gpu": cache_bytes,
+                       "table_bytes_per_gpu": table_bytes, "tables_this_rank": Tg,
+                       "store": "host-pinned GPU-mapped page store, link emulation (no NVMe on the box)",
+                       "ways": 32, "queue_pairs": 128, "sq_depth": 256, "prefetch_distance": args.prefetch,
+                       "l2": "inputs larger than L2 (16 GiB HBM cache over a 64 GiB store; distinct batch per step)",
+                       "parallelism": f"table-wise x{world}" if world > 1 else "single"},
+            "roofline": roofline, "roofline_link": roofline_link,
+            "hit_rate": 1.0 - miss_lookups / max(1, lookups_local),
+            "gpu_launches": args.steps, "clocks": clk, "setup_s": setup_s}
+
+    if not args.quick:
+        # ---- sync mode (prefetch distance 0) on fresh batches: the async-vs-sync overlap speedup
+        barrier()
+        s0 = torch.cuda.Event(enable_timing=True)
+        s1 = torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        for k in range(n_sync):
+            step(nb + k, 0)
+        s1.record(stream)
+        barrier()
+        system.sync(stream.cuda_stream)
+        ms_sync = max_over_ranks(s0.elapsed_time(s1)) / n_sync
+        line["sync_ms_per_step"] = ms_sync
+        line["async_vs_sync"] = ms_sync / (ms / args.steps)
+        # ---- hit path: replay the batch just processed (every page resident) -> HBM roofline
+        hb = nb + n_sync - 1
+        h0 = torch.cuda.Event(enable_timing=True)
+        h1 = torch.cuda.Event(enable_timing=True)
+        cnt.zero_()
+        h0.record(stream)
+        reps = 5
+        for _ in range(reps):
+            system.embbag(dbat[hb], key0, rows, out, cnt, prefetch_distance=0, stream=stream.cuda_stream)
+        h1.record(stream)
+        system.sync(stream.cuda_stream)
+        hit_s = h0.elapsed_time(h1) / reps / 1e3
+        c = cnt.cpu().numpy()
+        line["roofline_hit"] = {"bound": "hbm", "achieved": alg_bytes / hit_s / 1e9, "peak": hbm_peak,
+                                "unit": "GB/s", "frac": alg_bytes / hit_s / 1e9 / hbm_peak,
+                                "miss_lookups": int(c[1]), "ms_per_launch": hit_s * 1e3,
+                                "lookups_per_s": B * Tg * L / hit_s}
+        # ---- end to end through the C-ABI with host buffers (H2D indices, D2H pooled) ----
+        if world == 1:
+            # fresh batches (never seen by the cache in this run), like the timed region
+            hb_np = [host_batches[nb + n_sync + k] for k in range(args.steps)]
+            out_np = np.empty((B, Tg, D), dtype=np.float32)
+            keyh = shard.key0.copy()
+            t_e = time.perf_counter()
+            for k in range(args.steps):
+                system.embbag_host(hb_np[k], keyh, shard.rows, D, prefetch_distance=args.prefetch, out=out_np)
+            e2e_s = (time.perf_counter() - t_e) / args.steps
+            line["e2e"] = {"value": B * T * L / e2e_s, "unit": "lookups/s",
+                           "h2d_bytes_per_step": int(hb_np[0].nbytes + 2 * Tg * 8),
+                           "d2h_bytes_per_step": int(out_np.nbytes + 16),
+                           "path": "agile_embbag_host (C-ABI, host buffers)"}
+        else:
+            hbuf = [torch.from_numpy(host_batches[nb + n_sync + k]).pin_memory() for k in range(args.steps)]
+            res = torch.empty((world, B // world, a2a_out.shape[2], D), dtype=torch.float32).pin_memory()
+            barrier()
+            t_e = time.perf_counter()
+            for k in range(args.steps):
+                dbat[0].copy_(hbuf[k], non_blocking=True)
+                step(0, args.prefetch)
+                res.copy_(a2a_out, non_blocking=True)
+                torch.cuda.current_stream().synchronize()
+            barrier()
+            e2e_s = max_over_ranks(time.perf_counter() - t_e) / args.steps
+            line["e2e"] = {"value": B * T * L / e2e_s, "unit": "lookups/s",
+                           "h2d_bytes_per_step": int(hbuf[0].nbytes), "d2h_bytes_per_step": int(res.nbytes),
+                           "path": "H2D indices -> embbag -> NCCL all_to_all -> D2H pooled (per rank)"}
+        # ---- CPU baseline (rank 0, N=1 only): oracle C port on host threads, bounded sample ----
+        if rank == 0 and world == 1:
+            from oracle.cpu import CpuEmbeddingCache
+            threads = os.cpu_count() or 1
+            lines_ = system.num_lines
+            cc = CpuEmbeddingCache(lines_, 32, SEED)
+            bs = 128
+            done, tsum, k = 0, 0.0, 0
+            errs = []
+            while tsum < args.cpu_seconds and k < 400:
+                idx = host_batches[k % len(host_batches)][:bs]
+                t_c = time.perf_counter()
+                o = cc.embbag(idx, shard.key0, shard.rows, D, threads=threads)
+                dt = time.perf_counter() - t_c
+                if k >= 2:
+                    tsum += dt
+                    done += idx.size
+                k += 1
+            # cross-check the GPU output of the last timed-out batch against the CPU port
+            o_cpu = cc.embbag(host_batches[hb][:16], shard.key0, shard.rows, D, threads=threads)
+            system.embbag(dbat[hb], key0, rows, out, cnt, prefetch_distance=0, stream=stream.cuda_stream)
+            system.sync(stream.cuda_stream)
+            o_gpu = out[:16].cpu().numpy()
+            line["cpu_gpu_max_abs_diff"] = float(np.max(np.abs(o_cpu - o_gpu)))
+            line["cpu_baseline"] = {"value": done / tsum if tsum else None, "unit": "lookups/s", "cores": threads,
+                                    "kind": "port",
+                                    "sample": f"{k - 2} batches of {bs} samples x {T} tables x {L} (oracle/agile_oracle.c, "
+                                              f"set-assoc clock cache of {lines_} lines over the same synthetic store)"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    system.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -228,6 +228,8 @@ int agile_create(const char* config_text, int cuda_device, agile_ctx** out) {
   if (emu != "model" && emu != "link") return fail(ctx, AGILE_E_CONFIG, "device.emulation must be model|link");
   if (jitter != "none" && jitter != "uniform" && jitter != "exponential") return fail(ctx, AGILE_E_CONFIG, "unknown jitter kind");
   d.num_qp = d.num_devices * d.pairs_per_device;
+  // each service warp serves at most 128 CQs (kMaxCqPerLane x 32 lanes)
+  d.service_warps = std::max<uint32_t>(d.service_warps, (d.num_qp + 32 * kMaxCqPerLane - 1) / (32 * kMaxCqPerLane));
   d.cq_window = std::min<uint32_t>(32, d.cq_depth);
   d.num_lines = (uint32_t)lines;
   d.ways = (uint32_t)ways;

@@ -717,22 +717,20 @@ __device__ __forceinline__ void advance_head(const DevCtx& c, u32 q, u32 who) {
   if (moved) log_ev(c, who, M_NVME, A_HEAD, q, h);
 }
 
-// One window pass over a CQ (cq_polling, agile_service.py:147-171 + process_cqe 173-199).
-__device__ u32 cq_poll(const DevCtx& c, u32 cq, u32 who) {
+// One window pass over a CQ owned by the calling warp (cq_polling, agile_service.py:147-171 +
+// process_cqe 173-199): 32 lanes validate 32 consecutive CQEs against the expected phase; each
+// valid lane releases its SQE (first, so stuck producers move), then flips the cache line
+// BUSY->READY with one release-add (fan-out: waiters poll the tag word), then the SQ head
+// advances over the completed prefix.  Only a full window rings the CQ doorbell.  off/mask is the
+// CQ's poll state, held in the owning lane's registers by service_main.
+__device__ u32 cq_window_pass(const DevCtx& c, u32 cq, u64& off, u32& mask, u32 who, u64& lat_acc, u32& rings) {
   const u32 lane = lane_id();
-  CqWords* cw = &c.cqw[cq];
-  int got = 0;
-  if (lane == 0) got = atom_cas_acquire(&cw->claim, 0u, 1u) == 0u;
-  got = __shfl_sync(FULL, got, 0);
-  if (!got) return 0;
-  const u64 offset = ld_relaxed(&cw->poll_offset);
-  u32 mask = ld_relaxed(&cw->poll_mask);
   const u32 window = c.cq_window;
   const u32 Dq = c.cq_depth;
   const u32 Ds = c.sq_depth;
   bool valid = false;
   u32 sq = 0, slot = 0;
-  u64 v = offset + lane;
+  const u64 v = off + lane;
   if (lane < window && !((mask >> lane) & 1u)) {
     const u64 w = ld_acquire(reinterpret_cast<const u64*>(c.cqe + (u64)cq * Dq + (u32)(v & (Dq - 1))) + 1);
     const u32 phase = (u32)(w >> 48) & 1u;
@@ -743,59 +741,45 @@ __device__ u32 cq_poll(const DevCtx& c, u32 cq, u32 who) {
       slot = (u32)(w >> 32) & 0xffffu;   // CID == SQE slot
     }
   }
-  u64 lat = 0;
   if (valid) {
     const u32 idx = sq * Ds + slot;
-    if (sq >= c.num_qp || slot >= Ds) { set_error(c, E_UNKNOWN_CID, cq, v); valid = false; }
-    else {
+    if (sq >= c.num_qp || slot >= Ds) {
+      set_error(c, E_UNKNOWN_CID, cq, v);
+      valid = false;
+    } else {
       const CmdCtx x = c.cmd[idx];
-      // release the SQE first so stuck producers can move (agile_service.py:188-195)
-      if (atom_cas_acqrel(&c.sq_state[idx], SQ_ISSUED, SQ_EMPTY) != SQ_ISSUED)
-        set_error(c, E_UNKNOWN_CID, sq, slot);
+      const u32 os = atom_cas_acqrel(&c.sq_state[idx], SQ_ISSUED, SQ_EMPTY);
+      atomicExch(&c.sq_done_v[idx], x.vidx + 1);
+      u64 ot = (u64)ST_BUSY << ST_SHIFT;
+      const bool cache = x.line != NONE && (x.kind == K_FILL || x.kind == K_WB_KEEP);
+      if (cache) ot = atom_add_release(&c.tags[x.line], 1ull << ST_SHIFT);   // BUSY -> READY
+      if (os != SQ_ISSUED) set_error(c, E_UNKNOWN_CID, sq, slot);
+      if (tw_state(ot) != ST_BUSY) set_error(c, E_ILLEGAL_STATE, x.line, ot);
       log_ev(c, who, M_NVME, A_SQE_RELEASE, sq, slot, slot);
       log_ev(c, who, M_SVC, A_CQE_PROCESS, cq, v, slot, sq);
-      atomicExch(&c.sq_done_v[idx], x.vidx + 1);
-      if (x.line != NONE && (x.kind == K_FILL || x.kind == K_WB_KEEP)) {
-        // BUSY -> READY: one release-add on the state field preserves ref/pins/version
-        const u64 old = atom_add_release(&c.tags[x.line], 1ull << ST_SHIFT);
-        if (tw_state(old) != ST_BUSY) set_error(c, E_ILLEGAL_STATE, x.line, old);
-        log_state(c, who, x.line, ST_BUSY, ST_READY, x.key);
-      }
-      lat = gtimer() - x.t_submit;
+      if (cache) log_state(c, who, x.line, ST_BUSY, ST_READY, x.key);
+      lat_acc += gtimer() - x.t_submit;
       fence_sc();
     }
   }
   __syncwarp();
   // head advance: one leader per SQ among completed lanes
-  u32 grp = __match_any_sync(FULL, valid ? sq : 0xffffffffu);
+  const u32 grp = __match_any_sync(FULL, valid ? sq : 0xffffffffu);
   if (valid && (grp & lanemask_lt()) == 0) advance_head(c, sq, who);
   const u32 vb = __ballot_sync(FULL, valid);
   mask |= vb;
-  // stats (warp-aggregated)
-  u64 lsum = lat;
-#pragma unroll
-  for (int o = 16; o; o >>= 1) lsum += __shfl_xor_sync(FULL, lsum, o);
-  const u32 k = __popc(vb);
   const u32 fullw = window == 32 ? FULL : ((1u << window) - 1u);
-  if (lane == 0) {
-    if (k) {
-      atomicAdd(&c.stats[S_COMPLETIONS], (u64)k);
-      atomicAdd(&c.stats[S_BARRIER_COUNT], (u64)k);
-      atomicAdd(&c.stats[S_BARRIER_NS], lsum);
-    }
-    u64 off = offset;
-    if (mask == fullw) {
+  if (mask == fullw) {
+    if (lane == 0) {
       log_ev(c, who, M_SVC, A_WINDOW_RING, cq, off, off + window);
-      st_release(&cw->host_db, off + window);   // ring only full windows
-      atomicAdd(&c.stats[S_WINDOWS], 1ull);
-      off += window;
-      mask = 0;
+      st_release(&c.cqw[cq].host_db, off + window);   // ring only full windows
     }
-    st_relaxed(&cw->poll_offset, off);
-    st_relaxed(&cw->poll_mask, mask);
-    if (k) atom_add_release(&c.pw->outstanding, (u64)0 - (u64)k);
-    st_release(&cw->claim, 0u);
+    ++rings;
+    off += window;
+    mask = 0;
   }
+  const u32 k = __popc(vb);
+  if (k && lane == 0) atom_add_release(&c.pw->outstanding, (u64)0 - (u64)k);
   __syncwarp();
   return k;
 }
@@ -821,47 +805,107 @@ __device__ void drain_partial_windows(const DevCtx& c, u32 who) {
   }
 }
 
+// Service warps (AgileService._warp_program, agile_service.py:126-145).  Warp w serves CQs
+// w, w+S, w+2S, ... — the reference's round-robin stride, made static so the poll state (offset,
+// window mask) lives in the owning lane's registers and no claim word is needed.  Each pass one
+// lane per CQ checks the next expected CQE's phase (one round trip for all owned CQs); only ready
+// CQs get a window pass.  Idle passes back off poll_ns -> idle_max_ns.
+constexpr u32 kMaxCqPerLane = 4;
 __device__ void service_main(const DevCtx& c, const Launch& L, u32 sw) {
+  const u32 lane = lane_id();
   const u32 who = WHO_SVC | sw;
   const u32 n = c.num_qp;
   const u32 S = c.service_warps;
-  if (sw == 0 && lane_id() == 0) log_ev(c, who, M_SVC, A_START, S);
-  u32 pos = sw;
-  u32 idle = c.poll_ns;
-  u32 sweep = 0, since = 0;
-  const u32 per_sweep = (n + S - 1) / S;
-  while (true) {
-    const u32 got = cq_poll(c, pos % n, who);
-    pos += S;
-    sweep += got;
-    bool stop = false;
-    if (++since >= per_sweep) {
-      if (lane_id() == 0) {
-        const bool users = ld_acquire(&c.run->users_done) >= L.n_user_ctas;
-        const u64 out = ld_acquire(&c.pw->outstanding);
-        stop = (users && out == 0) || aborted(c);
-        if (users && atomicCAS(&c.run->stop_logged, 0u, 1u) == 0u) log_ev(c, who, M_SVC, A_STOP);
-      }
-      stop = __shfl_sync(FULL, (int)stop, 0) != 0;
-      if (stop) break;
-      if (sweep == 0) {
-        nap(idle);
-        idle = min(idle * 2, c.idle_max_ns);
-      } else {
-        idle = c.poll_ns;
-      }
-      sweep = 0;
-      since = 0;
+  const u32 nown = n > sw ? (n - sw + S - 1) / S : 0;
+  if (sw == 0 && lane == 0) log_ev(c, who, M_SVC, A_START, S);
+  if (nown > 32 * kMaxCqPerLane) set_error(c, E_PROTOCOL, nown, 0);
+  u64 off[kMaxCqPerLane];
+  u32 msk[kMaxCqPerLane];
+#pragma unroll
+  for (u32 j = 0; j < kMaxCqPerLane; ++j) {
+    const u32 k = lane + 32 * j;
+    off[j] = 0; msk[j] = 0;
+    if (k < nown) {
+      const u32 cq = sw + k * S;
+      off[j] = ld_relaxed(&c.cqw[cq].poll_offset);
+      msk[j] = ld_relaxed(&c.cqw[cq].poll_mask);
     }
   }
+  u32 idle = c.poll_ns;
+  u64 lat = 0;
+  u32 rings = 0, done = 0;
+  const u32 Dq = c.cq_depth;
+  while (true) {
+    u32 got = 0;
+#pragma unroll
+    for (u32 j = 0; j < kMaxCqPerLane; ++j) {
+      if (32 * j >= nown) break;
+      const u32 k = lane + 32 * j;
+      bool ready = false;
+      if (k < nown) {
+        const u32 cq = sw + k * S;
+        const u64 nv = off[j] + __popc(msk[j]);   // valid CQEs arrive in order: the mask is a prefix
+        const u64 w = ld_relaxed(reinterpret_cast<const u64*>(c.cqe + (u64)cq * Dq + (u32)(nv & (Dq - 1))) + 1);
+        ready = (((u32)(w >> 48)) & 1u) == 1u - (u32)((nv / Dq) & 1u);
+      }
+      u32 rb = __ballot_sync(FULL, ready);
+      while (rb) {
+        const int l = __ffs(rb) - 1;
+        rb &= rb - 1;
+        u64 o = __shfl_sync(FULL, off[j], l);
+        u32 m = __shfl_sync(FULL, msk[j], l);
+        const u32 cq = sw + ((u32)l + 32 * j) * S;
+        got += cq_window_pass(c, cq, o, m, who, lat, rings);
+        if (lane == (u32)l) { off[j] = o; msk[j] = m; }
+      }
+    }
+    done += got;
+    if (got) {
+      idle = c.poll_ns;
+      continue;
+    }
+    int stop = 0;
+    if (lane == 0) {
+      const bool users = ld_acquire(&c.run->users_done) >= L.n_user_ctas;
+      const u64 out = ld_acquire(&c.pw->outstanding);
+      stop = (users && out == 0) || aborted(c);
+      if (users && atomicCAS(&c.run->stop_logged, 0u, 1u) == 0u) log_ev(c, who, M_SVC, A_STOP);
+    }
+    if (__shfl_sync(FULL, stop, 0)) break;
+    nap(idle);
+    idle = min(idle * 2, c.idle_max_ns);
+  }
+  // persist the poll state for the drain and the next launch
+#pragma unroll
+  for (u32 j = 0; j < kMaxCqPerLane; ++j) {
+    const u32 k = lane + 32 * j;
+    if (k < nown) {
+      const u32 cq = sw + k * S;
+      st_relaxed(&c.cqw[cq].poll_offset, off[j]);
+      st_relaxed(&c.cqw[cq].poll_mask, msk[j]);
+    }
+  }
+  u64 lsum = lat;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) lsum += __shfl_xor_sync(FULL, lsum, o);
+  if (lane == 0) {
+    if (done) {
+      atomicAdd(&c.stats[S_COMPLETIONS], (u64)done);
+      atomicAdd(&c.stats[S_BARRIER_COUNT], (u64)done);
+      atomicAdd(&c.stats[S_BARRIER_NS], lsum);
+    }
+    if (rings) atomicAdd(&c.stats[S_WINDOWS], (u64)rings);
+  }
+  __threadfence();
   // the last warp out rings residual partial windows (agile_service.py:141-145)
   u32 order = 0;
-  if (lane_id() == 0) order = atomicAdd(&c.run->svc_exited, 1u);
+  if (lane == 0) order = atomicAdd(&c.run->svc_exited, 1u);
   order = __shfl_sync(FULL, order, 0);
   if (order == S - 1) {
+    __threadfence();
     drain_partial_windows(c, who);
     __syncwarp();
-    if (lane_id() == 0) st_release(&c.run->engine_stop, 1u);
+    if (lane == 0) st_release(&c.run->engine_stop, 1u);
   }
 }
 
@@ -977,6 +1021,35 @@ __device__ void engine_main(const DevCtx& c, u32 ew) {
   u64 bytes_r = 0, bytes_w = 0;
   while (true) {
     bool did = false;
+    // ---- start moving the bytes of the two oldest fetched commands: the loads (host link
+    //      latency) stay in flight while this pass posts completions and fetches new SQEs
+    const u32 tocopy = __ballot_sync(FULL, pv && !pcp);
+    int l0 = -1, l1 = -1;
+    uint4 v0[8], v1[8];
+    uint4* t0 = nullptr;
+    uint4* t1 = nullptr;
+    if (tocopy) {
+      did = true;
+      l0 = oldest_lane(pv && !pcp, pseq);   // oldest first: no lane starves behind new fetches
+      l1 = oldest_lane(pv && !pcp && (int)lane != l0, pseq);
+      const int s1l = l1 < 0 ? l0 : l1;
+      const u32 op0 = __shfl_sync(FULL, pop, l0), op1 = __shfl_sync(FULL, pop, s1l);
+      const u32 d0 = __shfl_sync(FULL, pdev, l0), d1 = __shfl_sync(FULL, pdev, s1l);
+      const u64 b0 = __shfl_sync(FULL, pblk, l0), b1 = __shfl_sync(FULL, pblk, s1l);
+      const u64 p0 = __shfl_sync(FULL, prp, l0), p1 = __shfl_sync(FULL, prp, s1l);
+      const uint4* s0 = op0 == OP_READ ? reinterpret_cast<const uint4*>(c.store[d0] + (b0 << kBlockShift))
+                                       : reinterpret_cast<const uint4*>(p0);
+      t0 = op0 == OP_READ ? reinterpret_cast<uint4*>(p0) : reinterpret_cast<uint4*>(c.store_w[d0] + (b0 << kBlockShift));
+      const uint4* s1 = op1 == OP_READ ? reinterpret_cast<const uint4*>(c.store[d1] + (b1 << kBlockShift))
+                                       : reinterpret_cast<const uint4*>(p1);
+      t1 = op1 == OP_READ ? reinterpret_cast<uint4*>(p1) : reinterpret_cast<uint4*>(c.store_w[d1] + (b1 << kBlockShift));
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v0[k] = __ldcg(s0 + lane + 32 * k);
+      if (l1 >= 0) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v1[k] = __ldcg(s1 + lane + 32 * k);
+      }
+    }
     const u64 now = gtimer();
     // ---- post due completions (device_post / stall, nvme_queue.py:266-279, ssd_model.py:200-206)
     const bool due = pv && pcp && pdue <= now;
@@ -1022,51 +1095,14 @@ __device__ void engine_main(const DevCtx& c, u32 ew) {
         }
       }
     }
-    // ---- move the bytes of up to two fetched commands (two 4 KiB pages in flight per pass),
-    //      interleaved with posting so completions are never held behind a long copy batch
-    const u32 tocopy = __ballot_sync(FULL, pv && !pcp);
-    if (tocopy) {
-      did = true;
-      // oldest-fetched first (no lane starves behind newly fetched commands)
-      const int l0 = oldest_lane(pv && !pcp, pseq);
-      const int l1 = oldest_lane(pv && !pcp && (int)lane != l0, pseq);
-      const int s1l = l1 < 0 ? l0 : l1;
-      const u32 op0 = __shfl_sync(FULL, pop, l0), op1 = __shfl_sync(FULL, pop, s1l);
-      const u32 d0 = __shfl_sync(FULL, pdev, l0), d1 = __shfl_sync(FULL, pdev, s1l);
-      const u64 b0 = __shfl_sync(FULL, pblk, l0), b1 = __shfl_sync(FULL, pblk, s1l);
-      const u64 p0 = __shfl_sync(FULL, prp, l0), p1 = __shfl_sync(FULL, prp, s1l);
-      const uint4* s0 = op0 == OP_READ ? reinterpret_cast<const uint4*>(c.store[d0] + (b0 << kBlockShift))
-                                       : reinterpret_cast<const uint4*>(p0);
-      uint4* t0 = op0 == OP_READ ? reinterpret_cast<uint4*>(p0)
-                                 : reinterpret_cast<uint4*>(c.store_w[d0] + (b0 << kBlockShift));
-      const uint4* s1 = op1 == OP_READ ? reinterpret_cast<const uint4*>(c.store[d1] + (b1 << kBlockShift))
-                                       : reinterpret_cast<const uint4*>(p1);
-      uint4* t1 = op1 == OP_READ ? reinterpret_cast<uint4*>(p1)
-                                 : reinterpret_cast<uint4*>(c.store_w[d1] + (b1 << kBlockShift));
-      uint4 v0[8], v1[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) v0[k] = __ldcg(s0 + lane + 32 * k);
-      if (l1 >= 0) {
-#pragma unroll
-        for (int k = 0; k < 8; ++k) v1[k] = __ldcg(s1 + lane + 32 * k);
-      }
-#pragma unroll
-      for (int k = 0; k < 8; ++k) __stcg(t0 + lane + 32 * k, v0[k]);
-      if (l1 >= 0) {
-#pragma unroll
-        for (int k = 0; k < 8; ++k) __stcg(t1 + lane + 32 * k, v1[k]);
-      }
-      __threadfence();   // page bytes visible before the CQE release of these commands
-      __syncwarp();
-      if ((int)lane == l0 || (int)lane == l1) pcp = true;
-    }
     // ---- fetch newly published SQEs into free lanes (on_sq_doorbell/_fetch, ssd_model.py:138-166);
     //      while bytes are still to be moved only every 4th pass pays the doorbell round trips
     const u32 freeb = __ballot_sync(FULL, !pv);
     u32 nfree = __popc(freeb);
     bool newcmd = false;
     ++pass;
-    const bool fetch_now = !__ballot_sync(FULL, pv && !pcp) || (pass & 3u) == 0;
+    const u32 ncopy = __popc(__ballot_sync(FULL, pv && !pcp));
+    const bool fetch_now = ncopy < 8 || (pass & 3u) == 0;
     if (nfree && nq && fetch_now) {
       u32 assigned = 0;   // free lanes handed out in earlier chunks
       for (u32 b0 = 0; b0 < nq && nfree; b0 += 32) {
@@ -1154,6 +1190,18 @@ __device__ void engine_main(const DevCtx& c, u32 ew) {
       seq += __popc(nb);
       if (lane == 0) atomicAdd(&c.stats[S_FETCHED], (u64)__popc(nb));
     }
+    // ---- finish the page moves started at the top of the pass
+    if (l0 >= 0) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) __stcg(t0 + lane + 32 * k, v0[k]);
+      if (l1 >= 0) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) __stcg(t1 + lane + 32 * k, v1[k]);
+      }
+      __threadfence();   // page bytes visible before the CQE release of these commands
+      __syncwarp();
+      if ((int)lane == l0 || (int)lane == l1) pcp = true;
+    }
     // ---- exit once the service is done and nothing is in service
     const bool busy = __ballot_sync(FULL, pv) != 0;
     if (!busy) {
@@ -1210,8 +1258,11 @@ __device__ __forceinline__ void user_done(const DevCtx& c) {
   }
 }
 
+#ifndef AGILE_MIN_CTAS
+#define AGILE_MIN_CTAS 2
+#endif
 template <class Work>
-__global__ void __launch_bounds__(kCtaThreads) agile_kernel(DevCtx c, Launch L, Work work) {
+__global__ void __launch_bounds__(kCtaThreads, AGILE_MIN_CTAS) agile_kernel(DevCtx c, Launch L, Work work) {
   const Role r = take_role(c);
   const u32 warp = threadIdx.x >> 5;
   if (r.kind == 0) {

@@ -33,11 +33,19 @@ __device__ __forceinline__ bool user_grid_barrier(const DevCtx& c, u32 n_user_ct
   return s_ok != 0;
 }
 
-// compute phase of the benchmarks: time-calibrated busy loop (Delay(compute_ns) of the reference)
+// compute phase of the benchmarks: Delay(compute_ns) of the reference (bench/ctc.py:81-83).  The
+// warp sleeps in 256 ns steps and lane 0 alone reads %globaltimer, so a computing CTA does not
+// steal issue slots from co-resident engine/service warps.
 __device__ __forceinline__ void compute_spin(u64 ns) {
   if (!ns) return;
-  const u64 t0 = gtimer();
-  while (gtimer() - t0 < ns) { }
+  int more = 1;
+  u64 t0 = 0;
+  if (lane_id() == 0) t0 = gtimer();
+  while (more) {
+    __nanosleep(256);
+    if (lane_id() == 0) more = gtimer() - t0 < ns;
+    more = __shfl_sync(0xffffffffu, more, 0);
+  }
 }
 
 __device__ __forceinline__ u32 user_who(u32 uidx) { return WHO_USER | (uidx * kCtaThreads + threadIdx.x); }
@@ -292,34 +300,57 @@ struct EmbBagWork {
     return true;
   }
 
+  static constexpr u32 kMaxPd = 8;
+  // next bag for this warp from the launch-wide counter (dynamic balance: a warp held up by a
+  // slow miss does not hold back a static share of the batch)
+  __device__ __forceinline__ u32 grab(const DevCtx& c) const {
+    u32 b = 0;
+    if (lane_id() == 0) b = (u32)atomicAdd(&c.run->work_next, 1ull);
+    return __shfl_sync(FULL, b, 0);
+  }
+
   __device__ void run(const DevCtx& c, u32 uidx, u32 nusers) {
     const u32 lane = lane_id();
     const u32 gw = uidx * kCtaWarps + (threadIdx.x >> 5);
-    const u32 nw = nusers * kCtaWarps;
     const u32 nbags = B * T;
     const u32 who = user_who(uidx);
     const bool lact = lane < L;
+    const u32 depth = pd > kMaxPd ? kMaxPd : pd;
     u32 misses_local = 0, lookups_local = 0;
-    // prologue prefetch
-    if (pd) {
-      for (u32 k = 0; k < pd; ++k) {
-        const u32 bag = gw + k * nw;
-        if (bag >= nbags) break;
-        u64 key = 0; u32 off = 0;
-        const bool a = bag_keys(bag, lact, key, off);
-        access_warp(c, a, key, false, who, gw, true);
-      }
+    // ring of grabbed-and-prefetched bags (async mode): the warp always has `depth` future bags'
+    // misses in flight while it sums the oldest one
+    u32 ring[kMaxPd];
+    u32 head = 0, count = 0;
+    for (u32 k = 0; k < depth; ++k) {
+      const u32 nb = grab(c);
+      if (nb >= nbags) break;
+      u64 key = 0; u32 off = 0;
+      const bool a = bag_keys(nb, lact, key, off);
+      access_warp(c, a, key, false, who, gw + k, true);
+      ring[(head + count) % kMaxPd] = nb;
+      ++count;
     }
-    for (u32 bag = gw; bag < nbags; bag += nw) {
-      if (aborted(c)) break;
-      if (pd) {
-        const u32 nb = bag + pd * nw;
+    u32 pass = 0;
+    while (true) {
+      u32 bag;
+      if (depth) {
+        if (!count) break;
+        bag = ring[head];
+        head = (head + 1) % kMaxPd;
+        --count;
+        const u32 nb = grab(c);
         if (nb < nbags) {
           u64 key = 0; u32 off = 0;
           const bool a = bag_keys(nb, lact, key, off);
-          access_warp(c, a, key, false, who, gw, true);
+          access_warp(c, a, key, false, who, gw + (++pass), true);
+          ring[(head + count) % kMaxPd] = nb;
+          ++count;
         }
+      } else {
+        bag = grab(c);
+        if (bag >= nbags) break;
       }
+      if (aborted(c)) break;
       u64 key = 0; u32 off = 0;
       const bool a = bag_keys(bag, lact, key, off);
       float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);

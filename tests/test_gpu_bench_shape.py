@@ -28,9 +28,11 @@ def test_ctc_async_overlaps_compute(gpu_system):
 
 @pytest.mark.parametrize("ndev", [1, 2])
 def test_model_mode_rate_ceiling_and_scaling(gpu_system, ndev):
-    s = gpu_system(num_devices=ndev, pairs=8, sq_depth=256, cq_depth=256, cache_lines=4096, ways=32,
-                   blocks=1 << 16, emulation="model", engine_warps=8, warps=4)
-    r = s.run_loop(64 * ndev, warmup_ns=2_000_000, measure_ns=20_000_000)
+    s = gpu_system(num_devices=ndev, pairs=8, sq_depth=256, cq_depth=256, cache_lines=8192 * ndev, ways=32,
+                   blocks=1 << 18, emulation="model", engine_warps=16, warps=4)
+    # in-flight population well above the channel count: GPU issue/completion latencies are
+    # microseconds, so the reference's 2x parallelism cannot cover them
+    r = s.run_loop(512 * ndev, warmup_ns=2_000_000, measure_ns=20_000_000)
     gbps = r["completions"] * 4096 / r["window_ns"]
     ceiling = ndev * 16 * 4096 / 17712
-    assert ceiling * 0.93 <= gbps <= ceiling * 1.02, (gbps, ceiling)
+    assert ceiling * 0.95 <= gbps <= ceiling * 1.01, (gbps, ceiling)
