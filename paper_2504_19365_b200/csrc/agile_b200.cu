@@ -32,6 +32,9 @@ struct agile_ctx {
   void* d_stage = nullptr;
   size_t d_stage_bytes = 0;
   cudaStream_t stream = nullptr;
+  // async_read WaitNodes (AgileBuf barriers) for the reads / loop / seq workloads
+  void* nodes = nullptr;
+  size_t nodes_cap = 0;
 };
 
 namespace {
@@ -125,6 +128,18 @@ int device_error(agile_ctx* ctx) {
   z.outstanding = pw.outstanding;
   cudaMemcpy(ctx->d.pw, &z, sizeof(z), cudaMemcpyHostToDevice);
   return code;
+}
+
+WaitNode* get_nodes(agile_ctx* ctx, size_t n) {
+  if (n > ctx->nodes_cap) {
+    if (ctx->nodes) { cudaDeviceSynchronize(); cudaFree(ctx->nodes); }
+    ctx->nodes = nullptr;
+    ctx->nodes_cap = 0;
+    if (cudaMalloc(&ctx->nodes, n * sizeof(WaitNode)) != cudaSuccess) return nullptr;
+    cudaMemset(ctx->nodes, 0, n * sizeof(WaitNode));
+    ctx->nodes_cap = n;
+  }
+  return reinterpret_cast<WaitNode*>(ctx->nodes);
 }
 
 template <class W>
@@ -254,6 +269,7 @@ int agile_create(const char* config_text, int cuda_device, agile_ctx** out) {
   m.seed = ctx->seed;
   int rc;
   if ((rc = dalloc(ctx, &d.tags, lines))) return rc;
+  if ((rc = dalloc(ctx, &d.wl, lines))) return rc;
   if ((rc = dalloc(ctx, &d.set_lock, d.num_sets))) return rc;
   if ((rc = dalloc(ctx, &d.hand, d.num_sets))) return rc;
   if ((rc = dalloc(ctx, &d.lines, lines * kBlockBytes))) return rc;
@@ -266,6 +282,7 @@ int agile_create(const char* config_text, int cuda_device, agile_ctx** out) {
   if ((rc = dalloc(ctx, &d.cqe, (size_t)d.num_qp * d.cq_depth))) return rc;
   if ((rc = dalloc(ctx, &d.cqw, d.num_qp))) return rc;
   if ((rc = dalloc(ctx, &d.chan_free, (size_t)d.num_devices * m.parallelism))) return rc;
+  if ((rc = dalloc(ctx, &d.chan_turn, (size_t)d.num_devices * m.parallelism))) return rc;
   if ((rc = dalloc(ctx, &d.dev_lock, d.num_devices))) return rc;
   if ((rc = dalloc(ctx, &d.dev_seq, d.num_devices))) return rc;
   if ((rc = dalloc(ctx, &d.run, 1))) return rc;
@@ -295,6 +312,7 @@ int agile_destroy(agile_ctx* ctx) {
   if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
   if (ctx->d_stage) cudaFree(ctx->d_stage);
   if (ctx->d.log) cudaFree(ctx->d.log);
+  if (ctx->nodes) cudaFree(ctx->nodes);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
   return 0;
@@ -397,6 +415,7 @@ int agile_reset(agile_ctx* ctx, int flags) {
   DevCtx& d = ctx->d;
   if (flags & 1) {
     CK(cudaMemset(d.tags, 0, (size_t)d.num_lines * 8));
+    CK(cudaMemset(d.wl, 0, (size_t)d.num_lines * 8));
     CK(cudaMemset(d.hand, 0, (size_t)d.num_sets * 4));
     CK(cudaMemset(d.set_lock, 0, (size_t)d.num_sets * 4));
   }
@@ -410,6 +429,7 @@ int agile_reset(agile_ctx* ctx, int flags) {
     CK(cudaMemset(d.cqe, 0, (size_t)d.num_qp * d.cq_depth * 16));
     CK(cudaMemset(d.cqw, 0, (size_t)d.num_qp * sizeof(CqWords)));
     CK(cudaMemset(d.chan_free, 0, (size_t)d.num_devices * d.model.parallelism * 8));
+    CK(cudaMemset(d.chan_turn, 0, (size_t)d.num_devices * d.model.parallelism * 8));
     CK(cudaMemset(d.dev_seq, 0, (size_t)d.num_devices * 8));
     CK(cudaMemset(d.pw, 0, sizeof(PersistWords)));
   }
@@ -489,6 +509,8 @@ int agile_run_seq(agile_ctx* ctx, const uint32_t* dev, const uint64_t* blk, int6
   w.dev = d_dev; w.blk = reinterpret_cast<const u64*>(d_blk); w.n = n;
   w.outcome = reinterpret_cast<signed char*>(d_out); w.victim = reinterpret_cast<u64*>(d_vic);
   w.pages = d_pages; w.scratch = d_scr;
+  w.nodes = get_nodes(ctx, 1);
+  if (!w.nodes) return fail(ctx, AGILE_E_CUDA, "node allocation failed");
   int rc = launch(ctx, w, 1, ctx->stream);
   if (!rc) rc = agile_sync(ctx, ctx->stream);
   if (!rc) {
@@ -514,6 +536,8 @@ int agile_run_reads(agile_ctx* ctx, const uint64_t* keys, uint32_t tasks, uint32
   w.epoch_t = reinterpret_cast<u64*>(epoch_t);
   w.tasks = tasks; w.reads = reads; w.epochs = epochs; w.async_mode = async_mode ? 1u : 0u;
   w.compute_ns = compute_ns;
+  w.nodes = get_nodes(ctx, (size_t)tasks * 2 * reads);
+  if (!w.nodes) return fail(ctx, AGILE_E_CUDA, "node allocation failed");
   const uint32_t users = (tasks + kCtaThreads - 1) / kCtaThreads;
   const uint32_t cap = resident_ctas<ReadsWork>(ctx);
   if (users + ctx->d.n_engine_ctas + ctx->d.n_service_ctas > cap)
@@ -536,6 +560,8 @@ int agile_run_loop(agile_ctx* ctx, uint32_t conc, uint64_t warmup_ns, uint64_t m
   w.warmup_ns = warmup_ns;
   w.measure_ns = measure_ns;
   w.max_per_task = max_per_task ? max_per_task : ~0ull;
+  w.nodes = get_nodes(ctx, conc);
+  if (!w.nodes) return fail(ctx, AGILE_E_CUDA, "node allocation failed");
   const uint32_t users = (conc + kCtaThreads - 1) / kCtaThreads;
   return launch(ctx, w, users, reinterpret_cast<cudaStream_t>(stream));
 }

@@ -246,7 +246,10 @@ __device__ int claim_key_warp(const DevCtx& c, u64 key, u32 pin_n, u32 who, u32&
     }
     const u64 nw = tw_make(ST_BUSY, key, tw_ver(old) + 1, true, pin_n);
     u64 prev = 0;
-    if (lane == 0) prev = atomicCAS(&c.tags[base + v], old, nw);
+    if (lane == 0) {
+      st_relaxed(&c.wl[base + v], ((u64)((tw_ver(old) + 1) & 0x1FFu)) << 55);   // open the waiter list
+      prev = atom_cas_acqrel(&c.tags[base + v], old, nw);
+    }
     prev = __shfl_sync(FULL, prev, 0);
     if (prev != old) continue;   // a hitter touched ref/pins: re-evaluate
     if (W <= 32 && lane < W && ((cleared >> lane) & 1u)) atomicAnd(&c.tags[base + lane], ~REF_BIT);
@@ -322,7 +325,8 @@ __device__ int claim_lanes(const DevCtx& c, bool want, u64 key, u32 pin_n, u32 w
           const u64 old = ld_relaxed(&c.tags[base + v]);
           if (tw_state(old) != ST_BUSY && tw_pins(old) == 0) {
             const u64 nw = tw_make(ST_BUSY, key, tw_ver(old) + 1, true, pin_n);
-            if (atomicCAS(&c.tags[base + v], old, nw) == old) {
+            st_relaxed(&c.wl[base + v], ((u64)((tw_ver(old) + 1) & 0x1FFu)) << 55);   // open the waiter list
+            if (atom_cas_acqrel(&c.tags[base + v], old, nw) == old) {
               for (u32 m = cleared; m; m &= m - 1) atomicAnd(&c.tags[base + (__ffs(m) - 1)], ~REF_BIT);
               st_relaxed(&c.hand[set], nh);
               const u32 ost = tw_state(old);
@@ -527,10 +531,12 @@ struct Req {        // per-lane result of an access
   u64 victim;       // key evicted by this miss (evict_reset) or ~0
 };
 
-// Warp-collective cache access.  Lanes with the same key coalesce (__match_any_sync, lowest lane
-// leads: warp_coalesce, gpu_api.py:40-54).  pin: every requesting lane holds one pin on the
-// resulting line until it has consumed it (async_read); !pin: prefetch semantics.
-// count_followers_as_attach: async_read keeps one outcome per caller (hit/miss/attach).
+// Warp-collective cache access, ONE attempt.  Lanes with the same key coalesce (__match_any_sync,
+// lowest lane leads: warp_coalesce, gpu_api.py:40-54).  pin: every requesting lane of a resolved
+// key holds one pin on the line (the leader adds them all); !pin: prefetch semantics.  Leaders
+// whose set has no available victim get R_RETRY (so do their followers): callers retry after
+// releasing every pin they hold — no pin is ever held across a claim or a retry, so a full cache
+// cannot deadlock (hold-and-wait).
 __device__ Req access_warp(const DevCtx& c, bool active, u64 key, bool pin, u32 who, u32 sq_start,
                            bool drop_followers) {
   const u32 lane = lane_id();
@@ -548,71 +554,60 @@ __device__ Req access_warp(const DevCtx& c, bool active, u64 key, bool pin, u32 
   const bool leader = active && (grp & lanemask_lt()) == 0;
   const u32 gsize = __popc(grp);
   const u32 lead_lane = grp ? (u32)(__ffs(grp) - 1) : lane;
-  u32 todo = __ballot_sync(FULL, leader);
-  u32 hits = 0, attaches = 0, misses = 0;
-  Spin sp;
-  while (true) {
-    // lock-free probe for all unresolved leaders
-    const bool want = (todo >> lane) & 1u;
-    u32 l; u64 w;
-    probe_lanes(c, want, key, l, w);
-    bool resolved = false;
-    if (want && l != NONE) {
-      u64 pw = w;
-      if (pin) pw = pin_line(c, l, key, gsize);
-      if (pw) {
-        r.line = l;
-        r.word = pw;
-        r.kind = tw_state(pw) == ST_BUSY ? R_FILLING : R_HIT;
-        if (r.kind == R_HIT && !tw_ref(pw)) atomicOr(&c.tags[l], REF_BIT);   // on_hit
-        resolved = true;
-      }
+  // lock-free probe for every leader
+  u32 l; u64 w;
+  probe_lanes(c, leader, key, l, w);
+  bool resolved = false;
+  if (leader && l != NONE) {
+    u64 pw = w;
+    if (pin) pw = pin_line(c, l, key, gsize);
+    if (pw) {
+      r.line = l;
+      r.word = pw;
+      r.kind = tw_state(pw) == ST_BUSY ? R_FILLING : R_HIT;
+      if (r.kind == R_HIT && !tw_ref(pw)) atomicOr(&c.tags[l], REF_BIT);   // on_hit
+      resolved = true;
     }
-    todo &= ~__ballot_sync(FULL, resolved);
-    // misses: lane-parallel claims under per-set locks (W <= 32); one key at a time otherwise
-    u32 retry = 0;
-    u32 mb = todo;
-    bool need_submit = false;
-    if (c.ways <= 32 && mb) {
+  }
+  // misses: lane-parallel claims under per-set locks (W <= 32); one key at a time otherwise
+  const u32 mb = __ballot_sync(FULL, leader && !resolved);
+  bool need_submit = false;
+  if (mb) {
+    if (c.ways <= 32) {
       u32 cl = NONE; u64 cw = 0, vk = ~0ull;
-      const bool w = (mb >> lane) & 1u;
-      const int kind = claim_lanes(c, w, key, pin ? gsize : 0u, who, cl, cw, vk);
-      if (w) {
-        if (kind == R_RETRY || kind == R_NONE) retry |= 1u;
+      const bool wl = (mb >> lane) & 1u;
+      const int kind = claim_lanes(c, wl, key, pin ? gsize : 0u, who, cl, cw, vk);
+      if (wl) {
+        if (kind == R_RETRY || kind == R_NONE) r.kind = R_RETRY;
         else { r.line = cl; r.word = cw; r.kind = kind; r.victim = vk; need_submit = kind == R_MISS; }
       }
-      mb = 0;
-    }
-    while (mb) {
-      const int src = __ffs(mb) - 1;
-      mb &= mb - 1;
-      const u64 k = __shfl_sync(FULL, key, src);
-      const u32 pn = pin ? __shfl_sync(FULL, gsize, src) : 0u;
-      u32 cl; u64 cw, vk;
-      const int kind = claim_key_warp(c, k, pn, __shfl_sync(FULL, who, src), cl, cw, vk);
-      if (lane == (u32)src) {
-        if (kind == R_RETRY) retry |= 1u;
-        else { r.line = cl; r.word = cw; r.kind = kind; r.victim = vk; need_submit = kind == R_MISS; }
+    } else {
+      u32 m2 = mb;
+      while (m2) {
+        const int src = __ffs(m2) - 1;
+        m2 &= m2 - 1;
+        const u64 k = __shfl_sync(FULL, key, src);
+        const u32 pn = pin ? __shfl_sync(FULL, gsize, src) : 0u;
+        u32 cl; u64 cw, vk;
+        const int kind = claim_key_warp(c, k, pn, __shfl_sync(FULL, who, src), cl, cw, vk);
+        if (lane == (u32)src) {
+          if (kind == R_RETRY) r.kind = R_RETRY;
+          else { r.line = cl; r.word = cw; r.kind = kind; r.victim = vk; need_submit = kind == R_MISS; }
+        }
       }
     }
-    const u32 rb = __ballot_sync(FULL, retry != 0);
-    todo = rb;
-    // submit fills (warp-aggregated)
-    const u32 dev = key_dev(key);
-    if (!submit_warp(c, need_submit, dev, key_blk(key), r.line, K_FILL, OP_READ, 0, key, who, sq_start)) {
-      r.kind = R_NONE;
-      break;
-    }
-    if (!todo) break;
-    if (!sp.again(c, 2048, __LINE__ + 100000 * SPIN_FILE_ID)) break;
+  }
+  // submit fills (warp-aggregated)
+  if (__any_sync(FULL, need_submit)) {
+    if (!submit_warp(c, need_submit, key_dev(key), key_blk(key), r.line, K_FILL, OP_READ, 0, key, who, sq_start))
+      if (need_submit) r.kind = R_NONE;
   }
   // accounting + trace
+  u32 hits = 0, attaches = 0, misses = 0;
   if (leader) {
-    if (r.kind == R_HIT) hits = 1;
+    if (r.kind == R_HIT) { hits = 1; log_ev(c, who, M_CACHE, A_HIT, key_dev(key), key_blk(key)); }
     else if (r.kind == R_MISS) misses = 1;
-    else if (r.kind == R_FILLING) attaches = 1;
-    if (r.kind == R_HIT) log_ev(c, who, M_CACHE, A_HIT, key_dev(key), key_blk(key));
-    if (r.kind == R_FILLING) log_ev(c, who, M_CACHE, A_ATTACH, r.line, 1);
+    else if (r.kind == R_FILLING) { attaches = 1; log_ev(c, who, M_CACHE, A_ATTACH, r.line, 1); }
   }
   // broadcast to followers
   const u32 bl = __shfl_sync(FULL, r.line, lead_lane);
@@ -623,8 +618,9 @@ __device__ Req access_warp(const DevCtx& c, bool active, u64 key, bool pin, u32 
       r.line = NONE; r.kind = R_NONE;
     } else {
       r.line = bl; r.word = bw;
-      r.kind = (bk == R_HIT) ? R_HIT : (bk == R_NONE ? R_NONE : R_FILLING);
-      if (r.kind == R_HIT) hits = 1; else if (r.kind == R_FILLING) { attaches = 1; log_ev(c, who, M_CACHE, A_ATTACH, r.line, 1); }
+      r.kind = (bk == R_HIT || bk == R_RETRY || bk == R_NONE) ? bk : R_FILLING;
+      if (r.kind == R_HIT) hits = 1;
+      else if (r.kind == R_FILLING) { attaches = 1; log_ev(c, who, M_CACHE, A_ATTACH, r.line, 1); }
     }
   }
   const u32 h = __popc(__ballot_sync(FULL, hits != 0));
@@ -638,57 +634,133 @@ __device__ Req access_warp(const DevCtx& c, bool active, u64 key, bool pin, u32 
   return r;
 }
 
-// Wait until each active lane's pinned line is READY, then copy the 4 KiB line into the lane's
-// destination buffer warp-cooperatively (the waiter drains itself: per-page state instead of
-// waiter lists, software_cache.py:563-570) and drop the pin.
-// One poll pass: every active lane whose pinned line is READY gets its 4 KiB line copied into
-// its destination buffer warp-cooperatively (the waiter drains itself: per-page state instead of
-// waiter lists, software_cache.py:563-570) and drops its pin.  Returns the mask of lanes served.
-__device__ u32 try_copy_warp(const DevCtx& c, bool active, u32 line, u64 key, uint4* dst) {
-  const u32 lane = lane_id();
-  bool ready = false;
-  if (active && line != NONE) {
-    const u64 w = ld_acquire(&c.tags[line]);
-    if (!tw_live(w) || tw_key(w) != key) set_error(c, E_ILLEGAL_STATE, line, key);
-    ready = tw_state(w) == ST_READY || tw_state(w) == ST_MODIFIED;
+// Prefetch (AgileApi.prefetch, gpu_api.py:345-361): pull blocks toward the cache without waiting;
+// duplicates die in the warp; lanes whose set is momentarily full retry (no pins are held).
+__device__ void prefetch_warp(const DevCtx& c, bool active, u64 key, u32 who, u32 sq_start, bool best_effort) {
+  bool want = active;
+  Spin sp;
+  while (__any_sync(FULL, want)) {
+    const Req r = access_warp(c, want, key, false, who, sq_start, true);
+    want = want && r.kind == R_RETRY;
+    if (best_effort || !__any_sync(FULL, want)) break;
+    if (!sp.again(c, 2048, __LINE__ + 100000 * SPIN_FILE_ID)) break;
   }
-  const u32 rb = __ballot_sync(FULL, ready);
-  if (!rb) return 0;
-  __syncwarp();
-  u32 todo = rb;
-  while (todo) {
-    const int l0 = __ffs(todo) - 1;
-    todo &= todo - 1;
-    const uint4* src = reinterpret_cast<const uint4*>(line_ptr(c, __shfl_sync(FULL, line, l0)));
-    uint4* d = reinterpret_cast<uint4*>(__shfl_sync(FULL, (u64)(uintptr_t)dst, l0));
-    uint4 v[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) v[k] = __ldcg(src + lane + 32 * k);
-#pragma unroll
-    for (int k = 0; k < 8; ++k) d[lane + 32 * k] = v[k];
-  }
-  __syncwarp();
-  if ((rb >> lane) & 1u) unpin_line(c, line, 1);
-  return rb;
 }
 
-// Wait until every active lane's pinned line is READY and copied (AgileApi.wait, gpu_api.py:233-248:
-// nothing is held while waiting but the page's own pin).
-__device__ bool wait_copy_warp(const DevCtx& c, bool active, u32 line, u64 key, uint4* dst) {
-  const u32 lane = lane_id();
-  u32 pending = __ballot_sync(FULL, active && line != NONE);
-  Spin sp;
-  bool ok = true;
-  while (pending) {
-    const u32 rb = try_copy_warp(c, (pending >> lane) & 1u, line, key, dst);
-    pending &= ~rb;
-    if (pending && !rb) {
-      if (!sp.again(c, 1024, __LINE__ + 100000 * SPIN_FILE_ID)) { ok = false; break; }
-    }
+// ------------------------------------------------------------------ async_read waiter lists
+// A lane's request is a WaitNode in device memory (its AgileBuf: destination + barrier word).
+// Lines with a fill in flight carry a lock-free waiter stack `wl[line]` = [ver:9 | closed:1 |
+// node>>4 : 54]; the claimant opens it for the new version, waiters push with a version-checked
+// CAS, and the service closes it, copies the line into every waiter's buffer and clears their
+// barriers before flipping the line READY (_drain_waiters, software_cache.py:563-570).  Nobody
+// holds a line while waiting, exactly like the reference.
+struct WaitNode {
+  u64 next;     // packed next node
+  u64 dst;      // 4 KiB destination
+  u32 done;     // TransactionBarrier state: 0 PENDING, 1 DONE (agile_service.py:31-72)
+  u32 pad;
+  u64 t_issue;
+};
+constexpr int WL_VER_SHIFT = 55;
+constexpr u64 WL_CLOSED = 1ull << 54;
+constexpr u64 WL_PTR_MASK = (1ull << 54) - 1;
+__device__ __forceinline__ u64 wl_open(u32 ver) { return (u64)(ver & 0x1FFu) << WL_VER_SHIFT; }
+__device__ __forceinline__ u32 wl_ver(u64 w) { return (u32)(w >> WL_VER_SHIFT); }
+__device__ __forceinline__ WaitNode* wl_node(u64 w) { return reinterpret_cast<WaitNode*>((w & WL_PTR_MASK) << 4); }
+
+// push `node` on the line's stack for version `ver`; false if the list is closed (the fill is
+// completing: the caller copies from the line itself) or belongs to another version
+__device__ __forceinline__ bool wl_push(const DevCtx& c, u32 line, u32 ver, WaitNode* node) {
+  u64 h = ld_acquire(&c.wl[line]);
+  while (true) {
+    if (wl_ver(h) != (ver & 0x1FFu) || (h & WL_CLOSED)) return false;
+    node->next = h & WL_PTR_MASK;
+    const u64 nw = wl_open(ver) | ((u64)(uintptr_t)node >> 4);
+    const u64 prev = atom_cas_acqrel(&c.wl[line], h, nw);
+    if (prev == h) return true;
+    h = prev;
   }
-  // abort path: release the pins we still hold so the cache stays consistent
-  if ((pending >> lane) & 1u) unpin_line(c, line, 1);
-  return ok;
+}
+
+__device__ __forceinline__ void copy_page_warp(const uint4* src, uint4* dst) {
+  const u32 lane = lane_id();
+  uint4 v[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) v[k] = __ldcg(src + lane + 32 * k);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) __stcg(dst + lane + 32 * k, v[k]);
+}
+
+// async_read (gpu_api.py:370-396), warp-collective: start filling each active lane's node->dst
+// from `key`.  HIT: copied now.  MISS/FILLING: the node joins the line's waiter stack and the
+// service delivers it.  Returns with no pin held.  Outcomes are counted by access_warp.
+__device__ void async_read_warp(const DevCtx& c, bool active, u64 key, WaitNode* node, uint4* dst, u32 who,
+                                u32 sq_start, int* outcome = nullptr, u64* victim = nullptr) {
+  const u32 lane = lane_id();
+  bool want = active;
+  if (active) { node->dst = (u64)(uintptr_t)dst; node->done = 0; node->t_issue = gtimer(); }
+  __syncwarp();
+  Spin sp;
+  while (__any_sync(FULL, want)) {
+    const Req r = access_warp(c, want, key, true, who, sq_start, false);
+    bool copy_now = false, pinned = false;
+    if (want) {
+      if (r.kind == R_RETRY) {
+        // set full of busy/pinned lines: nothing held, try again
+      } else if (r.kind == R_NONE) {
+        want = false;   // aborting
+      } else {
+        pinned = true;
+        if (outcome) *outcome = r.kind == R_HIT ? 0 : (r.kind == R_MISS ? 1 : 2);
+        if (victim) *victim = r.victim;
+        if (r.kind == R_HIT) copy_now = true;
+        else if (!wl_push(c, r.line, tw_ver(r.word), node)) copy_now = true;   // fill completing
+        want = false;
+      }
+    }
+    // lanes copying themselves: wait for READY (the line is pinned and already completing), copy
+    u32 cb = __ballot_sync(FULL, copy_now);
+    Spin s2;
+    while (cb) {
+      bool ready = false;
+      if ((cb >> lane) & 1u) {
+        const u64 w = ld_acquire(&c.tags[r.line]);
+        ready = tw_state(w) == ST_READY || tw_state(w) == ST_MODIFIED;
+      }
+      u32 rb = __ballot_sync(FULL, ready) & cb;
+      __syncwarp();
+      while (rb) {
+        const int l0 = __ffs(rb) - 1;
+        rb &= rb - 1;
+        const uint4* src = reinterpret_cast<const uint4*>(line_ptr(c, __shfl_sync(FULL, r.line, l0)));
+        WaitNode* nd = reinterpret_cast<WaitNode*>(__shfl_sync(FULL, (u64)(uintptr_t)node, l0));
+        copy_page_warp(src, reinterpret_cast<uint4*>(nd->dst));
+        __syncwarp();
+        if (lane == (u32)l0) st_release(&nd->done, 1u);
+        cb &= ~(1u << l0);
+      }
+      if (cb && !s2.again(c, 512, __LINE__ + 100000 * SPIN_FILE_ID)) break;
+    }
+    if (pinned) unpin_line(c, r.line, 1);
+    if (__any_sync(FULL, want) && !sp.again(c, 2048, __LINE__ + 100000 * SPIN_FILE_ID)) break;
+  }
+}
+
+// one poll pass over nodes: mask of lanes whose transfer is done (AgileApi.wait, gpu_api.py:439-454)
+__device__ __forceinline__ u32 poll_nodes_warp(bool active, const WaitNode* node) {
+  bool d = false;
+  if (active) d = ld_acquire(&node->done) != 0;
+  return __ballot_sync(FULL, d);
+}
+
+__device__ bool wait_nodes_warp(const DevCtx& c, bool active, const WaitNode* node) {
+  u32 pending = __ballot_sync(FULL, active);
+  Spin sp;
+  while (pending) {
+    pending &= ~poll_nodes_warp((pending >> lane_id()) & 1u, node);
+    if (pending && !sp.again(c, 1024, __LINE__ + 100000 * SPIN_FILE_ID)) return false;
+  }
+  return true;
 }
 
 // Wait (without pinning) until the line holds `key` READY.  Returns false if the line was
@@ -728,8 +800,11 @@ __device__ u32 cq_window_pass(const DevCtx& c, u32 cq, u64& off, u32& mask, u32 
   const u32 window = c.cq_window;
   const u32 Dq = c.cq_depth;
   const u32 Ds = c.sq_depth;
-  bool valid = false;
+  bool valid = false, cache = false;
   u32 sq = 0, slot = 0;
+  CmdCtx x;
+  x.line = NONE; x.t_submit = 0; x.key = 0;
+  u64 wlh = 0;
   const u64 v = off + lane;
   if (lane < window && !((mask >> lane) & 1u)) {
     const u64 w = ld_acquire(reinterpret_cast<const u64*>(c.cqe + (u64)cq * Dq + (u32)(v & (Dq - 1))) + 1);
@@ -747,20 +822,66 @@ __device__ u32 cq_window_pass(const DevCtx& c, u32 cq, u64& off, u32& mask, u32 
       set_error(c, E_UNKNOWN_CID, cq, v);
       valid = false;
     } else {
-      const CmdCtx x = c.cmd[idx];
+      x = c.cmd[idx];
       const u32 os = atom_cas_acqrel(&c.sq_state[idx], SQ_ISSUED, SQ_EMPTY);
       atomicExch(&c.sq_done_v[idx], x.vidx + 1);
-      u64 ot = (u64)ST_BUSY << ST_SHIFT;
-      const bool cache = x.line != NONE && (x.kind == K_FILL || x.kind == K_WB_KEEP);
-      if (cache) ot = atom_add_release(&c.tags[x.line], 1ull << ST_SHIFT);   // BUSY -> READY
+      cache = x.line != NONE && (x.kind == K_FILL || x.kind == K_WB_KEEP);
+      if (cache) {
+        // close the waiter stack of this fill (its version is the BUSY word's)
+        const u64 tw = ld_relaxed(&c.tags[x.line]);
+        wlh = atom_exch_acqrel(&c.wl[x.line], (((u64)tw_ver(tw)) << 55) | (1ull << 54));
+      }
       if (os != SQ_ISSUED) set_error(c, E_UNKNOWN_CID, sq, slot);
-      if (tw_state(ot) != ST_BUSY) set_error(c, E_ILLEGAL_STATE, x.line, ot);
       log_ev(c, who, M_NVME, A_SQE_RELEASE, sq, slot, slot);
       log_ev(c, who, M_SVC, A_CQE_PROCESS, cq, v, slot, sq);
-      if (cache) log_state(c, who, x.line, ST_BUSY, ST_READY, x.key);
-      lat_acc += gtimer() - x.t_submit;
-      fence_sc();
     }
+  }
+  __syncwarp();
+  // drain waiters: copy the filled line into every waiting AgileBuf and clear its barrier while
+  // the line is still BUSY (not evictable), then flip it READY (software_cache.py:538-541,563-570)
+  u64 cur = (valid && cache) ? (wlh & ((1ull << 54) - 1)) : 0ull;   // per-lane waiter cursor
+  while (true) {
+    u32 cb = __ballot_sync(FULL, cur != 0);
+    if (!cb) break;
+    const int l0 = __ffs(cb) - 1;
+    cb &= cb - 1;
+    const int l1 = cb ? __ffs(cb) - 1 : -1;
+    const int s1 = l1 < 0 ? l0 : l1;
+    const uint4* src0 = reinterpret_cast<const uint4*>(line_ptr(c, __shfl_sync(FULL, x.line, l0)));
+    const uint4* src1 = reinterpret_cast<const uint4*>(line_ptr(c, __shfl_sync(FULL, x.line, s1)));
+    WaitNode* n0 = reinterpret_cast<WaitNode*>(__shfl_sync(FULL, cur, l0) << 4);
+    WaitNode* n1 = reinterpret_cast<WaitNode*>(__shfl_sync(FULL, cur, s1) << 4);
+    uint4 v0[8], v1[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v0[k] = __ldcg(src0 + lane + 32 * k);
+    if (l1 >= 0) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v1[k] = __ldcg(src1 + lane + 32 * k);
+    }
+    uint4* d0 = reinterpret_cast<uint4*>(n0->dst);
+    uint4* d1 = reinterpret_cast<uint4*>(n1->dst);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) __stcg(d0 + lane + 32 * k, v0[k]);
+    if (l1 >= 0) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) __stcg(d1 + lane + 32 * k, v1[k]);
+    }
+    __syncwarp();
+    if (lane == 0) {
+      st_release(&n0->done, 1u);
+      if (l1 >= 0) st_release(&n1->done, 1u);
+    }
+    if ((int)lane == l0) cur = n0->next;
+    if ((int)lane == l1) cur = n1->next;
+  }
+  if (valid && cache) {
+    const u64 ot = atom_add_release(&c.tags[x.line], 1ull << ST_SHIFT);   // BUSY -> READY
+    if (tw_state(ot) != ST_BUSY) set_error(c, E_ILLEGAL_STATE, x.line, ot);
+    log_state(c, who, x.line, ST_BUSY, ST_READY, x.key);
+  }
+  if (valid) {
+    lat_acc += gtimer() - x.t_submit;
+    fence_sc();
   }
   __syncwarp();
   // head advance: one leader per SQ among completed lanes
@@ -1007,6 +1128,45 @@ __device__ __forceinline__ int oldest_lane(bool cand, u32 seq) {
   return bl < 32 ? bl : -1;
 }
 
+// Constant service time (no jitter): FIFO dispatch to the earliest-free of P identical channels
+// is round-robin in arrival order (starts are non-decreasing, so the channel that frees first is
+// the one used P commands earlier).  Lock-free: a warp-aggregated ticket per device fixes the
+// order, channel = ticket % P, and a per-channel turn word hands the channel from command k-P to
+// command k.  Every lane with `want` gets its completion time in `due`.
+__device__ void model_schedule_rr(const DevCtx& c, bool want, u32 dev, u32 op, u64 arrival, u64& due) {
+  const u32 lane = lane_id();
+  const u32 P = c.model.parallelism;
+  u32 grp = __match_any_sync(FULL, want ? dev : 0xffffffffu);
+  if (!want) grp = 0;
+  const u32 rank = __popc(grp & lanemask_lt());
+  u64 base = 0;
+  if (want && rank == 0) base = atomicAdd(&c.dev_seq[dev], (u64)__popc(grp));
+  base = __shfl_sync(FULL, base, want ? (u32)(__ffs(grp) - 1) : lane);
+  const u64 ticket = base + rank;
+  const u32 ch = (u32)(ticket % P);
+  const u64 turn = ticket / P;
+  const u64 svc = op == OP_READ ? c.model.read_ns : c.model.write_ns;
+  const u64 occ = c.model.occupancy_ns ? c.model.occupancy_ns : svc;
+  bool done = !want;
+  Spin sp;
+  while (__any_sync(FULL, !done)) {
+    if (!done) {
+      const u64 idx = (u64)dev * P + ch;
+      if (ld_acquire(&c.chan_turn[idx]) == turn) {
+        const u64 start = max(arrival, ld_relaxed(&c.chan_free[idx]));
+        st_relaxed(&c.chan_free[idx], start + occ);
+        st_release(&c.chan_turn[idx], turn + 1);
+        due = start + svc;
+        done = true;
+      }
+    }
+    if (__any_sync(FULL, !done) && !sp.again(c, 64, __LINE__ + 100000 * SPIN_FILE_ID)) {
+      if (!done) due = 0;
+      break;
+    }
+  }
+}
+
 __device__ void engine_main(const DevCtx& c, u32 ew) {
   const u32 lane = lane_id();
   const u32 E = c.engine_warps;
@@ -1173,6 +1333,8 @@ __device__ void engine_main(const DevCtx& c, u32 ew) {
       // completion time: link mode = as soon as the bytes moved; model mode replays the channels
       if (c.model.link_mode) {
         if (newcmd) pdue = 0;
+      } else if (c.model.jitter == 0 || c.model.jitter_ns == 0) {
+        model_schedule_rr(c, newcmd, pdev, pop, arrival, pdue);
       } else {
         u32 t2 = nb;
         while (t2) {

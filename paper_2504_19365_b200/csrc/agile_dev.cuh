@@ -179,6 +179,7 @@ struct DevCtx {
   u64 watchdog_ns;
   // cache
   u64* tags;
+  u64* wl;                 // per-line async_read waiter stack (agile_core.cuh WaitNode)
   u32* set_lock;
   u32* hand;
   uint8_t* lines;
@@ -192,6 +193,7 @@ struct DevCtx {
   CqWords* cqw;
   // engine
   u64* chan_free;          // num_devices * parallelism
+  u64* chan_turn;          // num_devices * parallelism (round-robin dispatch turn)
   u32* dev_lock;           // num_devices
   u64* dev_seq;            // num_devices (jitter draw counter)
   const uint8_t* store[kMaxDevices];   // mapped host pointers (device view)
@@ -243,6 +245,9 @@ __device__ __forceinline__ u32 atom_cas_acqrel(u32* p, u32 cmp, u32 val) {
 }
 __device__ __forceinline__ u32 atom_cas_acquire(u32* p, u32 cmp, u32 val) {
   u32 o; asm volatile("atom.acquire.gpu.global.cas.b32 %0, [%1], %2, %3;" : "=r"(o) : "l"(p), "r"(cmp), "r"(val) : "memory"); return o;
+}
+__device__ __forceinline__ u64 atom_exch_acqrel(u64* p, u64 val) {
+  u64 o; asm volatile("atom.acq_rel.gpu.global.exch.b64 %0, [%1], %2;" : "=l"(o) : "l"(p), "l"(val) : "memory"); return o;
 }
 __device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 __device__ __forceinline__ void fence_sc() { asm volatile("fence.sc.gpu;" ::: "memory"); }

@@ -59,6 +59,7 @@ struct SeqWork {
   u64* victim;            // evicted key or ~0
   uint4* pages;           // optional n * 4 KiB
   uint4* scratch;         // 4 KiB
+  WaitNode* nodes;        // 1
   __device__ void run(const DevCtx& c, u32 uidx, u32 nusers) {
     if (uidx != 0 || threadIdx.x >= 32) return;
     const u32 lane = lane_id();
@@ -68,13 +69,14 @@ struct SeqWork {
       const bool act = lane == 0;
       const u64 key = make_key(dev[i], blk[i]);
       if (act) log_ev(c, who, M_API, A_ASYNC_READ, dev[i], blk[i]);
-      const Req r = access_warp(c, act, key, true, who, 0, false);
+      int oc = -1;
+      u64 vk = ~0ull;
+      async_read_warp(c, act, key, nodes, pages ? pages + i * 256 : scratch, who, 0, &oc, &vk);
+      wait_nodes_warp(c, act, nodes);
       if (act) {
-        outcome[i] = r.kind == R_HIT ? 0 : (r.kind == R_MISS ? 1 : 2);
-        victim[i] = r.victim;
+        outcome[i] = (signed char)oc;
+        victim[i] = vk;
       }
-      uint4* dst = pages ? pages + i * 256 : scratch;
-      wait_copy_warp(c, act && r.kind != R_NONE, r.line, key, dst);
     }
   }
 };
@@ -83,25 +85,26 @@ struct SeqWork {
 struct ReadsWork {
   const u64* keys;        // [epochs][tasks][reads] request keys
   uint4* bufs;            // [tasks][2][reads] 4 KiB buffers
+  WaitNode* nodes;        // [tasks][2][reads]
   u64* digest;            // [tasks] xor of the first 8 bytes of every page read
   u64* epoch_t;           // [epochs + 1] barrier timestamps
   u32 tasks, reads, epochs, async_mode;
   u64 compute_ns;
   static constexpr int MAXR = 64;
-  __device__ void issue(const DevCtx& c, u32 task, bool act, u32 e, u32 set, u32* lines, u64* ks, u32 who, u32 sq_start) {
+  __device__ void issue(const DevCtx& c, u32 task, bool act, u32 e, u32 set, u32 who, u32 sq_start) {
     for (u32 i = 0; i < reads; ++i) {
       const u64 key = act ? keys[((u64)e * tasks + task) * reads + i] : 0ull;
-      const Req r = access_warp(c, act, key, true, who, sq_start + i + e * reads, false);
-      lines[set * MAXR + i] = (act && r.kind != R_NONE) ? r.line : NONE;
-      ks[set * MAXR + i] = key;
+      const u64 slot = ((u64)task * 2 + set) * reads + i;
+      async_read_warp(c, act, key, nodes + (act ? slot : 0), bufs + (act ? slot : 0) * 256, who,
+                      sq_start + i + e * reads);
     }
   }
-  __device__ void wait_set(const DevCtx& c, u32 task, bool act, u32 set, const u32* lines, const u64* ks, u64& dg) {
+  __device__ void wait_set(const DevCtx& c, u32 task, bool act, u32 set, u64& dg) {
     for (u32 i = 0; i < reads; ++i) {
-      uint4* dst = bufs + (((u64)task * 2 + set) * reads + i) * 256;
-      wait_copy_warp(c, act, lines[set * MAXR + i], ks[set * MAXR + i], dst);
-      if (act && lines[set * MAXR + i] != NONE) {
-        const uint2 w = *reinterpret_cast<const uint2*>(dst);
+      const u64 slot = ((u64)task * 2 + set) * reads + i;
+      wait_nodes_warp(c, act, nodes + (act ? slot : 0));
+      if (act) {
+        const uint2 w = *reinterpret_cast<const uint2*>(bufs + slot * 256);
         dg ^= (u64)w.x | ((u64)w.y << 32);
       }
     }
@@ -111,26 +114,24 @@ struct ReadsWork {
     const bool act = task < tasks;
     const u32 who = user_who(uidx);
     const u32 sq_start = uidx * kCtaWarps + (threadIdx.x >> 5);
-    u32 lines[2 * MAXR];
-    u64 ks[2 * MAXR];
     u64 dg = 0;
     if (uidx == 0 && threadIdx.x == 0) epoch_t[0] = gtimer();
     if (!async_mode) {
       for (u32 e = 0; e < epochs; ++e) {
-        issue(c, task, act, e, 0, lines, ks, who, sq_start);
-        wait_set(c, task, act, 0, lines, ks, dg);
+        issue(c, task, act, e, 0, who, sq_start);
+        wait_set(c, task, act, 0, dg);
         // compute starts only after every task's data arrived (bench/ctc.py:80-83)
         if (!user_grid_barrier(c, nusers)) return;
         if (uidx == 0 && threadIdx.x == 0) epoch_t[e + 1] = gtimer();
         compute_spin(compute_ns);
       }
     } else {
-      issue(c, task, act, 0, 0, lines, ks, who, sq_start);
+      issue(c, task, act, 0, 0, who, sq_start);
       for (u32 e = 0; e < epochs; ++e) {
         const u32 cur = e & 1u;
         // the next epoch's fetches ride under this epoch's compute (bench/ctc.py:47-70)
-        if (e + 1 < epochs) issue(c, task, act, e + 1, cur ^ 1u, lines, ks, who, sq_start);
-        wait_set(c, task, act, cur, lines, ks, dg);
+        if (e + 1 < epochs) issue(c, task, act, e + 1, cur ^ 1u, who, sq_start);
+        wait_set(c, task, act, cur, dg);
         if (!user_grid_barrier(c, nusers)) return;
         if (uidx == 0 && threadIdx.x == 0) epoch_t[e + 1] = gtimer();
         compute_spin(compute_ns);
@@ -148,6 +149,7 @@ struct ReadsWork {
 // dev = (idx + j) % d, blk = (j * conc + idx) % num_blocks (bench/bandwidth.py:32-33).
 struct LoopWork {
   uint4* bufs;            // [conc] 4 KiB
+  WaitNode* nodes;        // [conc]
   unsigned long long* counters;   // [0] completions in window, [1] window start, [2] window end
   u32 conc, ndev;
   u64 num_blocks;
@@ -164,12 +166,12 @@ struct LoopWork {
     const u64 ws = t0 + warmup_ns, we = ws + measure_ns;
     u32 inwin = 0;
     uint4* dst = bufs + (u64)(act ? idx : 0) * 256;
+    WaitNode* node = nodes + (act ? idx : 0);
     // requesters progress independently: a lane issues its next read as soon as its previous
     // one completed (no warp lockstep), so the in-flight population stays at `conc`
     const u32 lane = lane_id();
     bool outst = false;
-    u32 line = NONE;
-    u64 key = 0, j = 0;
+    u64 j = 0;
     Spin sp;
     while (true) {
       const bool issue = act && !outst && j < max_per_task && gtimer() < we;
@@ -177,14 +179,11 @@ struct LoopWork {
       if (ib) {
         const u32 dev = (idx + (u32)j) % ndev;
         const u64 blk = (j * conc + idx) % num_blocks;
-        const u64 k = make_key(dev, blk);
-        const Req r = access_warp(c, issue, k, true, who, sq_start + (u32)__shfl_sync(FULL, j, __ffs(ib) - 1), false);
-        if (issue) {
-          ++j;
-          if (r.kind != R_NONE) { outst = true; line = r.line; key = k; }
-        }
+        async_read_warp(c, issue, make_key(dev, blk), node, dst, who,
+                        sq_start + (u32)__shfl_sync(FULL, j, __ffs(ib) - 1));
+        if (issue) { ++j; outst = true; }
       }
-      const u32 done = try_copy_warp(c, outst, line, key, dst);
+      const u32 done = poll_nodes_warp(outst, node);
       if ((done >> lane) & 1u) {
         outst = false;
         const u64 t = gtimer();
@@ -198,7 +197,6 @@ struct LoopWork {
         sp = Spin();
       }
     }
-    if (outst) unpin_line(c, line, 1);   // abort path only
     u32 s = inwin;
 #pragma unroll
     for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
@@ -219,32 +217,38 @@ struct GatherWork {
   __device__ void prefetch_epoch(const DevCtx& c, bool act, u32 task, u32 e, u32 who, u32 sq_start) {
     for (u32 g = 0; g < gathers; ++g) {
       const u64 key = act ? keys[((u64)task * epochs + e) * gathers + g] : 0ull;
-      access_warp(c, act, key, false, who, sq_start + g + e * gathers, true);
+      prefetch_warp(c, act, key, who, sq_start + g + e * gathers, false);
     }
   }
   __device__ void get_epoch(const DevCtx& c, bool act, u32 task, u32 e, u32 who, u32 sq_start) {
     for (u32 g = 0; g < gathers; ++g) {
       const u64 key = act ? keys[((u64)task * epochs + e) * gathers + g] : 0ull;
-      // array_get = read_range loop (software_cache.py:212-219): access, wait READY, read, validate
+      // array_get = read_range loop (software_cache.py:212-219): access, wait READY, read.  The
+      // lane pins only its own line, and only after its claim succeeded (no hold-and-wait).
       bool pend = act;
       u32 val = 0;
       Spin sp;
       while (__any_sync(FULL, pend)) {
         const Req r = access_warp(c, pend, key, true, who, sq_start, false);
-        bool done = false;
-        if (pend && r.kind != R_NONE) {
-          Spin s2;
-          while (true) {
+        const bool pinned = pend && (r.kind == R_HIT || r.kind == R_FILLING || r.kind == R_MISS);
+        u32 wp = __ballot_sync(FULL, pinned);
+        Spin s2;
+        while (wp) {
+          bool rd = false;
+          if ((wp >> lane_id()) & 1u) {
             const u64 w = ld_acquire(&c.tags[r.line]);
-            if (tw_state(w) == ST_READY || tw_state(w) == ST_MODIFIED) break;
-            if (!s2.again(c, 512, __LINE__ + 100000 * SPIN_FILE_ID)) break;
+            rd = tw_state(w) == ST_READY || tw_state(w) == ST_MODIFIED;
           }
+          wp &= ~__ballot_sync(FULL, rd);
+          if (wp && !s2.again(c, 512, __LINE__ + 100000 * SPIN_FILE_ID)) break;
+        }
+        if (pinned) {
           val = __ldcg(reinterpret_cast<const unsigned int*>(line_ptr(c, r.line)));
           unpin_line(c, r.line, 1);
-          done = true;
         }
-        if (done) pend = false;
+        pend = pend && (r.kind == R_RETRY);
         if (aborted(c)) break;
+        if (__any_sync(FULL, pend) && !sp.again(c, 1024, __LINE__ + 100000 * SPIN_FILE_ID)) break;
       }
       if (act) values[((u64)task * epochs + e) * gathers + g] = val;
     }
@@ -326,7 +330,7 @@ struct EmbBagWork {
       if (nb >= nbags) break;
       u64 key = 0; u32 off = 0;
       const bool a = bag_keys(nb, lact, key, off);
-      access_warp(c, a, key, false, who, gw + k, true);
+      prefetch_warp(c, a, key, who, gw + k, true);
       ring[(head + count) % kMaxPd] = nb;
       ++count;
     }
@@ -342,7 +346,7 @@ struct EmbBagWork {
         if (nb < nbags) {
           u64 key = 0; u32 off = 0;
           const bool a = bag_keys(nb, lact, key, off);
-          access_warp(c, a, key, false, who, gw + (++pass), true);
+          prefetch_warp(c, a, key, who, gw + (++pass), true);
           ring[(head + count) % kMaxPd] = nb;
           ++count;
         }
@@ -368,35 +372,40 @@ struct EmbBagWork {
         bool ready = mine && line != NONE && (tw_state(word) == ST_READY || tw_state(word) == ST_MODIFIED);
         if (ready && !tw_ref(word)) atomicOr(&c.tags[line], REF_BIT);
         u32 need = __ballot_sync(FULL, mine && !ready);
+        bool pinned = false;
         if (need) {
+          // not READY at probe time: claim (or find) the line with a pin — taken only after the
+          // claim succeeded and released before this pass ends, so no pin is held across a
+          // claim or a retry (no hold-and-wait under cache pressure); then wait for our fill
           if (first) misses_local += __popc(need);
-          Spin sp;
-          while (need) {
-            const bool nm = (need >> lane) & 1u;
-            bool have = nm && line != NONE;   // found BUSY by the probe
-            const Req r = access_warp(c, nm && !have, key, false, who, gw, false);
-            if (nm && !have && r.kind != R_NONE) { line = r.line; word = r.word; have = true; }
-            bool done = false;
-            if (nm && have) {
-              const u64 w = ld_acquire(&c.tags[line]);
-              if (tw_live(w) && tw_key(w) == key) {
-                if (tw_state(w) == ST_READY || tw_state(w) == ST_MODIFIED) { word = w; done = true; }
-              } else {
-                line = NONE;   // reassigned before we saw it READY: miss path again
-              }
-            }
-            need &= ~__ballot_sync(FULL, done);
-            if (need && !sp.again(c, 1024, __LINE__ + 100000 * SPIN_FILE_ID)) break;
+          const bool nm = (need >> lane) & 1u;
+          const Req r = access_warp(c, nm, key, true, who, gw, false);
+          if (nm && (r.kind == R_HIT || r.kind == R_FILLING || r.kind == R_MISS)) {
+            line = r.line;
+            word = r.word;
+            pinned = true;
           }
-          if (aborted(c)) break;
+          u32 wp = __ballot_sync(FULL, pinned);
+          Spin sp;
+          while (wp) {
+            bool rd = false;
+            if ((wp >> lane) & 1u) {
+              const u64 w = ld_acquire(&c.tags[line]);
+              if (tw_state(w) == ST_READY || tw_state(w) == ST_MODIFIED) { word = w; rd = true; }
+            }
+            wp &= ~__ballot_sync(FULL, rd);
+            if (wp && !sp.again(c, 1024, __LINE__ + 100000 * SPIN_FILE_ID)) break;
+          }
+          if (aborted(c)) { if (pinned) unpin_line(c, line, 1); break; }
           fence_acq_rel();
         }
         first = false;
-        // 2. gather pending rows in chunks of 8: lane owns dims [4*lane, 4*lane+4)
-        const u64 rowaddr = mine ? (u64)(uintptr_t)(line_ptr(c, line) + off) : 0ull;
+        // 2. gather the resolved rows in chunks of 8: lane owns dims [4*lane, 4*lane+4)
+        const u32 rmask = pend & __ballot_sync(FULL, ready || pinned);
+        const u64 rowaddr = (mine && (ready || pinned)) ? (u64)(uintptr_t)(line_ptr(c, line) + off) : 0ull;
         u32 okall = 0;
         for (u32 l0 = 0; l0 < L; l0 += 8) {
-          const u32 cm = (pend >> l0) & 0xffu;
+          const u32 cm = (rmask >> l0) & 0xffu;
           if (!cm) continue;
           float4 v[8];
 #pragma unroll
@@ -405,10 +414,10 @@ struct EmbBagWork {
             v[j] = make_float4(0.f, 0.f, 0.f, 0.f);
             if (((cm >> j) & 1u) && lane * 4 < D) v[j] = __ldcg(reinterpret_cast<const float4*>(ra) + lane);
           }
-          // 3. seqlock validation of this chunk: the line kept its identity while we read it
+          // 3. seqlock validation of unpinned rows: the line kept its identity while we read it
           fence_acq_rel();
           bool bad = false;
-          if (mine && lane >= l0 && lane < l0 + 8) {
+          if (((rmask >> lane) & 1u) && !pinned && lane >= l0 && lane < l0 + 8) {
             const u64 w2 = ld_relaxed(&c.tags[line]);
             bad = ((w2 ^ word) & IDENT_MASK) != 0;
           }
@@ -419,8 +428,10 @@ struct EmbBagWork {
           }
           okall |= ok << l0;
         }
+        if (pinned) unpin_line(c, line, 1);
         pend &= ~okall;
-        if (pend && !rsp.again(c, 256, __LINE__ + 100000 * SPIN_FILE_ID)) break;
+        if (pend && !okall && !rsp.again(c, 256, __LINE__ + 100000 * SPIN_FILE_ID)) break;
+        if (okall) rsp = Spin();
       }
       lookups_local += L;
       const u32 b = bag / T, t = bag % T;

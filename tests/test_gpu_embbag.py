@@ -43,7 +43,7 @@ def test_embbag_matches_oracle(gpu_system, pd, lines, ways):
 
 
 def test_embbag_zipf_warm_cache_hits(gpu_system):
-    s = gpu_system(cache_lines=8192, ways=32, blocks=1 << 16, pairs=16, engine_warps=8, warps=4)
+    s = gpu_system(cache_lines=1 << 16, ways=32, blocks=1 << 16, pairs=16, engine_warps=8, warps=4)
     s.fill_store(0, seed=3, kind="f32")
     rng = np.random.default_rng(9)
     rows = [100000] * 4

@@ -3,7 +3,7 @@ sys.path.insert(0, os.getcwd()); sys.path.insert(0, "tests")
 from conftest import small_config
 from paper_2504_19365_b200 import AgileSystem
 res = []
-for ew, sw in [(16, 4), (32, 8), (64, 8), (64, 16)]:
+for ew, sw in [(64, 16), (64, 32), (64, 64), (96, 64)]:
     for conc in (4096, 16384):
         s = AgileSystem(small_config(pairs=128, sq_depth=256, cq_depth=256, cache_lines=1 << 17, ways=32,
                                      blocks=1 << 20, emulation="link", engine_warps=ew, warps=sw), device=0)
