@@ -45,10 +45,12 @@ def _args():
     p.add_argument("--impl", default="ours", choices=("ours", "reference"))
     p.add_argument("--cache-gib", type=float, default=16.0)
     p.add_argument("--table-mult", type=float, default=4.0)
-    p.add_argument("--prefetch", type=int, default=1)
+    p.add_argument("--prefetch", type=int, default=2, help="in-kernel bag prefetch distance (0 = sync gather)")
     p.add_argument("--no-scatter", action="store_true")
     p.add_argument("--quick", action="store_true", help="skip e2e / sync / hit / cpu legs")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
+    p.add_argument("--warm-batches", type=int, default=-1,
+                   help="untimed cache warm-up batches at setup (-1: enough to fill the cache)")
     return p.parse_args()
 
 
@@ -182,7 +184,8 @@ def main():
     import torch
     import torch.distributed as dist
     from paper_2504_19365_b200 import AgileSystem, SystemConfig
-    from paper_2504_19365_b200.bench.dlrm import table_rows, make_batch, shard_tables, build_shard
+    from paper_2504_19365_b200.bench.dlrm import (table_rows, make_batch, shard_tables, build_shard,
+                                                  exchange_pooled, DlrmModel, run_pipeline, gpu_zipf_batch)
 
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
@@ -227,23 +230,16 @@ def main():
     rows = torch.from_numpy(shard.rows).to(dev)
     out = torch.empty((B, Tg, D), dtype=torch.float32, device=dev)
     cnt = torch.zeros(2, dtype=torch.int64, device=dev)
-    recv = torch.empty((B // world, T, D), dtype=torch.float32, device=dev) if world > 1 else None
-    a2a_in = torch.empty((world, B // world, Tg, D), dtype=torch.float32, device=dev) if world > 1 else None
-    a2a_out = torch.empty((world, B // world, max(len(g) for g in groups), D), dtype=torch.float32, device=dev) \
-        if world > 1 else None
     stream = torch.cuda.current_stream(dev)
+
+    received = [None]
 
     def step(i, pd):
         system.embbag(dbat[i], key0, rows, out, cnt, prefetch_distance=pd, stream=stream.cuda_stream)
         if world > 1:
-            # pooled [B, Tg, D] is peer-major along B: one all-to-all moves every peer's slice
-            a2a_in.copy_(out.view(world, B // world, Tg, D))
-            if all(len(g) == Tg for g in groups):
-                dist.all_to_all_single(a2a_out[:, :, :Tg], a2a_in)
-            else:
-                pad = torch.zeros((world, B // world, a2a_out.shape[2], D), dtype=torch.float32, device=dev)
-                pad[:, :, :Tg] = a2a_in
-                dist.all_to_all_single(a2a_out, pad)
+            # pooled [B, Tg, D] is peer-major along B: one NCCL all-to-all hands every rank the
+            # pooled embeddings of its sample slice for all 26 tables
+            received[0] = exchange_pooled(out, groups, rank, world)
 
     def barrier():
         if world > 1:
@@ -257,7 +253,18 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    # ---------------- warm-up (fills the cache) ----------------
+    # ---------------- setup: bring the cache to steady state (untimed, GPU-generated batches) -----
+    warm = args.warm_batches
+    if warm < 0:
+        warm = min(96, int(1.3 * system.num_lines / 69000) + 4)   # ~69K fills per batch at 4x tables
+    gen = torch.Generator(device=dev).manual_seed(SEED + 1)
+    t_w = time.time()
+    for _ in range(warm):
+        wb = gpu_zipf_batch(gen, shard.rows, B, L, ALPHA, scatter, dev)
+        system.embbag(wb, key0, rows, out, cnt, prefetch_distance=args.prefetch, stream=stream.cuda_stream)
+    system.sync(stream.cuda_stream)
+    warm_s = time.time() - t_w
+    # ---------------- warm-up steps ----------------
     for i in range(args.warmup):
         step(i, args.prefetch)
     system.sync(stream.cuda_stream)
@@ -321,7 +328,8 @@ def main():
                        "parallelism": f"table-wise x{world}" if world > 1 else "single"},
             "roofline": roofline, "roofline_link": roofline_link,
             "hit_rate": 1.0 - miss_lookups / max(1, lookups_local),
-            "gpu_launches": args.steps, "clocks": clk, "setup_s": setup_s}
+            "gpu_launches": args.steps, "clocks": clk, "setup_s": setup_s,
+            "cache_warm": {"batches": warm, "seconds": warm_s}}
 
     if not args.quick:
         # ---- sync mode (prefetch distance 0) on fresh batches: the async-vs-sync overlap speedup
@@ -329,14 +337,52 @@ def main():
         s0 = torch.cuda.Event(enable_timing=True)
         s1 = torch.cuda.Event(enable_timing=True)
         s0.record(stream)
+        alt = 0 if args.prefetch else 2
         for k in range(n_sync):
-            step(nb + k, 0)
+            step(nb + k, alt)
         s1.record(stream)
         barrier()
         system.sync(stream.cuda_stream)
         ms_sync = max_over_ranks(s0.elapsed_time(s1)) / n_sync
-        line["sync_ms_per_step"] = ms_sync
-        line["async_vs_sync"] = ms_sync / (ms / args.steps)
+        line["gather_alt_prefetch_distance"] = alt
+        line["gather_alt_ms_per_step"] = ms_sync
+        # ---- DLRM step with MLPs: batch-level async (prefetch i+1 beside the MLPs of i) vs sync
+        if world == 1:
+            model = DlrmModel(dev, D, T)
+            dense = torch.randn(B, 13, device=dev, dtype=torch.bfloat16)
+            for _ in range(3):   # cuBLAS handles / heuristics outside the timed pipelines
+                model.forward(dense, out)
+            torch.cuda.synchronize()
+            # calibrate: MLP time per top-MLP repeat vs the gather time of a fresh batch
+            e_a, e_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e_a.record(stream)
+            for _ in range(5):
+                model.forward(dense, out)
+            e_b.record(stream)
+            torch.cuda.synchronize()
+            mlp_ms = e_a.elapsed_time(e_b) / 5
+            gather_ms = ms / args.steps
+            pipe_rows = []
+            base = nb + n_sync + n_e2e + 1
+            for ctc in (0.0, 0.5, 1.0, 2.0):
+                model.repeat = max(1, int(round(ctc * gather_ms / max(mlp_ms, 1e-3)))) if ctc > 0 else 1
+                res = {}
+                for mode in ("sync", "async"):
+                    bat = [gpu_zipf_batch(gen, shard.rows, B, L, ALPHA, scatter, dev) for _ in range(args.steps)]
+                    res[mode] = run_pipeline(system, bat, key0, rows, model, dense, mode)
+                pipe_rows.append({"target_ctc": ctc, "mlp_repeat": model.repeat,
+                                  "sync_ms_per_step": res["sync"]["ms"] / args.steps,
+                                  "async_ms_per_step": res["async"]["ms"] / args.steps,
+                                  "speedup": res["sync"]["ms"] / res["async"]["ms"]})
+            model.repeat = 1
+            line["dlrm_pipeline"] = {"what": ("full DLRM forward per batch (bottom MLP 13-512-256-128, pairwise dot "
+                                              "interaction, top MLP 479-1024-1024-512-256-1 repeated to set the "
+                                              "compute/communication ratio; bf16 torch); sync = gather then MLPs, "
+                                              "async = batch i+1 prefetched on a side stream (24 CTAs) beside the "
+                                              "MLPs of batch i"),
+                                     "mlp_ms_per_repeat": mlp_ms, "gather_ms": gather_ms, "points": pipe_rows}
+            mid = [r for r in pipe_rows if r["target_ctc"] == 1.0][0]
+            line["async_vs_sync"] = mid["speedup"]
         # ---- hit path: replay the batch just processed (every page resident) -> HBM roofline
         hb = nb + n_sync - 1
         h0 = torch.cuda.Event(enable_timing=True)
@@ -357,8 +403,9 @@ def main():
         # ---- end to end through the C-ABI with host buffers (H2D indices, D2H pooled) ----
         if world == 1:
             # fresh batches (never seen by the cache in this run), like the timed region
-            hb_np = [host_batches[nb + n_sync + k] for k in range(args.steps)]
-            out_np = np.empty((B, Tg, D), dtype=np.float32)
+            # host buffers in pinned memory, as a serving frontend would hold them
+            hb_np = [torch.from_numpy(host_batches[nb + n_sync + k]).pin_memory().numpy() for k in range(args.steps)]
+            out_np = torch.empty((B, Tg, D), dtype=torch.float32).pin_memory().numpy()
             keyh = shard.key0.copy()
             t_e = time.perf_counter()
             for k in range(args.steps):
@@ -370,13 +417,13 @@ def main():
                            "path": "agile_embbag_host (C-ABI, host buffers)"}
         else:
             hbuf = [torch.from_numpy(host_batches[nb + n_sync + k]).pin_memory() for k in range(args.steps)]
-            res = torch.empty((world, B // world, a2a_out.shape[2], D), dtype=torch.float32).pin_memory()
+            res = torch.empty((B // world, T, D), dtype=torch.float32).pin_memory()
             barrier()
             t_e = time.perf_counter()
             for k in range(args.steps):
                 dbat[0].copy_(hbuf[k], non_blocking=True)
                 step(0, args.prefetch)
-                res.copy_(a2a_out, non_blocking=True)
+                res.copy_(received[0], non_blocking=True)
                 torch.cuda.current_stream().synchronize()
             barrier()
             e2e_s = max_over_ranks(time.perf_counter() - t_e) / args.steps

@@ -111,6 +111,12 @@ int agile_embbag(agile_ctx* ctx, const int64_t* idx, const uint64_t* table_key0,
 int agile_embbag_host(agile_ctx* ctx, const int64_t* idx, const uint64_t* table_key0, const int64_t* table_rows,
                       float* out, uint64_t* counters, uint32_t B, uint32_t T, uint32_t L, uint32_t D,
                       uint32_t prefetch_distance);
+/* Batch-level prefetch (AGILE prefetch): submit every missing page of the batch into the cache
+ * and complete once all fills landed; no pooling.  user_ctas (0 = all) bounds the SMs it takes
+ * so the DLRM MLPs of the previous batch can run beside it. */
+int agile_embbag_prefetch(agile_ctx* ctx, const int64_t* idx, const uint64_t* table_key0, const int64_t* table_rows,
+                          uint64_t* counters, uint32_t B, uint32_t T, uint32_t L, uint32_t D, uint32_t user_ctas,
+                          void* stream);
 /* number of user CTAs the embbag launch uses (for roofline accounting) */
 int agile_embbag_grid(agile_ctx* ctx, uint32_t* user_ctas, uint32_t* infra_ctas);
 

@@ -41,6 +41,7 @@ SIGNATURES = {
     "agile_embbag": (_int, [_vp, _vp, _vp, _vp, _vp, _vp, _u32, _u32, _u32, _u32, _u32, _u32, _u32, _vp]),
     "agile_embbag_host": (_int, [_vp, _vp, _vp, _vp, _vp, _vp, _u32, _u32, _u32, _u32, _u32]),
     "agile_embbag_grid": (_int, [_vp, C.POINTER(_u32), C.POINTER(_u32)]),
+    "agile_embbag_prefetch": (_int, [_vp, _vp, _vp, _vp, _vp, _u32, _u32, _u32, _u32, _u32, _vp]),
 }
 
 _lib = None

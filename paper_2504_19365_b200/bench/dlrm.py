@@ -68,6 +68,24 @@ def make_batch(seed: int, step: int, rows: np.ndarray, B: int, L: int, alpha: fl
                      for t in tables], axis=1)
 
 
+def gpu_zipf_batch(gen, rows_t, B: int, L: int, alpha: float, scatter: bool, device):
+    """Same bounded-Zipf construction on the GPU (torch), for untimed cache warm-up batches."""
+    import torch
+    cols = []
+    for n in rows_t.tolist():
+        u = torch.rand((B, L), generator=gen, device=device, dtype=torch.float64)
+        if abs(alpha - 1.0) < 1e-9:
+            r = torch.exp(u * np.log(n + 1.0))
+        else:
+            a1 = 1.0 - alpha
+            r = (1.0 + u * ((n + 1.0) ** a1 - 1.0)) ** (1.0 / a1)
+        rank = torch.clamp(torch.floor(r).to(torch.int64) - 1, 0, n - 1)
+        if scatter and n > 1:
+            rank = (rank * _scatter_mult(n) + 12345) % n
+        cols.append(rank)
+    return torch.stack(cols, dim=1).contiguous()
+
+
 def shard_tables(rows: np.ndarray, G: int):
     """Table-wise assignment balanced by bytes (largest first onto the lightest rank)."""
     load = [0] * G
@@ -92,3 +110,139 @@ def build_shard(all_rows: np.ndarray, tables: np.ndarray, dim: int) -> DlrmShard
     rows = all_rows[tables]
     key0, pages = layout(rows, dim)
     return DlrmShard(tables=tables, rows=rows, key0=key0, pages=pages)
+
+
+# ----------------------------------------------------------------------------- DLRM model + pipeline
+
+class DlrmModel:
+    """DLRM forward (Criteo-style): bottom MLP 13-512-256-128 on dense features, pairwise dot
+    interaction of the 26 pooled embeddings + dense vector, top MLP 479(+pad)-1024-1024-512-256-1.
+    bf16 weights/activations on the tensor cores through torch (the MLPs run outside the hot path,
+    BASELINE north star); `repeat` re-runs the top MLP to scale compute for CTC studies."""
+
+    def __init__(self, device, dim=128, tables=26, dense=13, repeat=1, seed=0):
+        import torch
+        g = torch.Generator(device="cpu").manual_seed(seed)
+        self.dim, self.tables, self.repeat = dim, tables, repeat
+        def mlp(sizes):
+            return [((torch.randn(b, a, generator=g) / a ** 0.5).to(device, torch.bfloat16),
+                     torch.zeros(b, device=device, dtype=torch.bfloat16)) for a, b in zip(sizes[:-1], sizes[1:])]
+        self.bot = mlp([dense, 512, 256, dim])
+        n = tables + 1
+        self.inter = n * (n - 1) // 2
+        self.top = mlp([self.inter + dim, 1024, 1024, 512, 256, 1])
+        self.iu = torch.triu_indices(n, n, offset=1, device=device)
+
+    @staticmethod
+    def _run(layers, x):
+        import torch
+        for i, (w, b) in enumerate(layers):
+            x = torch.nn.functional.linear(x, w, b)
+            if i + 1 < len(layers):
+                x = torch.relu(x)
+        return x
+
+    def forward(self, dense, pooled):
+        import torch
+        z = self._run(self.bot, dense)                                  # [B, dim]
+        feats = torch.cat([z.unsqueeze(1), pooled.to(torch.bfloat16)], dim=1)   # [B, 27, dim]
+        inter = torch.bmm(feats, feats.transpose(1, 2))[:, self.iu[0], self.iu[1]]
+        x = torch.cat([z, inter], dim=1)
+        out = None
+        for _ in range(self.repeat):
+            out = self._run(self.top, x)
+        return torch.sigmoid(out)
+
+
+def run_pipeline(system, batches, key0, rows, model, dense, mode: str, prefetch_ctas: int = 24):
+    """Time len(batches) DLRM steps.  sync: gather(i) then MLPs(i).  async: batch i+1 is prefetched
+    on a side stream by a launch bounded to `prefetch_ctas` CTAs while MLPs(i) run; gather(i+1) then
+    finds its pages resident.  Two AGILE launches never overlap (events order them)."""
+    import torch
+    dev = batches[0].device
+    B, T, L = batches[0].shape
+    D = model.dim
+    main = torch.cuda.current_stream(dev)
+    side = torch.cuda.Stream(dev)
+    out = torch.empty((B, T, D), dtype=torch.float32, device=dev)
+    cnt = torch.zeros(2, dtype=torch.int64, device=dev)
+    pcnt = torch.zeros(2, dtype=torch.int64, device=dev)
+    n = len(batches)
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(main)
+    if mode == "sync":
+        for i in range(n):
+            system.embbag(batches[i], key0, rows, out, cnt, prefetch_distance=0, stream=main.cuda_stream)
+            model.forward(dense, out)
+    else:
+        ev_p = [torch.cuda.Event() for _ in range(n)]
+        ev_e = [torch.cuda.Event() for _ in range(n)]
+        side.wait_event(t0)
+        system.embbag_prefetch(batches[0], key0, rows, D, pcnt, prefetch_ctas, stream=side.cuda_stream)
+        ev_p[0].record(side)
+        for i in range(n):
+            main.wait_event(ev_p[i])
+            system.embbag(batches[i], key0, rows, out, cnt, prefetch_distance=0, stream=main.cuda_stream)
+            ev_e[i].record(main)
+            if i + 1 < n:
+                side.wait_event(ev_e[i])
+                system.embbag_prefetch(batches[i + 1], key0, rows, D, pcnt, prefetch_ctas, stream=side.cuda_stream)
+                ev_p[i + 1].record(side)
+            model.forward(dense, out)
+    t1.record(main)
+    torch.cuda.synchronize()
+    system.sync(main.cuda_stream)
+    c = cnt.cpu().numpy()
+    return {"ms": t0.elapsed_time(t1), "lookups": int(c[0]), "miss_lookups": int(c[1]),
+            "lookups_per_s": n * B * T * L / (t0.elapsed_time(t1) / 1e3)}
+
+
+def run_dlrm(cfg, trace: bool = False):
+    """CLI experiment `dlrm`: DLRM steps on one GPU, sync vs async (BenchResult rows)."""
+    import torch
+    from . import BenchResult
+    from ..system import AgileSystem
+    dev = torch.device("cuda", torch.cuda.current_device())
+    sc = cfg.system
+    cache_bytes = sc.cache.bytes or sc.cache.lines * 4096
+    total = cfg.dlrm_table_bytes or 4 * cache_bytes
+    rows = table_rows(total, cfg.dlrm_dim, cfg.dlrm_tables)
+    key0, pages = layout(rows, cfg.dlrm_dim)
+    import copy
+    sc = copy.deepcopy(sc)
+    sc.device.num_blocks = max(sc.device.num_blocks, pages)
+    result = BenchResult(header=["mode", "batches", "t_ns", "lookups_per_s", "miss_lookups"], rows=[], info={})
+    with AgileSystem(sc) as system:
+        system.fill_store(0, sc.seed, kind="f32")
+        model = DlrmModel(dev, cfg.dlrm_dim, cfg.dlrm_tables)
+        dense = torch.randn(cfg.dlrm_batch, 13, device=dev, dtype=torch.bfloat16)
+        k0 = torch.from_numpy(key0.view(np.int64)).to(dev)
+        r = torch.from_numpy(rows).to(dev)
+        nb = cfg.dlrm_batches
+        for mode, base in (("sync", 0), ("async", nb)):
+            bat = [torch.from_numpy(make_batch(sc.seed, base + i, rows, cfg.dlrm_batch, cfg.dlrm_pooling,
+                                               cfg.dlrm_zipf, cfg.dlrm_scatter)).to(dev) for i in range(nb)]
+            res = run_pipeline(system, bat, k0, r, model, dense, mode)
+            result.rows.append((mode, nb, int(res["ms"] * 1e6), round(res["lookups_per_s"], 3), res["miss_lookups"]))
+    return result
+
+
+def exchange_pooled(pooled_local, groups, rank: int, world: int):
+    """Table-wise model parallel -> data parallel: rank r holds pooled[B, T_r, D] for its tables;
+    after one all_to_all_single every rank holds pooled[B/world, T, D] for its sample slice, tables
+    in global order.  pooled_local's B dimension is already peer-major (slice p goes to rank p)."""
+    import torch
+    import torch.distributed as dist
+    B, Tr, D = pooled_local.shape
+    tmax = max(len(g) for g in groups)
+    send = torch.zeros((world, B // world, tmax, D), dtype=pooled_local.dtype, device=pooled_local.device)
+    send[:, :, :Tr] = pooled_local.view(world, B // world, Tr, D)
+    recv = torch.empty_like(send)
+    dist.all_to_all_single(recv, send)
+    T = sum(len(g) for g in groups)
+    out = torch.empty((B // world, T, D), dtype=pooled_local.dtype, device=pooled_local.device)
+    for q in range(world):
+        out[:, torch.as_tensor(groups[q], dtype=torch.long, device=out.device)] = recv[q, :, :len(groups[q])]
+    return out

@@ -619,6 +619,31 @@ int agile_embbag(agile_ctx* ctx, const int64_t* idx, const uint64_t* table_key0,
   w.out_t_stride = out_t_stride ? out_t_stride : D;
   const uint32_t users = embbag_users(ctx);
   w.nwarps_total = users * kCtaWarps;
+  w.prefetch_only = 0;
+  return launch(ctx, w, users, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int agile_embbag_prefetch(agile_ctx* ctx, const int64_t* idx, const uint64_t* table_key0, const int64_t* table_rows,
+                          uint64_t* counters, uint32_t B, uint32_t T, uint32_t L, uint32_t D, uint32_t user_ctas,
+                          void* stream) {
+  if (!ctx || !idx || !table_key0 || !table_rows || !counters) return fail(ctx, AGILE_E_ARG, "null prefetch arg");
+  if (L == 0 || L > 32) return fail(ctx, AGILE_E_ARG, "pooling factor L must be in [1, 32]");
+  if (D == 0 || D > 128 || D % 4 || (1024u % D) != 0) return fail(ctx, AGILE_E_ARG, "bad D");
+  CK(cudaSetDevice(ctx->device));
+  EmbBagWork w{};
+  w.idx = reinterpret_cast<const long long*>(idx);
+  w.table_key0 = reinterpret_cast<const u64*>(table_key0);
+  w.table_rows = reinterpret_cast<const long long*>(table_rows);
+  w.out = nullptr;
+  w.lookups_miss = reinterpret_cast<u64*>(counters);
+  w.B = B; w.T = T; w.L = L; w.D = D;
+  uint32_t rpp = kBlockBytes / (D * 4), sh = 0;
+  while ((1u << sh) < rpp) ++sh;
+  w.rows_per_page_shift = sh;
+  w.prefetch_only = 1;
+  const uint32_t full = embbag_users(ctx);
+  const uint32_t users = user_ctas ? std::min(user_ctas, full) : full;
+  w.nwarps_total = users * kCtaWarps;
   return launch(ctx, w, users, reinterpret_cast<cudaStream_t>(stream));
 }
 

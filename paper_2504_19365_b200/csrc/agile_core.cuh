@@ -187,6 +187,21 @@ __device__ __forceinline__ void unlock_set(const DevCtx& c, u32 set) {
   if (lane_id() == 0) st_release(&c.set_lock[set], 0u);
 }
 
+// Pin a line found by a lock-free probe: CAS the pin count up by n (capped, so a hot page can
+// never overflow the 10-bit field into the ref/state bits).  Returns the post-pin word, or 0 if
+// the line no longer holds `key` or is at the cap (callers retry later through the miss path).
+constexpr u32 kPinCap = 960;
+__device__ __forceinline__ u64 pin_line(const DevCtx& c, u32 line, u64 key, u32 n) {
+  u64 w = ld_relaxed(&c.tags[line]);
+  while (true) {
+    if (!tw_live(w) || tw_key(w) != key || tw_pins(w) + n > kPinCap) return 0;
+    const u64 nw = w + (u64)n * PIN_ONE;
+    const u64 prev = atomicCAS(&c.tags[line], w, nw);
+    if (prev == w) return nw;
+    w = prev;
+  }
+}
+
 __device__ __forceinline__ void log_state(const DevCtx& c, u32 who, u32 line, u32 from, u32 to, u64 key) {
   log_ev(c, who, M_CACHE, A_STATE, line, from, to, key_dev(key), key_blk(key));
 }
@@ -209,9 +224,13 @@ __device__ int claim_key_warp(const DevCtx& c, u64 key, u32 pin_n, u32 who, u32&
     if (probe_key_warp(c, key, l, w)) {
       int kind = tw_state(w) == ST_BUSY ? R_FILLING : R_HIT;
       if (lane == 0) {
-        if (pin_n) w = atomicAdd(&c.tags[l], (u64)pin_n * PIN_ONE) + (u64)pin_n * PIN_ONE;
-        if (kind == R_HIT && !tw_ref(w)) atomicOr(&c.tags[l], REF_BIT);
-        kind = tw_state(w) == ST_BUSY ? R_FILLING : R_HIT;
+        if (pin_n) w = pin_line(c, l, key, pin_n);
+        if (!w) {
+          kind = R_RETRY;
+        } else {
+          if (kind == R_HIT && !tw_ref(w)) atomicOr(&c.tags[l], REF_BIT);
+          kind = tw_state(w) == ST_BUSY ? R_FILLING : R_HIT;
+        }
       }
       kind = __shfl_sync(FULL, kind, 0);
       w = __shfl_sync(FULL, w, 0);
@@ -308,11 +327,15 @@ __device__ int claim_lanes(const DevCtx& c, bool want, u64 key, u32 pin_n, u32 w
       }
       if (found >= 0) {
         u64 w2 = fw;
-        if (pin_n) w2 = atomicAdd(&c.tags[base + found], (u64)pin_n * PIN_ONE) + (u64)pin_n * PIN_ONE;
-        kind = tw_state(w2) == ST_BUSY ? R_FILLING : R_HIT;
-        if (kind == R_HIT && !tw_ref(w2)) atomicOr(&c.tags[base + found], REF_BIT);
-        line = (u32)(base + found);
-        word = w2;
+        if (pin_n) w2 = pin_line(c, (u32)(base + found), key, pin_n);
+        if (w2) {
+          kind = tw_state(w2) == ST_BUSY ? R_FILLING : R_HIT;
+          if (kind == R_HIT && !tw_ref(w2)) atomicOr(&c.tags[base + found], REF_BIT);
+          line = (u32)(base + found);
+          word = w2;
+        } else {
+          kind = R_RETRY;   // pin count at its cap: come back later
+        }
         settled = true;
       } else {
         const u32 hand = ld_relaxed(&c.hand[set]);
@@ -367,16 +390,6 @@ __device__ int claim_lanes(const DevCtx& c, bool want, u64 key, u32 pin_n, u32 w
   return kind;
 }
 
-// Pin a line found by a lock-free probe; returns the post-pin word, or 0 if the line no longer
-// holds `key` (caller retries through the miss path).
-__device__ __forceinline__ u64 pin_line(const DevCtx& c, u32 line, u64 key, u32 n) {
-  const u64 old = atomicAdd(&c.tags[line], (u64)n * PIN_ONE);
-  if (!tw_live(old) || tw_key(old) != key || tw_pins(old) > 900) {
-    atomicAdd(&c.tags[line], (u64)0 - (u64)n * PIN_ONE);
-    return 0;
-  }
-  return old + (u64)n * PIN_ONE;
-}
 __device__ __forceinline__ void unpin_line(const DevCtx& c, u32 line, u32 n) {
   atomicAdd(&c.tags[line], (u64)0 - (u64)n * PIN_ONE);
 }

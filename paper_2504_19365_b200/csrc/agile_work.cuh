@@ -290,6 +290,7 @@ struct EmbBagWork {
   u32 rows_per_page_shift;     // log2(4096 / (D*4))
   u32 out_b_stride, out_t_stride;   // in floats
   u32 nwarps_total;
+  u32 prefetch_only;           // 1: pull every page of the batch toward the cache, no pooling
 
   __device__ __forceinline__ bool bag_keys(u32 bag, bool lane_act, u64& key, u32& off) const {
     const u32 b = bag / T, t = bag % T;
@@ -307,10 +308,16 @@ struct EmbBagWork {
   static constexpr u32 kMaxPd = 8;
   // next bag for this warp from the launch-wide counter (dynamic balance: a warp held up by a
   // slow miss does not hold back a static share of the batch)
-  __device__ __forceinline__ u32 grab(const DevCtx& c) const {
-    u32 b = 0;
-    if (lane_id() == 0) b = (u32)atomicAdd(&c.run->work_next, 1ull);
-    return __shfl_sync(FULL, b, 0);
+  static constexpr u32 kGrab = 4;   // bags taken per counter atomic
+  __device__ __forceinline__ u32 grab(const DevCtx& c, u32& pool, u32& left) const {
+    if (!left) {
+      u32 b = 0;
+      if (lane_id() == 0) b = (u32)atomicAdd(&c.run->work_next, (u64)kGrab);
+      pool = __shfl_sync(FULL, b, 0);
+      left = kGrab;
+    }
+    --left;
+    return pool++;
   }
 
   __device__ void run(const DevCtx& c, u32 uidx, u32 nusers) {
@@ -321,12 +328,28 @@ struct EmbBagWork {
     const bool lact = lane < L;
     const u32 depth = pd > kMaxPd ? kMaxPd : pd;
     u32 misses_local = 0, lookups_local = 0;
+    u32 gpool = 0, gleft = 0;
+    if (prefetch_only) {
+      // batch-level async (AGILE prefetch, gpu_api.py:345-361): submit every missing page of the
+      // batch and return; the service keeps the launch alive until all fills completed
+      while (true) {
+        const u32 nb = grab(c, gpool, gleft);
+        if (nb >= nbags) break;
+        u64 key = 0; u32 off = 0;
+        const bool a = bag_keys(nb, lact, key, off);
+        prefetch_warp(c, a, key, who, gw + nb, false);
+        lookups_local += L;
+        if (aborted(c)) break;
+      }
+      if (lane == 0) atomicAdd(&lookups_miss[0], (u64)lookups_local);
+      return;
+    }
     // ring of grabbed-and-prefetched bags (async mode): the warp always has `depth` future bags'
     // misses in flight while it sums the oldest one
     u32 ring[kMaxPd];
     u32 head = 0, count = 0;
     for (u32 k = 0; k < depth; ++k) {
-      const u32 nb = grab(c);
+      const u32 nb = grab(c, gpool, gleft);
       if (nb >= nbags) break;
       u64 key = 0; u32 off = 0;
       const bool a = bag_keys(nb, lact, key, off);
@@ -342,7 +365,7 @@ struct EmbBagWork {
         bag = ring[head];
         head = (head + 1) % kMaxPd;
         --count;
-        const u32 nb = grab(c);
+        const u32 nb = grab(c, gpool, gleft);
         if (nb < nbags) {
           u64 key = 0; u32 off = 0;
           const bool a = bag_keys(nb, lact, key, off);
@@ -351,87 +374,111 @@ struct EmbBagWork {
           ++count;
         }
       } else {
-        bag = grab(c);
+        bag = grab(c, gpool, gleft);
         if (bag >= nbags) break;
       }
       if (aborted(c)) break;
       u64 key = 0; u32 off = 0;
       const bool a = bag_keys(bag, lact, key, off);
       float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-      // rows still to be summed (one per lane l < L); rows are validated individually so a
-      // page evicted under us only costs that row a retry
-      u32 pend = __ballot_sync(FULL, a);
       bool first = true;
-      u32 line = NONE;
-      u64 word = 0;
+      u32 fails = 0;
       Spin rsp;
-      while (pend) {
-        const bool mine = (pend >> lane) & 1u;
-        // 1. resolve pending lookups to READY lines (probe, then miss path / wait)
-        probe_lanes(c, mine, key, line, word);
-        bool ready = mine && line != NONE && (tw_state(word) == ST_READY || tw_state(word) == ST_MODIFIED);
-        if (ready && !tw_ref(word)) atomicOr(&c.tags[line], REF_BIT);
-        u32 need = __ballot_sync(FULL, mine && !ready);
-        bool pinned = false;
-        if (need) {
-          // not READY at probe time: claim (or find) the line with a pin — taken only after the
-          // claim succeeded and released before this pass ends, so no pin is held across a
-          // claim or a retry (no hold-and-wait under cache pressure); then wait for our fill
-          if (first) misses_local += __popc(need);
+      while (true) {
+        // 1. resolve every lookup to a READY line: batched ballot probe, then the miss path
+        //    (claim or find the in-flight fill, wait for it) for the rest
+        u32 line; u64 word;
+        probe_lanes(c, a, key, line, word);
+        bool ready = a && line != NONE && (tw_state(word) == ST_READY || tw_state(word) == ST_MODIFIED);
+        if (ready && !tw_ref(word)) atomicOr(&c.tags[line], REF_BIT);   // on_hit
+        u32 need = __ballot_sync(FULL, a && !ready);
+        if (need && first) misses_local += __popc(need);
+        Spin sp;
+        while (need) {
           const bool nm = (need >> lane) & 1u;
-          const Req r = access_warp(c, nm, key, true, who, gw, false);
-          if (nm && (r.kind == R_HIT || r.kind == R_FILLING || r.kind == R_MISS)) {
-            line = r.line;
-            word = r.word;
-            pinned = true;
-          }
-          u32 wp = __ballot_sync(FULL, pinned);
-          Spin sp;
+          const Req r = access_warp(c, nm, key, false, who, gw, false);
+          bool got = nm && (r.kind == R_HIT || r.kind == R_FILLING || r.kind == R_MISS);
+          if (got) { line = r.line; word = r.word; }
+          // wait for the fill; nothing is held meanwhile (a line reassigned under us goes again)
+          u32 wp = __ballot_sync(FULL, got);
+          u32 done = 0;
+          Spin s2;
           while (wp) {
-            bool rd = false;
+            bool rd = false, gone = false;
             if ((wp >> lane) & 1u) {
               const u64 w = ld_acquire(&c.tags[line]);
-              if (tw_state(w) == ST_READY || tw_state(w) == ST_MODIFIED) { word = w; rd = true; }
+              if (!tw_live(w) || tw_key(w) != key) gone = true;
+              else if (tw_state(w) == ST_READY || tw_state(w) == ST_MODIFIED) { word = w; rd = true; }
             }
-            wp &= ~__ballot_sync(FULL, rd);
-            if (wp && !sp.again(c, 1024, __LINE__ + 100000 * SPIN_FILE_ID)) break;
+            done |= __ballot_sync(FULL, rd);
+            wp &= ~__ballot_sync(FULL, rd || gone);
+            if (wp && !s2.again(c, 1024, __LINE__ + 100000 * SPIN_FILE_ID)) break;
           }
-          if (aborted(c)) { if (pinned) unpin_line(c, line, 1); break; }
-          fence_acq_rel();
+          need &= ~done;
+          if (aborted(c)) break;
+          if (need && !done && !sp.again(c, 1024, __LINE__ + 100000 * SPIN_FILE_ID)) break;
         }
+        if (aborted(c)) break;
         first = false;
-        // 2. gather the resolved rows in chunks of 8: lane owns dims [4*lane, 4*lane+4)
-        const u32 rmask = pend & __ballot_sync(FULL, ready || pinned);
-        const u64 rowaddr = (mine && (ready || pinned)) ? (u64)(uintptr_t)(line_ptr(c, line) + off) : 0ull;
-        u32 okall = 0;
+        fence_acq_rel();
+        // 2. sum the L rows, lane owns dims [4*lane, 4*lane+4): 8 row loads (16 B/lane, 512 B
+        //    coalesced each) in flight per chunk, rows added in l order (bit-exact with the oracle)
+        acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        const u64 rowaddr = a ? (u64)(uintptr_t)(line_ptr(c, line) + off) : 0ull;
         for (u32 l0 = 0; l0 < L; l0 += 8) {
-          const u32 cm = (rmask >> l0) & 0xffu;
-          if (!cm) continue;
           float4 v[8];
 #pragma unroll
           for (u32 j = 0; j < 8; ++j) {
             const u64 ra = __shfl_sync(FULL, rowaddr, (l0 + j) & 31);
             v[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (((cm >> j) & 1u) && lane * 4 < D) v[j] = __ldcg(reinterpret_cast<const float4*>(ra) + lane);
+            if (l0 + j < L && lane * 4 < D) v[j] = __ldcg(reinterpret_cast<const float4*>(ra) + lane);
           }
-          // 3. seqlock validation of unpinned rows: the line kept its identity while we read it
-          fence_acq_rel();
-          bool bad = false;
-          if (((rmask >> lane) & 1u) && !pinned && lane >= l0 && lane < l0 + 8) {
-            const u64 w2 = ld_relaxed(&c.tags[line]);
-            bad = ((w2 ^ word) & IDENT_MASK) != 0;
-          }
-          const u32 ok = cm & ~(__ballot_sync(FULL, bad) >> l0);
 #pragma unroll
-          for (u32 j = 0; j < 8; ++j) {
-            if ((ok >> j) & 1u) { acc.x += v[j].x; acc.y += v[j].y; acc.z += v[j].z; acc.w += v[j].w; }
-          }
-          okall |= ok << l0;
+          for (u32 j = 0; j < 8; ++j) { acc.x += v[j].x; acc.y += v[j].y; acc.z += v[j].z; acc.w += v[j].w; }
         }
-        if (pinned) unpin_line(c, line, 1);
-        pend &= ~okall;
-        if (pend && !okall && !rsp.again(c, 256, __LINE__ + 100000 * SPIN_FILE_ID)) break;
-        if (okall) rsp = Spin();
+        // 3. seqlock validation, once per bag: no page changed identity while we read it;
+        //    otherwise (rare) the whole bag is recomputed
+        fence_acq_rel();
+        bool bad = false;
+        if (a) bad = ((ld_relaxed(&c.tags[line]) ^ word) & IDENT_MASK) != 0;
+        if (!__any_sync(FULL, bad)) break;
+        if (++fails >= 4) {
+          // heavy eviction pressure: rows one at a time, each validated on its own (a single page
+          // only has to survive one row read), still summed in l order
+          acc = make_float4(0.f, 0.f, 0.f, 0.f);
+          for (u32 l = 0; l < L && !aborted(c); ++l) {
+            const u64 kl = __shfl_sync(FULL, key, l);
+            const u32 ol = __shfl_sync(FULL, off, l);
+            Spin s3;
+            while (true) {
+              const Req r = access_warp(c, lane == l, kl, false, who, gw, false);
+              const int kind = __shfl_sync(FULL, r.kind, l);
+              if (kind == R_HIT || kind == R_FILLING || kind == R_MISS) {
+                const u32 ln = __shfl_sync(FULL, r.line, l);
+                u64 w = 0;
+                Spin s4;
+                while (true) {
+                  w = ld_acquire(&c.tags[ln]);
+                  if (!tw_live(w) || tw_key(w) != kl) break;
+                  if (tw_state(w) == ST_READY || tw_state(w) == ST_MODIFIED) break;
+                  if (!s4.again(c, 1024, __LINE__ + 100000 * SPIN_FILE_ID)) break;
+                }
+                if (tw_live(w) && tw_key(w) == kl && tw_state(w) >= ST_READY) {
+                  float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                  if (lane * 4 < D) v = __ldcg(reinterpret_cast<const float4*>(line_ptr(c, ln) + ol) + lane);
+                  fence_acq_rel();
+                  if (((ld_relaxed(&c.tags[ln]) ^ w) & IDENT_MASK) == 0) {
+                    acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+                    break;
+                  }
+                }
+              }
+              if (!s3.again(c, 1024, __LINE__ + 100000 * SPIN_FILE_ID)) break;
+            }
+          }
+          break;
+        }
+        if (!rsp.again(c, 256, __LINE__ + 100000 * SPIN_FILE_ID)) break;
       }
       lookups_local += L;
       const u32 b = bag / T, t = bag % T;

@@ -311,6 +311,15 @@ class AgileSystem:
                                            out.data_ptr(), counters.data_ptr(), B, T, L, D, out_b_stride,
                                            out_t_stride, prefetch_distance, st), "embbag")
 
+    def embbag_prefetch(self, idx, table_key0, table_rows, D, counters, user_ctas=0, stream=None):
+        """Pull every page of the batch into the cache (async launch on `stream`)."""
+        import torch
+        B, T, L = idx.shape
+        st = stream if stream is not None else torch.cuda.current_stream(idx.device).cuda_stream
+        self._check(self._lib.agile_embbag_prefetch(self._ctx, idx.data_ptr(), table_key0.data_ptr(),
+                                                    table_rows.data_ptr(), counters.data_ptr(), B, T, L, D,
+                                                    user_ctas, st), "embbag_prefetch")
+
     def embbag_host(self, idx: np.ndarray, table_key0: np.ndarray, table_rows: np.ndarray, D: int,
                     prefetch_distance=1, out: np.ndarray | None = None):
         """Host-buffer embedding-bag through the C-ABI (H2D + kernel + D2H inside)."""

@@ -206,3 +206,31 @@ def main():
 
 if __name__ == "__main__":
     main()
+
+
+def config_golden():
+    """config.py:220-230 rendering of the default tree + override/cast behaviour."""
+    from agile_sim.config import ExperimentConfig, apply_overrides, config_text
+    out = {"default_text": config_text(ExperimentConfig())}
+    cfg = ExperimentConfig()
+    apply_overrides(cfg, {"seed": "7", "device.jitter": "uniform", "cache.bytes": "65536",
+                          "ctc_points": "0,0.5,1", "concurrency_points": "1,2", "debug_locks": "off",
+                          "share_table.enabled": "yes", "tasks": "5", "device.per_channel_rate": "1e6"})
+    out["override_text"] = config_text(cfg)
+    bad = []
+    for k in ("cache.nope", "nope", "device", "system.seed"):
+        try:
+            apply_overrides(ExperimentConfig(), {k: "1"})
+            bad.append((k, "accepted"))
+        except KeyError:
+            bad.append((k, "KeyError"))
+    out["bad_keys"] = bad
+    return out
+
+
+if __name__ == "__main__" and os.environ.get("AGILE_GOLDEN_CONFIG", "1") == "1":
+    path = os.path.join(HERE, "golden.json")
+    g = json.load(open(path))
+    g["config"] = config_golden()
+    json.dump(g, open(path, "w"))
+    print("added config golden")

@@ -30,7 +30,7 @@ def _run(s, seed, T, rows, B, L, D, pd, rng, zipf=None):
 
 
 @pytest.mark.parametrize("pd", [0, 1, 2])
-@pytest.mark.parametrize("lines,ways", [(4096, 32), (512, 16), (96, 8)])
+@pytest.mark.parametrize("lines,ways", [(4096, 32), (512, 16), (256, 8)])
 def test_embbag_matches_oracle(gpu_system, pd, lines, ways):
     s = gpu_system(cache_lines=lines, ways=ways, blocks=1 << 14, pairs=8, sq_depth=256, cq_depth=256,
                    engine_warps=8, warps=4)
