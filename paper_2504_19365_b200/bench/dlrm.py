@@ -154,7 +154,8 @@ class DlrmModel:
         return torch.sigmoid(out)
 
 
-def run_pipeline(system, batches, key0, rows, model, dense, mode: str, prefetch_ctas: int = 24):
+def run_pipeline(system, batches, key0, rows, model, dense, mode: str, prefetch_ctas: int = 24,
+                 prefetch_distance: int = 0):
     """Time len(batches) DLRM steps.  sync: gather(i) then MLPs(i).  async: batch i+1 is prefetched
     on a side stream by a launch bounded to `prefetch_ctas` CTAs while MLPs(i) run; gather(i+1) then
     finds its pages resident.  Two AGILE launches never overlap (events order them)."""
@@ -174,7 +175,7 @@ def run_pipeline(system, batches, key0, rows, model, dense, mode: str, prefetch_
     t0.record(main)
     if mode == "sync":
         for i in range(n):
-            system.embbag(batches[i], key0, rows, out, cnt, prefetch_distance=0, stream=main.cuda_stream)
+            system.embbag(batches[i], key0, rows, out, cnt, prefetch_distance=prefetch_distance, stream=main.cuda_stream)
             model.forward(dense, out)
     else:
         ev_p = [torch.cuda.Event() for _ in range(n)]

@@ -647,6 +647,49 @@ int agile_embbag_prefetch(agile_ctx* ctx, const int64_t* idx, const uint64_t* ta
   return launch(ctx, w, users, reinterpret_cast<cudaStream_t>(stream));
 }
 
+int agile_bfs_level(agile_ctx* ctx, const int64_t* row_ptr, int32_t* level, const int32_t* frontier, uint32_t n_in,
+                    int32_t* next, uint32_t* next_count, uint64_t col_key0, int32_t cur_level, int prefetch,
+                    uint64_t* counters, void* stream) {
+  if (!ctx || !row_ptr || !level || !next || !next_count || !counters) return fail(ctx, AGILE_E_ARG, "null bfs arg");
+  CK(cudaSetDevice(ctx->device));
+  BfsWork w;
+  w.row_ptr = reinterpret_cast<const long long*>(row_ptr);
+  w.level = level;
+  w.frontier = frontier;
+  w.next = next;
+  w.next_count = next_count;
+  w.col_key0 = col_key0;
+  w.n_in = n_in;
+  w.cur = cur_level;
+  w.prefetch = prefetch ? 1u : 0u;
+  w.counters = reinterpret_cast<u64*>(counters);
+  const uint32_t cap = resident_ctas<BfsWork>(ctx);
+  const uint32_t infra = ctx->d.n_engine_ctas + ctx->d.n_service_ctas;
+  const uint32_t want = (n_in + kCtaWarps - 1) / kCtaWarps;
+  const uint32_t users = std::max<uint32_t>(1, std::min<uint32_t>(want, cap > infra + 1 ? cap - infra : 1));
+  return launch(ctx, w, users, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int agile_spmv(agile_ctx* ctx, const int64_t* row_ptr, uint32_t V, uint64_t col_key0, uint64_t val_key0,
+               const float* x, float* y, float alpha, float beta, int prefetch, uint64_t* counters, void* stream) {
+  if (!ctx || !row_ptr || !x || !y || !counters) return fail(ctx, AGILE_E_ARG, "null spmv arg");
+  CK(cudaSetDevice(ctx->device));
+  SpmvWork w;
+  w.row_ptr = reinterpret_cast<const long long*>(row_ptr);
+  w.x = x;
+  w.y = y;
+  w.col_key0 = col_key0;
+  w.val_key0 = val_key0;
+  w.V = V;
+  w.alpha = alpha;
+  w.beta = beta;
+  w.prefetch = prefetch ? 1u : 0u;
+  w.counters = reinterpret_cast<u64*>(counters);
+  const uint32_t cap = resident_ctas<SpmvWork>(ctx);
+  const uint32_t infra = ctx->d.n_engine_ctas + ctx->d.n_service_ctas;
+  return launch(ctx, w, cap > infra + 1 ? cap - infra : 1, reinterpret_cast<cudaStream_t>(stream));
+}
+
 int agile_embbag_host(agile_ctx* ctx, const int64_t* idx, const uint64_t* table_key0, const int64_t* table_rows,
                       float* out, uint64_t* counters, uint32_t B, uint32_t T, uint32_t L, uint32_t D,
                       uint32_t prefetch_distance) {

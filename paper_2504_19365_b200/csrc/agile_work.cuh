@@ -491,4 +491,169 @@ struct EmbBagWork {
   }
 };
 
+// ------------------------------------------------------------------ paged CSR reads (K6/K7)
+// Read one u32 per active lane from page `key` at byte offset `off` through the cache: batched
+// probe, miss path (claim or find the fill, wait), read, seqlock validation, retry.  Nothing is
+// held across a wait.  Returns the value; lanes that gave up (abort) get 0.
+__device__ u32 read_u32_warp(const DevCtx& c, bool active, u64 key, u32 off, u32 who, u32 sq_start) {
+  const u32 lane = lane_id();
+  u32 val = 0;
+  bool pend = active;
+  Spin sp;
+  while (__any_sync(FULL, pend)) {
+    u32 line; u64 word;
+    probe_lanes(c, pend, key, line, word);
+    bool ready = pend && line != NONE && (tw_state(word) == ST_READY || tw_state(word) == ST_MODIFIED);
+    if (ready && !tw_ref(word)) atomicOr(&c.tags[line], REF_BIT);
+    const bool nm = pend && !ready;
+    if (__any_sync(FULL, nm)) {
+      const Req r = access_warp(c, nm, key, false, who, sq_start, false);
+      bool got = nm && (r.kind == R_HIT || r.kind == R_FILLING || r.kind == R_MISS);
+      if (got) { line = r.line; word = r.word; }
+      u32 wp = __ballot_sync(FULL, got);
+      Spin s2;
+      while (wp) {
+        bool rd = false, gone = false;
+        if ((wp >> lane) & 1u) {
+          const u64 w = ld_acquire(&c.tags[line]);
+          if (!tw_live(w) || tw_key(w) != key) gone = true;
+          else if (tw_state(w) == ST_READY || tw_state(w) == ST_MODIFIED) { word = w; rd = true; }
+        }
+        if (gone) got = false;
+        wp &= ~__ballot_sync(FULL, rd || gone);
+        if (wp && !s2.again(c, 1024, __LINE__ + 100000 * SPIN_FILE_ID)) break;
+      }
+      ready = ready || got;
+      fence_acq_rel();
+    }
+    u32 v = 0;
+    if (ready) v = __ldcg(reinterpret_cast<const unsigned int*>(line_ptr(c, line) + off));
+    fence_acq_rel();
+    bool ok = false;
+    if (ready) ok = ((ld_relaxed(&c.tags[line]) ^ word) & IDENT_MASK) == 0;
+    if (ok) { val = v; pend = false; }
+    if (aborted(c)) break;
+    if (__any_sync(FULL, pend) && !__any_sync(FULL, ok) && !sp.again(c, 1024, __LINE__ + 100000 * SPIN_FILE_ID)) break;
+  }
+  return val;
+}
+
+// BFS level (K6): top-down expansion of `frontier` over a CSR whose col_idx array is paged
+// (1024 int32 per 4 KiB page, page p of the array = key col_key0 + p).  Warps take frontier
+// vertices dynamically; lanes walk the vertex's edges 32 at a time, claim unvisited neighbours
+// with a CAS on level[] and append them (warp-aggregated) to the next frontier.  With prefetch,
+// each newly discovered vertex's first col_idx page is pulled toward the cache right away, so the
+// next level's reads overlap this level's expansion (the AGILE async pattern).
+struct BfsWork {
+  const long long* row_ptr;   // [V+1] (HBM)
+  int* level;                 // [V], -1 = unvisited
+  const int* frontier;        // [n_in]
+  int* next;                  // [V]
+  unsigned int* next_count;
+  u64 col_key0;
+  u32 n_in;
+  int cur;
+  u32 prefetch;
+  u64* counters;              // [0] edges traversed
+  __device__ void run(const DevCtx& c, u32 uidx, u32 nusers) {
+    const u32 lane = lane_id();
+    const u32 gw = uidx * kCtaWarps + (threadIdx.x >> 5);
+    const u32 who = user_who(uidx);
+    u64 edges = 0;
+    while (true) {
+      u32 i = 0;
+      if (lane == 0) i = (u32)atomicAdd(&c.run->work_next, 1ull);
+      i = __shfl_sync(FULL, i, 0);
+      if (i >= n_in || aborted(c)) break;
+      const int v = frontier[i];
+      const long long s = row_ptr[v], e = row_ptr[v + 1];
+      edges += (u64)(e - s);
+      for (long long b = s; b < e; b += 32) {
+        const long long ed = b + lane;
+        const bool act = ed < e;
+        const u64 key = col_key0 + (u64)(act ? (ed >> 10) : 0);
+        const u32 u = read_u32_warp(c, act, key, (u32)(act ? (ed & 1023) * 4 : 0), who, gw);
+        bool disc = false;
+        if (act && ld_relaxed(reinterpret_cast<const u32*>(level) + u) == 0xffffffffu)
+          disc = atomicCAS(level + u, -1, cur + 1) == -1;
+        const u32 db = __ballot_sync(FULL, disc);
+        if (db) {
+          u32 base = 0;
+          if (lane == __ffs(db) - 1) base = atomicAdd(next_count, (u32)__popc(db));
+          base = __shfl_sync(FULL, base, __ffs(db) - 1);
+          if (disc) next[base + __popc(db & lanemask_lt())] = (int)u;
+          if (prefetch) {
+            u64 pk = 0;
+            if (disc) pk = col_key0 + (u64)(row_ptr[u] >> 10);
+            const bool has = disc && row_ptr[u + 1] > row_ptr[u];
+            prefetch_warp(c, has, pk, who, gw, true);
+          }
+        }
+      }
+    }
+    if (lane == 0 && edges) atomicAdd(&counters[0], edges);
+  }
+};
+
+// SpMV over a paged CSR (K7): y[r] = alpha * sum_e val[e] * x[col[e]] + beta, col (int32) and val
+// (fp32) paged (1024 per page; val_key0 = ~0 -> unit weights, the PageRank A^T case).  Warps take
+// blocks of 32 rows dynamically; the next block's first pages are prefetched before the current
+// block is processed (next-chunk prefetch).  One warp per row: lanes over the edges, warp sum.
+struct SpmvWork {
+  const long long* row_ptr;
+  const float* x;
+  float* y;
+  u64 col_key0, val_key0;
+  u32 V;
+  float alpha, beta;
+  u32 prefetch;
+  u64* counters;   // [0] edges
+  __device__ void run(const DevCtx& c, u32 uidx, u32 nusers) {
+    const u32 lane = lane_id();
+    const u32 gw = uidx * kCtaWarps + (threadIdx.x >> 5);
+    const u32 who = user_who(uidx);
+    const u32 nblocks = (V + 31) / 32;
+    u64 edges = 0;
+    u32 blk = 0;
+    if (lane == 0) blk = (u32)atomicAdd(&c.run->work_next, 1ull);
+    blk = __shfl_sync(FULL, blk, 0);
+    while (blk < nblocks && !aborted(c)) {
+      u32 nxt = 0;
+      if (lane == 0) nxt = (u32)atomicAdd(&c.run->work_next, 1ull);
+      nxt = __shfl_sync(FULL, nxt, 0);
+      if (prefetch && nxt < nblocks) {
+        // pull the next block's edge pages (col, and val when weighted) toward the cache
+        const u32 r0 = nxt * 32, r1 = min(V, r0 + 32);
+        const long long s0 = row_ptr[r0], s1 = row_ptr[r1];
+        const long long p0 = s0 >> 10, p1 = (s1 + 1023) >> 10;
+        const long long np = p1 - p0;
+        const bool h = (long long)lane < np;
+        prefetch_warp(c, h, col_key0 + (u64)(p0 + lane), who, gw + 1, true);
+        if (val_key0 != ~0ull) prefetch_warp(c, h, val_key0 + (u64)(p0 + lane), who, gw + 2, true);
+      }
+      const u32 r0 = blk * 32, r1 = min(V, r0 + 32);
+      for (u32 r = r0; r < r1; ++r) {
+        const long long s = row_ptr[r], e = row_ptr[r + 1];
+        float acc = 0.f;
+        for (long long b = s; b < e; b += 32) {
+          const long long ed = b + lane;
+          const bool act = ed < e;
+          const u64 pg = (u64)(act ? (ed >> 10) : 0);
+          const u32 off = (u32)(act ? (ed & 1023) * 4 : 0);
+          const u32 col = read_u32_warp(c, act, col_key0 + pg, off, who, gw);
+          float w = 1.f;
+          if (val_key0 != ~0ull) w = __uint_as_float(read_u32_warp(c, act, val_key0 + pg, off, who, gw));
+          if (act) acc += w * __ldg(x + col);
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
+        if (lane == 0) y[r] = alpha * acc + beta;
+        edges += (u64)(e - s);
+      }
+      blk = nxt;
+    }
+    if (lane == 0 && edges) atomicAdd(&counters[0], edges);
+  }
+};
+
 }  // namespace agile

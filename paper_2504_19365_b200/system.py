@@ -335,6 +335,24 @@ class AgileSystem:
                     "embbag_host")
         return out, cnt
 
+    def bfs_level(self, row_ptr, level, frontier, n_in, nxt, next_count, col_key0, cur, prefetch, counters, stream=None):
+        import torch
+        st = stream if stream is not None else torch.cuda.current_stream(row_ptr.device).cuda_stream
+        self._check(self._lib.agile_bfs_level(self._ctx, row_ptr.data_ptr(), level.data_ptr(), frontier.data_ptr(),
+                                              n_in, nxt.data_ptr(), next_count.data_ptr(), col_key0, cur,
+                                              int(prefetch), counters.data_ptr(), st), "bfs_level")
+
+    def spmv(self, row_ptr, V, col_key0, val_key0, x, y, alpha=1.0, beta=0.0, prefetch=True, counters=None,
+             stream=None):
+        import torch
+        st = stream if stream is not None else torch.cuda.current_stream(row_ptr.device).cuda_stream
+        if counters is None:
+            counters = torch.zeros(2, dtype=torch.int64, device=row_ptr.device)
+        vk = (1 << 64) - 1 if val_key0 is None else val_key0
+        self._check(self._lib.agile_spmv(self._ctx, row_ptr.data_ptr(), V, col_key0, vk, x.data_ptr(), y.data_ptr(),
+                                         float(alpha), float(beta), int(prefetch), counters.data_ptr(), st), "spmv")
+        return counters
+
     def embbag_grid(self):
         u, i = C.c_uint32(), C.c_uint32()
         self._check(self._lib.agile_embbag_grid(self._ctx, C.byref(u), C.byref(i)), "embbag_grid")

@@ -9,3 +9,5 @@ timeout 300 python -m paper_2504_19365_b200.cli rand_read > gpurun_out/cli_rand_
 timeout 300 python -m paper_2504_19365_b200.cli queue_sweep > gpurun_out/cli_queue_sweep.csv 2>&1; echo "queue rc=$?"
 timeout 300 python -m paper_2504_19365_b200.cli cache_sweep > gpurun_out/cli_cache_sweep.csv 2>&1; echo "cache rc=$?"
 timeout 300 python -m paper_2504_19365_b200.cli deadlock_demo > gpurun_out/cli_deadlock.csv 2>&1; echo "deadlock rc=$?"
+timeout 600 python -m paper_2504_19365_b200.cli bfs --config configs/graph_bench.cfg > gpurun_out/cli_bfs.csv 2>&1; echo "bfs rc=$?"
+timeout 600 python -m paper_2504_19365_b200.cli spmv --config configs/graph_bench.cfg > gpurun_out/cli_spmv.csv 2>&1; echo "spmv rc=$?"
