@@ -45,10 +45,12 @@ def _args():
     p.add_argument("--impl", default="ours", choices=("ours", "reference"))
     p.add_argument("--cache-gib", type=float, default=16.0)
     p.add_argument("--table-mult", type=float, default=4.0)
-    p.add_argument("--prefetch", type=int, default=2, help="in-kernel bag prefetch distance (0 = sync gather)")
+    p.add_argument("--prefetch", type=int, default=0, help="in-kernel bag prefetch distance (0 = sync gather)")
     p.add_argument("--no-scatter", action="store_true")
     p.add_argument("--quick", action="store_true", help="skip e2e / sync / hit / cpu legs")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
+    p.add_argument("--engine-warps", type=int, default=128)
+    p.add_argument("--service-warps", type=int, default=48)
     p.add_argument("--warm-batches", type=int, default=-1,
                    help="untimed cache warm-up batches at setup (-1: enough to fill the cache)")
     return p.parse_args()
@@ -210,8 +212,8 @@ def main():
     cfg.queues.pairs_per_device = 128        # paper defaults: 128 QPs x 256 (config.py:49-51)
     cfg.queues.sq_depth = 256
     cfg.queues.cq_depth = 256
-    cfg.engine.warps = 64
-    cfg.service.warps = 16
+    cfg.engine.warps = args.engine_warps
+    cfg.service.warps = args.service_warps
     cfg.service.idle_max_ns = 1600
     cfg.debug_locks = False
     t0 = time.time()
@@ -304,10 +306,17 @@ def main():
     avg_kern_s = statistics.mean(kern_ms) / 1e3
     bags_local = B * Tg
     alg_bytes = bags_local * L * (D * 4 + 8) + bags_local * D * 4      # rows + indices + pooled out
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_embbag_traffic.json")) as fh:
+            traffic = json.load(fh)["dram_bytes_per_launch"]
+    except Exception:
+        pass
     roofline = {"bound": "hbm", "achieved": alg_bytes / avg_kern_s / 1e9, "peak": hbm_peak, "unit": "GB/s",
-                "frac": alg_bytes / avg_kern_s / 1e9 / hbm_peak, "traffic": None,
+                "frac": alg_bytes / avg_kern_s / 1e9 / hbm_peak, "traffic": traffic,
                 "kernel": "agile_kernel<EmbBagWork> (fused engine+service+embbag)",
-                "bytes_per_launch": alg_bytes, "peak_kind": peak_kind}
+                "bytes_per_launch": alg_bytes, "peak_kind": peak_kind,
+                "binding": "host link (see roofline_link): misses move 4 KiB pages over PCIe; hits are L2/HBM"}
     miss_bytes = fills / args.steps * 4096
     roofline_link = {"bound": "link", "achieved": miss_bytes / avg_kern_s / 1e9, "peak": link_peak, "unit": "GB/s",
                      "frac": miss_bytes / avg_kern_s / 1e9 / link_peak,
@@ -337,7 +346,7 @@ def main():
         s0 = torch.cuda.Event(enable_timing=True)
         s1 = torch.cuda.Event(enable_timing=True)
         s0.record(stream)
-        alt = 0 if args.prefetch else 2
+        alt = 0 if args.prefetch else 2   # the other in-kernel prefetch mode, for comparison
         for k in range(n_sync):
             step(nb + k, alt)
         s1.record(stream)

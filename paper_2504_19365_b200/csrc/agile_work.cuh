@@ -406,7 +406,7 @@ struct EmbBagWork {
           while (wp) {
             bool rd = false, gone = false;
             if ((wp >> lane) & 1u) {
-              const u64 w = ld_acquire(&c.tags[line]);
+              const u64 w = ld_relaxed(&c.tags[line]);
               if (!tw_live(w) || tw_key(w) != key) gone = true;
               else if (tw_state(w) == ST_READY || tw_state(w) == ST_MODIFIED) { word = w; rd = true; }
             }
@@ -515,7 +515,7 @@ __device__ u32 read_u32_warp(const DevCtx& c, bool active, u64 key, u32 off, u32
       while (wp) {
         bool rd = false, gone = false;
         if ((wp >> lane) & 1u) {
-          const u64 w = ld_acquire(&c.tags[line]);
+          const u64 w = ld_relaxed(&c.tags[line]);
           if (!tw_live(w) || tw_key(w) != key) gone = true;
           else if (tw_state(w) == ST_READY || tw_state(w) == ST_MODIFIED) { word = w; rd = true; }
         }
