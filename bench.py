@@ -187,7 +187,8 @@ def main():
     import torch.distributed as dist
     from paper_2504_19365_b200 import AgileSystem, SystemConfig
     from paper_2504_19365_b200.bench.dlrm import (table_rows, make_batch, shard_tables, build_shard,
-                                                  exchange_pooled, DlrmModel, run_pipeline, gpu_zipf_batch)
+                                                  exchange_pooled, DlrmModel, run_pipeline, gpu_zipf_batch,
+                                                  mlp_graph_ms)
 
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
@@ -359,42 +360,35 @@ def main():
         if world == 1:
             model = DlrmModel(dev, D, T)
             dense = torch.randn(B, 13, device=dev, dtype=torch.bfloat16)
-            for _ in range(3):   # cuBLAS handles / heuristics outside the timed pipelines
-                model.forward(dense, out)
-            torch.cuda.synchronize()
-            # calibrate: MLP time per top-MLP repeat vs the gather time of a fresh batch
-            def fwd_ms(rep):
-                model.repeat = rep
-                e_a, e_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e_a.record(stream)
-                for _ in range(5):
-                    model.forward(dense, out)
-                e_b.record(stream)
-                torch.cuda.synchronize()
-                return e_a.elapsed_time(e_b) / 5
-            f1, f9 = fwd_ms(1), fwd_ms(9)
-            per_rep = max((f9 - f1) / 8, 1e-3)          # top-MLP cost per repeat
-            mlp_ms = f1
+            # calibrate on the device: MLP graph time per top-MLP pass vs the gather time
+            f1 = mlp_graph_ms(model.capture(dense, out, 1))
+            f9 = mlp_graph_ms(model.capture(dense, out, 9))
+            per_rep = max((f9 - f1) / 8, 1e-3)          # top-MLP cost per pass
             gather_ms = ms / args.steps
             pipe_rows = []
-            base = nb + n_sync + n_e2e + 1
-            for ctc in (0.0, 0.5, 1.0, 2.0):
-                model.repeat = max(1, int(round((ctc * gather_ms - f1) / per_rep)) + 1) if ctc > 0 else 1
+            for ctc in (0.0, 0.5, 0.75, 1.0, 1.5, 2.0):
+                rep = max(1, int(round((ctc * gather_ms - f1) / per_rep)) + 1) if ctc > 0 else 1
+                mlp = model.capture(dense, out, rep)
+                mlp_ms = mlp_graph_ms(mlp, 3)
                 res = {}
                 for mode in ("sync", "async"):
                     bat = [gpu_zipf_batch(gen, shard.rows, B, L, ALPHA, scatter, dev) for _ in range(args.steps)]
-                    res[mode] = run_pipeline(system, bat, key0, rows, model, dense, mode, prefetch_distance=args.prefetch)
-                pipe_rows.append({"target_ctc": ctc, "mlp_repeat": model.repeat,
-                                  "sync_ms_per_step": res["sync"]["ms"] / args.steps,
+                    res[mode] = run_pipeline(system, bat, key0, rows, mlp, out, mode, prefetch_distance=args.prefetch)
+                t_s = res["sync"]["ms"] / args.steps
+                pipe_rows.append({"target_ctc": ctc, "mlp_repeat": rep, "mlp_ms": mlp_ms,
+                                  "ctc": mlp_ms / max(1e-9, t_s - mlp_ms),
+                                  "sync_ms_per_step": t_s,
                                   "async_ms_per_step": res["async"]["ms"] / args.steps,
-                                  "speedup": res["sync"]["ms"] / res["async"]["ms"]})
-            model.repeat = 1
+                                  "speedup": res["sync"]["ms"] / res["async"]["ms"],
+                                  "ideal": 1.0 + min(mlp_ms, t_s - mlp_ms) / max(mlp_ms, t_s - mlp_ms)})
+                del mlp
             line["dlrm_pipeline"] = {"what": ("full DLRM forward per batch (bottom MLP 13-512-256-128, pairwise dot "
                                               "interaction, top MLP 479-1024-1024-512-256-1 repeated to set the "
-                                              "compute/communication ratio; bf16 torch); sync = gather then MLPs, "
-                                              "async = batch i+1 prefetched on a side stream (24 CTAs) beside the "
-                                              "MLPs of batch i"),
-                                     "mlp_ms_forward": mlp_ms, "mlp_ms_per_top_repeat": per_rep,
+                                              "compute/communication ratio; bf16 torch, captured as one CUDA graph); "
+                                              "sync = gather then MLPs, async = batch i+1 prefetched on a side "
+                                              "stream (24 user CTAs) beside the MLPs of batch i; ctc = MLP time / "
+                                              "sync gather time; ideal = Eq. 1 (bench/__init__.py:35-41)"),
+                                     "mlp_ms_forward": f1, "mlp_ms_per_top_repeat": per_rep,
                                      "gather_ms": gather_ms, "points": pipe_rows}
             mid = [r for r in pipe_rows if r["target_ctc"] == 1.0][0]
             line["async_vs_sync"] = mid["speedup"]

@@ -117,17 +117,21 @@ int agile_embbag_host(agile_ctx* ctx, const int64_t* idx, const uint64_t* table_
 int agile_embbag_prefetch(agile_ctx* ctx, const int64_t* idx, const uint64_t* table_key0, const int64_t* table_rows,
                           uint64_t* counters, uint32_t B, uint32_t T, uint32_t L, uint32_t D, uint32_t user_ctas,
                           void* stream);
-/* BFS level over a paged CSR (K6): row_ptr[V+1] int64 in HBM, col_idx int32 paged from page key
- * col_key0 (1024 per page).  Expands frontier[n_in]: unvisited neighbours get level cur+1 and are
- * appended to next (next_count += found).  prefetch: pull each discovered vertex's first col page
- * into the cache immediately.  counters[0] += edges traversed. */
-int agile_bfs_level(agile_ctx* ctx, const int64_t* row_ptr, int32_t* level, const int32_t* frontier, uint32_t n_in,
-                    int32_t* next, uint32_t* next_count, uint64_t col_key0, int32_t cur_level, int prefetch,
-                    uint64_t* counters, void* stream);
-/* SpMV over a paged CSR (K7): y = alpha * A x + beta; col int32 and val fp32 paged (val_key0 =
- * UINT64_MAX: unit weights, the PageRank A^T case); prefetch: next row block's pages. */
-int agile_spmv(agile_ctx* ctx, const int64_t* row_ptr, uint32_t V, uint64_t col_key0, uint64_t val_key0,
-               const float* x, float* y, float alpha, float beta, int prefetch, uint64_t* counters, void* stream);
+/* Breadth-first search over a paged CSR (K6; BASELINE configs[2]; new workload, the reference
+ * has no graph driver).  row_ptr[V+1] int64 in HBM; col_idx int32 lives in the page
+ * store from page key col_key0 (1024 entries per 4 KiB page) and is read through the HBM cache.
+ * level[V] int32 (device) receives the BFS level of every vertex, -1 if unreached.  Level-
+ * synchronous top-down over a sorted frontier; prefetch_distance = edge chunks a warp grabs and
+ * prefetches ahead (0 = synchronous).  stats (host, may be NULL): [0] levels, [1] edges expanded,
+ * [2] page misses, [3] device ns. */
+int agile_bfs(agile_ctx* ctx, const int64_t* row_ptr, uint32_t V, uint32_t source, uint64_t col_key0,
+              int32_t* level, uint32_t prefetch_distance, uint64_t* stats, void* stream);
+/* SpMV over a paged CSR (K7; configs[3]): y = alpha * A x + beta for E edges; col int32 and val
+ * fp32 paged one page per 1024 edges (val_key0 = UINT64_MAX: unit weights, the PageRank A^T
+ * case).  Deterministic summation order.  counters (device u64[2]) += {edges, page misses}. */
+int agile_spmv(agile_ctx* ctx, const int64_t* row_ptr, uint32_t V, uint64_t E, uint64_t col_key0, uint64_t val_key0,
+               const float* x, float* y, float alpha, float beta, uint32_t prefetch_distance, uint64_t* counters,
+               void* stream);
 /* number of user CTAs the embbag launch uses (for roofline accounting) */
 int agile_embbag_grid(agile_ctx* ctx, uint32_t* user_ctas, uint32_t* infra_ctas);
 

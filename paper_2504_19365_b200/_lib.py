@@ -41,8 +41,8 @@ SIGNATURES = {
     "agile_embbag": (_int, [_vp, _vp, _vp, _vp, _vp, _vp, _u32, _u32, _u32, _u32, _u32, _u32, _u32, _vp]),
     "agile_embbag_host": (_int, [_vp, _vp, _vp, _vp, _vp, _vp, _u32, _u32, _u32, _u32, _u32]),
     "agile_embbag_grid": (_int, [_vp, C.POINTER(_u32), C.POINTER(_u32)]),
-    "agile_bfs_level": (_int, [_vp, _vp, _vp, _vp, _u32, _vp, _vp, _u64, C.c_int32, _int, _vp, _vp]),
-    "agile_spmv": (_int, [_vp, _vp, _u32, _u64, _u64, _vp, _vp, C.c_float, C.c_float, _int, _vp, _vp]),
+    "agile_bfs": (_int, [_vp, _vp, _u32, _u32, _u64, _vp, _u32, _vp, _vp]),
+    "agile_spmv": (_int, [_vp, _vp, _u32, _u64, _u64, _u64, _vp, _vp, C.c_float, C.c_float, _u32, _vp, _vp]),
     "agile_embbag_prefetch": (_int, [_vp, _vp, _vp, _vp, _vp, _u32, _u32, _u32, _u32, _u32, _vp]),
 }
 

@@ -153,19 +153,54 @@ class DlrmModel:
             out = self._run(self.top, x)
         return torch.sigmoid(out)
 
+    def capture(self, dense, pooled, repeat: int):
+        """The forward as one CUDA graph over the fixed `pooled` buffer.  Eager, the MLPs are
+        host-launch-bound (~10 small GEMMs per top-MLP pass at batch 2048): the GPU would idle
+        between kernels and a "compute" phase would really be CPU time.  Replaying a graph makes
+        the MLP phase GPU time, so the compute/communication ratio is the device's."""
+        import torch
+        self.repeat = repeat
+        side = torch.cuda.Stream(dense.device)
+        side.wait_stream(torch.cuda.current_stream(dense.device))
+        with torch.cuda.stream(side):
+            for _ in range(2):
+                self.forward(dense, pooled)
+        torch.cuda.current_stream(dense.device).wait_stream(side)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            res = self.forward(dense, pooled)
+        g.result = res
+        return g
 
-def run_pipeline(system, batches, key0, rows, model, dense, mode: str, prefetch_ctas: int = 24,
+
+def mlp_graph_ms(graph, reps: int = 10) -> float:
+    """Device time of one replay (CUDA events on the current stream, after a warm replay)."""
+    import torch
+    graph.replay()
+    st = torch.cuda.current_stream()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(st)
+    for _ in range(reps):
+        graph.replay()
+    b.record(st)
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps
+
+
+def run_pipeline(system, batches, key0, rows, mlp, out, mode: str, prefetch_ctas: int = 24,
                  prefetch_distance: int = 0):
-    """Time len(batches) DLRM steps.  sync: gather(i) then MLPs(i).  async: batch i+1 is prefetched
-    on a side stream by a launch bounded to `prefetch_ctas` CTAs while MLPs(i) run; gather(i+1) then
-    finds its pages resident.  Two AGILE launches never overlap (events order them)."""
+    """Time len(batches) DLRM steps; `mlp` is a captured forward graph reading `out` (the pooled
+    [B, T, D] buffer the gathers write).  sync: gather(i) then MLPs(i) (bench/ctc.py:27-44
+    shape: compute starts once the data arrived).  async: batch i+1 is prefetched on a side stream
+    by a launch bounded to `prefetch_ctas` user CTAs while MLPs(i) run; gather(i+1) then finds its
+    pages resident (bench/ctc.py:47-70 shape).  Two AGILE launches never overlap (events order
+    them); gather(i+1) overwrites `out` only after MLPs(i) consumed it (same stream)."""
     import torch
     dev = batches[0].device
     B, T, L = batches[0].shape
-    D = model.dim
+    D = out.shape[-1]
     main = torch.cuda.current_stream(dev)
     side = torch.cuda.Stream(dev)
-    out = torch.empty((B, T, D), dtype=torch.float32, device=dev)
     cnt = torch.zeros(2, dtype=torch.int64, device=dev)
     pcnt = torch.zeros(2, dtype=torch.int64, device=dev)
     n = len(batches)
@@ -176,7 +211,7 @@ def run_pipeline(system, batches, key0, rows, model, dense, mode: str, prefetch_
     if mode == "sync":
         for i in range(n):
             system.embbag(batches[i], key0, rows, out, cnt, prefetch_distance=prefetch_distance, stream=main.cuda_stream)
-            model.forward(dense, out)
+            mlp.replay()
     else:
         ev_p = [torch.cuda.Event() for _ in range(n)]
         ev_e = [torch.cuda.Event() for _ in range(n)]
@@ -191,7 +226,7 @@ def run_pipeline(system, batches, key0, rows, model, dense, mode: str, prefetch_
                 side.wait_event(ev_e[i])
                 system.embbag_prefetch(batches[i + 1], key0, rows, D, pcnt, prefetch_ctas, stream=side.cuda_stream)
                 ev_p[i + 1].record(side)
-            model.forward(dense, out)
+            mlp.replay()
     t1.record(main)
     torch.cuda.synchronize()
     system.sync(main.cuda_stream)
@@ -219,13 +254,15 @@ def run_dlrm(cfg, trace: bool = False):
         system.fill_store(0, sc.seed, kind="f32")
         model = DlrmModel(dev, cfg.dlrm_dim, cfg.dlrm_tables)
         dense = torch.randn(cfg.dlrm_batch, 13, device=dev, dtype=torch.bfloat16)
+        out = torch.zeros((cfg.dlrm_batch, cfg.dlrm_tables, cfg.dlrm_dim), dtype=torch.float32, device=dev)
+        mlp = model.capture(dense, out, 1)
         k0 = torch.from_numpy(key0.view(np.int64)).to(dev)
         r = torch.from_numpy(rows).to(dev)
         nb = cfg.dlrm_batches
         for mode, base in (("sync", 0), ("async", nb)):
             bat = [torch.from_numpy(make_batch(sc.seed, base + i, rows, cfg.dlrm_batch, cfg.dlrm_pooling,
                                                cfg.dlrm_zipf, cfg.dlrm_scatter)).to(dev) for i in range(nb)]
-            res = run_pipeline(system, bat, k0, r, model, dense, mode)
+            res = run_pipeline(system, bat, k0, r, mlp, out, mode)
             result.rows.append((mode, nb, int(res["ms"] * 1e6), round(res["lookups_per_s"], 3), res["miss_lookups"]))
     return result
 

@@ -3,56 +3,83 @@ reference has no graph driver).
 
 * RMAT / Kronecker generator (Graph500 parameters A, B, C = 0.57, 0.19, 0.19; edge factor 16),
   vertex labels permuted, directed edges kept as generated (duplicates/self-loops included, as
-  Graph500 does).  Built on the GPU with torch.
+  Graph500 does).  Built on the GPU with torch in bounded memory (scale 27 = 2^31 edges).
 * CSR: row_ptr int64 [V+1] resident in HBM; col_idx int32 (and SpMV values fp32) laid out in the
   emulated device's page store, 1024 entries per 4 KiB page, read through the HBM cache.
-* BFS: level-synchronous top-down, one fused launch per level, next-frontier pages prefetched as
-  vertices are discovered.  SpMV: y = A x with next-row-block prefetch; PageRank: 10 iterations of
-  r <- (1-d)/V + d * A^T (r / outdeg) on the transposed CSR with unit weights.
+* BFS (agile_bfs): level-synchronous top-down over a sorted frontier, one fused launch per level;
+  warps walk the frontier's edge list in chunks, async mode prefetches the pages of the chunks a
+  warp grabbed ahead.  SpMV (agile_spmv): page-aligned edge chunks, deterministic row sums;
+  PageRank: 10 iterations of r <- (1-d)/V + d * A^T (r / outdeg) on the in-edge CSR.
 """
 
 from __future__ import annotations
-
-import time
 
 import numpy as np
 
 ENTRIES_PER_PAGE = 1024
 
 
-def rmat_edges(scale: int, edge_factor: int, seed: int, device, abc=(0.57, 0.19, 0.19)):
+def _rmat_chunk(n: int, scale: int, g, device, abc):
+    """n RMAT edges (src, dst) int64 from generator g: per bit level, one uniform picks the quadrant."""
+    import torch
+    a, b, c = abc
+    src = torch.zeros(n, dtype=torch.int64, device=device)
+    dst = torch.zeros(n, dtype=torch.int64, device=device)
+    for lvl in range(scale):
+        r = torch.rand(n, generator=g, device=device)
+        src |= (r >= a + b).to(torch.int64) << lvl
+        dst |= (((r >= a) & (r < a + b)) | (r >= a + b + c)).to(torch.int64) << lvl
+    return src, dst
+
+
+def rmat_csr(scale: int, edge_factor: int, seed: int, device, transpose: bool = False,
+             abc=(0.57, 0.19, 0.19), chunk: int = 1 << 27):
+    """RMAT / Kronecker graph as CSR, built on the GPU in bounded memory (scale 27 = 2^31 edges).
+
+    Edges are drawn in chunks, vertex labels permuted (Graph500), duplicates and self-loops kept.
+    CSR by source (by destination with transpose=True, the in-edge CSR PageRank needs): keys
+    src << scale | dst are sorted in buckets of the leading source bits (each bucket stays below
+    2^31 keys), so col_idx is ascending within every row and the CSR is identical run to run.
+    Returns row_ptr int64 [V+1], col int32 [E], out-degree int64 [V] (of the original direction).
+    """
     import torch
     V = 1 << scale
     E = V * edge_factor
     g = torch.Generator(device=device).manual_seed(seed)
-    a, b, c = abc
-    src = torch.zeros(E, dtype=torch.int64, device=device)
-    dst = torch.zeros(E, dtype=torch.int64, device=device)
-    for lvl in range(scale):
-        r = torch.rand(E, generator=g, device=device)
-        sb = (r >= a + b).to(torch.int64)
-        db = ((r >= a) & (r < a + b) | (r >= a + b + c)).to(torch.int64)
-        src |= sb << lvl
-        dst |= db << lvl
     perm = torch.randperm(V, generator=g, device=device)
-    return perm[src], perm[dst], V
-
-
-def build_csr(src, dst, V):
-    """CSR by source: row_ptr int64 [V+1], col int32 [E] (stable by destination within a row)."""
-    import torch
-    key = src * V + dst
-    key, _ = torch.sort(key)
-    s = key // V
-    col = (key % V).to(torch.int32)
-    counts = torch.bincount(s, minlength=V)
-    row_ptr = torch.zeros(V + 1, dtype=torch.int64, device=src.device)
-    row_ptr[1:] = torch.cumsum(counts, 0)
-    return row_ptr, col
+    keys = torch.empty(E, dtype=torch.int64, device=device)
+    outdeg = torch.zeros(V, dtype=torch.int64, device=device)
+    for c0 in range(0, E, chunk):
+        n = min(chunk, E - c0)
+        src, dst = _rmat_chunk(n, scale, g, device, abc)
+        src, dst = perm[src], perm[dst]
+        outdeg += torch.bincount(src, minlength=V)
+        if transpose:
+            src, dst = dst, src
+        keys[c0:c0 + n] = (src << scale) | dst
+        del src, dst
+    nb = 1
+    while E // nb >= (1 << 30):
+        nb *= 2
+    col = torch.empty(E, dtype=torch.int32, device=device)
+    deg = torch.zeros(V, dtype=torch.int64, device=device)
+    pos = 0
+    shift = 2 * scale - (nb.bit_length() - 1)
+    for bkt in range(nb):
+        sel = keys[(keys >> shift) == bkt] if nb > 1 else keys
+        sel, _ = torch.sort(sel)
+        col[pos:pos + sel.numel()] = (sel & (V - 1)).to(torch.int32)
+        deg += torch.bincount(sel >> scale, minlength=V)
+        pos += sel.numel()
+        del sel
+    del keys
+    row_ptr = torch.zeros(V + 1, dtype=torch.int64, device=device)
+    row_ptr[1:] = torch.cumsum(deg, 0)
+    return row_ptr, col, outdeg
 
 
 def edge_values(E: int, seed: int, device):
-    """Synthetic fp32 SpMV weights in [-1, 1) (hash of the edge index)."""
+    """Synthetic fp32 SpMV weights in [-1, 1)."""
     import torch
     g = torch.Generator(device=device).manual_seed(seed + 7)
     return torch.rand(E, generator=g, device=device) * 2 - 1
@@ -72,81 +99,69 @@ def write_paged(system, dev: int, first_page: int, arr_gpu) -> int:
     return first_page + pages_for(n)
 
 
-def run_bfs(system, row_ptr, V, source: int, col_key0: int, prefetch: bool = True):
-    """Levels int32 [V] (-1 unreachable), plus stats."""
+def pick_source(row_ptr, seed: int) -> int:
+    """A seeded random vertex with out-degree > 0 (Graph500 search keys)."""
     import torch
-    dev = row_ptr.device
-    level = torch.full((V,), -1, dtype=torch.int32, device=dev)
-    level[source] = 0
-    fa = torch.zeros(V, dtype=torch.int32, device=dev)
-    fb = torch.zeros(V, dtype=torch.int32, device=dev)
-    fa[0] = source
-    n_in = 1
-    cnt = torch.zeros(1, dtype=torch.int32, device=dev)
-    ctr = torch.zeros(2, dtype=torch.int64, device=dev)
-    st = torch.cuda.current_stream(dev)
+    deg = row_ptr[1:] - row_ptr[:-1]
+    cand = torch.nonzero(deg > 0).flatten()
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    return int(cand[torch.randint(len(cand), (1,), generator=g).item()].item())
+
+
+def run_bfs(system, row_ptr, V, source: int, col_key0: int, prefetch_distance: int = 0):
+    """Levels int32 [V] (-1 unreachable), plus stats (levels, edges, page misses, ms, teps)."""
+    import torch
+    level = torch.empty(V, dtype=torch.int32, device=row_ptr.device)
+    st = system.bfs(row_ptr, V, source, col_key0, level, prefetch_distance)
+    st["teps"] = st["edges"] / (st["ms"] / 1e3) if st["ms"] else 0.0
+    return level, st
+
+
+def _timed(fn):
+    import torch
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    fn()
+    e1.record(st)
     torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(st)
-    cur = 0
-    levels = 0
-    while n_in:
-        cnt.zero_()
-        system.bfs_level(row_ptr, level, fa, n_in, fb, cnt, col_key0, cur, prefetch, ctr, stream=st.cuda_stream)
-        n_in = int(cnt.item())
-        fa, fb = fb, fa
-        cur += 1
-        levels += 1
-    e1.record(st)
-    system.sync(st.cuda_stream)
-    ms = e0.elapsed_time(e1)
-    edges = int(ctr[0].item())
-    return level, {"levels": levels, "ms": ms, "edges": edges, "teps": edges / (ms / 1e3) if ms else 0.0,
-                   "wall_s": time.perf_counter() - t0}
+    return e0.elapsed_time(e1)
 
 
-def run_spmv(system, row_ptr, V, col_key0, val_key0, x, iters: int = 1, prefetch: bool = True):
+def run_spmv(system, row_ptr, V, E, col_key0, val_key0, x, iters: int = 1, prefetch_distance: int = 0):
     import torch
-    dev = row_ptr.device
-    y = torch.empty(V, dtype=torch.float32, device=dev)
-    ctr = torch.zeros(2, dtype=torch.int64, device=dev)
-    st = torch.cuda.current_stream(dev)
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(st)
-    for _ in range(iters):
-        system.spmv(row_ptr, V, col_key0, val_key0, x, y, 1.0, 0.0, prefetch, ctr, stream=st.cuda_stream)
-    e1.record(st)
-    system.sync(st.cuda_stream)
-    ms = e0.elapsed_time(e1)
-    return y, {"ms": ms, "edges": int(ctr[0].item()), "gflops": 2 * int(ctr[0].item()) / (ms / 1e3) / 1e9}
+    y = torch.empty(V, dtype=torch.float32, device=row_ptr.device)
+    ctr = torch.zeros(2, dtype=torch.int64, device=row_ptr.device)
+    ms = _timed(lambda: [system.spmv(row_ptr, V, E, col_key0, val_key0, x, y, 1.0, 0.0, prefetch_distance, ctr)
+                         for _ in range(iters)])
+    system.sync()
+    c = ctr.cpu().numpy()
+    return y, {"ms": ms, "edges": int(c[0]), "page_misses": int(c[1]), "gflops": 2 * int(c[0]) / (ms / 1e3) / 1e9}
 
 
-def run_pagerank(system, rowT, V, colT_key0, outdeg, iters: int = 10, d: float = 0.85, prefetch: bool = True):
-    """r <- (1-d)/V + d * A^T (r / outdeg) on the transposed CSR (in-edges), unit weights."""
+def run_pagerank(system, rowT, V, E, colT_key0, outdeg, iters: int = 10, d: float = 0.85, prefetch_distance: int = 0):
+    """r <- (1-d)/V + d * A^T (r / outdeg) on the in-edge CSR, unit weights."""
     import torch
-    dev = rowT.device
-    r = torch.full((V,), 1.0 / V, dtype=torch.float32, device=dev)
+    r = torch.full((V,), 1.0 / V, dtype=torch.float32, device=rowT.device)
     y = torch.empty_like(r)
     inv = torch.where(outdeg > 0, 1.0 / outdeg.clamp(min=1).float(), torch.zeros_like(r))
-    ctr = torch.zeros(2, dtype=torch.int64, device=dev)
-    st = torch.cuda.current_stream(dev)
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(st)
-    for _ in range(iters):
-        x = r * inv
-        system.spmv(rowT, V, colT_key0, None, x, y, d, (1 - d) / V, prefetch, ctr, stream=st.cuda_stream)
-        r, y = y, r
-    e1.record(st)
-    system.sync(st.cuda_stream)
-    return r, {"ms": e0.elapsed_time(e1), "edges": int(ctr[0].item())}
+    ctr = torch.zeros(2, dtype=torch.int64, device=rowT.device)
+
+    def body():
+        nonlocal r, y
+        for _ in range(iters):
+            x = r * inv
+            system.spmv(rowT, V, E, colT_key0, None, x, y, d, (1 - d) / V, prefetch_distance, ctr)
+            r, y = y, r
+    ms = _timed(body)
+    system.sync()
+    c = ctr.cpu().numpy()
+    return r, {"ms": ms, "edges": int(c[0]), "page_misses": int(c[1])}
 
 
 def run_graph(cfg, kind: str):
-    """CLI experiments `bfs` / `spmv`: RMAT graph_scale, cache = graph_cache_fraction of edge bytes."""
+    """CLI experiments `bfs` / `spmv`: RMAT graph_scale, cache = graph_cache_fraction of the paged
+    bytes; sync (prefetch distance 0) and async (graph_prefetch) runs on a cold cache each."""
     import copy
 
     import torch
@@ -154,15 +169,14 @@ def run_graph(cfg, kind: str):
     from . import BenchResult
     from ..system import AgileSystem
     dev = torch.device("cuda", torch.cuda.current_device())
-    src, dst, V = rmat_edges(cfg.graph_scale, cfg.graph_edge_factor, cfg.system.seed, dev)
+    seed = cfg.system.seed
     if kind == "spmv":
-        # PageRank runs on the transpose (in-edges)
-        row_ptr, col = build_csr(dst, src, V)
-        outdeg = torch.bincount(src, minlength=V)
+        row_ptr, col, outdeg = rmat_csr(cfg.graph_scale, cfg.graph_edge_factor, seed, dev, transpose=True)
     else:
-        row_ptr, col = build_csr(src, dst, V)
+        row_ptr, col, outdeg = rmat_csr(cfg.graph_scale, cfg.graph_edge_factor, seed, dev)
+    V = row_ptr.numel() - 1
     E = col.numel()
-    vals = edge_values(E, cfg.system.seed, dev) if kind == "spmv" else None
+    vals = edge_values(E, seed, dev) if kind == "spmv" else None
     sc = copy.deepcopy(cfg.system)
     npages = pages_for(E) * (2 if vals is not None else 1)
     sc.device.num_blocks = max(npages, 1)
@@ -177,22 +191,20 @@ def run_graph(cfg, kind: str):
         if vals is not None:
             write_paged(system, 0, nxt, vals)
             val_key0 = nxt
-        for pf in (False, True):
+        del col, vals
+        for pd in (0, cfg.graph_prefetch):
             system.reset()
             if kind == "bfs":
-                deg = row_ptr[1:] - row_ptr[:-1]
-                cand = torch.nonzero(deg > 0).flatten()
-                g = torch.Generator(device="cpu").manual_seed(cfg.system.seed)
-                source = int(cand[torch.randint(len(cand), (1,), generator=g).item()].item())
-                _, st = run_bfs(system, row_ptr, V, source, 0, pf)
-                res.rows.append(("bfs", cfg.graph_scale, V, E, int(pf), round(st["ms"], 3), round(st["teps"] / 1e9, 6)))
-                res.info[f"bfs_levels_pf{int(pf)}"] = st["levels"]
+                source = pick_source(row_ptr, seed)
+                _, st = run_bfs(system, row_ptr, V, source, 0, pd)
+                res.rows.append(("bfs", cfg.graph_scale, V, E, pd, round(st["ms"], 3), round(st["teps"] / 1e9, 6)))
+                res.info[f"bfs_levels_pd{pd}"] = st["levels"]
             else:
-                _, st = run_pagerank(system, row_ptr, V, 0, outdeg, cfg.pagerank_iters, prefetch=pf)
-                res.rows.append(("pagerank", cfg.graph_scale, V, E, int(pf), round(st["ms"], 3),
+                _, st = run_pagerank(system, row_ptr, V, E, 0, outdeg, cfg.pagerank_iters, prefetch_distance=pd)
+                res.rows.append(("pagerank", cfg.graph_scale, V, E, pd, round(st["ms"], 3),
                                  round(st["edges"] / (st["ms"] / 1e3) / 1e9, 6)))
                 x = torch.rand(V, device=dev)
                 system.reset()
-                _, s2 = run_spmv(system, row_ptr, V, 0, val_key0, x, 1, pf)
-                res.rows.append(("spmv", cfg.graph_scale, V, E, int(pf), round(s2["ms"], 3), round(s2["gflops"], 6)))
+                _, s2 = run_spmv(system, row_ptr, V, E, 0, val_key0, x, 1, pd)
+                res.rows.append(("spmv", cfg.graph_scale, V, E, pd, round(s2["ms"], 3), round(s2["gflops"], 6)))
     return res

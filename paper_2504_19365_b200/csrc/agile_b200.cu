@@ -1,6 +1,7 @@
 // agile_b200.cu — host side of the C-ABI (include/agile_b200.h): context construction from the
 // reference's config text, HBM layout, pinned/mapped page stores, fused launches, error surfacing.
 #include <cuda_runtime.h>
+#include <cub/cub.cuh>
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -35,6 +36,8 @@ struct agile_ctx {
   // async_read WaitNodes (AgileBuf barriers) for the reads / loop / seq workloads
   void* nodes = nullptr;
   size_t nodes_cap = 0;
+  // named device scratch for the graph drivers (frontiers, bitmaps, scans, chunk partials)
+  std::map<std::string, std::pair<void*, size_t>> scratch;
 };
 
 namespace {
@@ -269,6 +272,7 @@ int agile_create(const char* config_text, int cuda_device, agile_ctx** out) {
   m.seed = ctx->seed;
   int rc;
   if ((rc = dalloc(ctx, &d.tags, lines))) return rc;
+  if ((rc = dalloc(ctx, &d.sig, lines))) return rc;
   if ((rc = dalloc(ctx, &d.wl, lines))) return rc;
   if ((rc = dalloc(ctx, &d.set_lock, d.num_sets))) return rc;
   if ((rc = dalloc(ctx, &d.hand, d.num_sets))) return rc;
@@ -313,6 +317,7 @@ int agile_destroy(agile_ctx* ctx) {
   if (ctx->d_stage) cudaFree(ctx->d_stage);
   if (ctx->d.log) cudaFree(ctx->d.log);
   if (ctx->nodes) cudaFree(ctx->nodes);
+  for (auto& kv : ctx->scratch) cudaFree(kv.second.first);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
   return 0;
@@ -415,6 +420,7 @@ int agile_reset(agile_ctx* ctx, int flags) {
   DevCtx& d = ctx->d;
   if (flags & 1) {
     CK(cudaMemset(d.tags, 0, (size_t)d.num_lines * 8));
+    CK(cudaMemset(d.sig, 0, (size_t)d.num_lines * 2));
     CK(cudaMemset(d.wl, 0, (size_t)d.num_lines * 8));
     CK(cudaMemset(d.hand, 0, (size_t)d.num_sets * 4));
     CK(cudaMemset(d.set_lock, 0, (size_t)d.num_sets * 4));
@@ -647,47 +653,210 @@ int agile_embbag_prefetch(agile_ctx* ctx, const int64_t* idx, const uint64_t* ta
   return launch(ctx, w, users, reinterpret_cast<cudaStream_t>(stream));
 }
 
-int agile_bfs_level(agile_ctx* ctx, const int64_t* row_ptr, int32_t* level, const int32_t* frontier, uint32_t n_in,
-                    int32_t* next, uint32_t* next_count, uint64_t col_key0, int32_t cur_level, int prefetch,
-                    uint64_t* counters, void* stream) {
-  if (!ctx || !row_ptr || !level || !next || !next_count || !counters) return fail(ctx, AGILE_E_ARG, "null bfs arg");
-  CK(cudaSetDevice(ctx->device));
-  BfsWork w;
-  w.row_ptr = reinterpret_cast<const long long*>(row_ptr);
-  w.level = level;
-  w.frontier = frontier;
-  w.next = next;
-  w.next_count = next_count;
-  w.col_key0 = col_key0;
-  w.n_in = n_in;
-  w.cur = cur_level;
-  w.prefetch = prefetch ? 1u : 0u;
-  w.counters = reinterpret_cast<u64*>(counters);
-  const uint32_t cap = resident_ctas<BfsWork>(ctx);
-  const uint32_t infra = ctx->d.n_engine_ctas + ctx->d.n_service_ctas;
-  const uint32_t want = (n_in + kCtaWarps - 1) / kCtaWarps;
-  const uint32_t users = std::max<uint32_t>(1, std::min<uint32_t>(want, cap > infra + 1 ? cap - infra : 1));
-  return launch(ctx, w, users, reinterpret_cast<cudaStream_t>(stream));
+// ------------------------------------------------------------------ graph drivers (K6 / K7)
+}  // extern "C"
+
+namespace {
+
+template <class T>
+T* scratch(agile_ctx* ctx, const char* name, size_t count) {
+  auto& e = ctx->scratch[name];
+  const size_t bytes = std::max<size_t>(count * sizeof(T), 256);
+  if (e.second < bytes) {
+    if (e.first) { cudaDeviceSynchronize(); cudaFree(e.first); }
+    e.first = nullptr;
+    e.second = 0;
+    if (cudaMalloc(&e.first, bytes) != cudaSuccess) return nullptr;
+    e.second = bytes;
+  }
+  return reinterpret_cast<T*>(e.first);
 }
 
-int agile_spmv(agile_ctx* ctx, const int64_t* row_ptr, uint32_t V, uint64_t col_key0, uint64_t val_key0,
-               const float* x, float* y, float alpha, float beta, int prefetch, uint64_t* counters, void* stream) {
-  if (!ctx || !row_ptr || !x || !y || !counters) return fail(ctx, AGILE_E_ARG, "null spmv arg");
+// deg[i] = out-degree of frontier vertex i (deg[n] = 0), for the exclusive scan into eoff
+__global__ void frontier_degree_kernel(const long long* row_ptr, const int* f, uint32_t n, long long* deg) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i <= n; i += (uint64_t)gridDim.x * blockDim.x)
+    deg[i] = i < n ? row_ptr[f[i] + 1] - row_ptr[f[i]] : 0;
+}
+
+__global__ void popc_kernel(const uint32_t* bits, uint32_t nw, uint32_t* cnt) {
+  for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < nw; w += (uint64_t)gridDim.x * blockDim.x)
+    cnt[w] = __popc(bits[w]);
+}
+
+// next frontier in ascending vertex order from the discovery bitmap
+__global__ void compact_kernel(const uint32_t* bits, const uint32_t* cnt, const uint32_t* pos, uint32_t nw, int* out,
+                               uint32_t* n_out) {
+  for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < nw; w += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t b = bits[w];
+    uint32_t p = pos[w];
+    while (b) {
+      const int k = __ffs(b) - 1;
+      b &= b - 1;
+      out[p++] = (int)(w * 32 + k);
+    }
+    if (w == nw - 1) *n_out = pos[w] + cnt[w];
+  }
+}
+
+__global__ void fill_f32_kernel(float* y, uint64_t n, float v) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) y[i] = v;
+}
+
+// rows crossing chunk boundaries: the chunk where the row starts walks the following chunks'
+// partials in chunk order (deterministic), then writes y
+__global__ void spmv_fixup_kernel(const long long* row_ptr, const uint32_t* last_row, const float* part_first,
+                                  const float* part_last, uint64_t nch, uint64_t E, float alpha, float beta, float* y) {
+  for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < nch; c += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t r = last_row[c];
+    if (r == 0xffffffffu) continue;
+    const long long rend = row_ptr[r + 1];
+    float s = part_last[c];
+    for (uint64_t c2 = c + 1; c2 < nch; ++c2) {
+      s += part_first[c2];
+      const uint64_t ce = (c2 + 1) * SpmvWork::kChunk;
+      const long long e1 = (long long)(ce < E ? ce : E);
+      if (rend <= e1) break;
+    }
+    y[r] = alpha * s + beta;
+  }
+}
+
+uint32_t grid_for(uint64_t n) { return (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, 148 * 16)); }
+
+}  // namespace
+
+extern "C" {
+
+int agile_bfs(agile_ctx* ctx, const int64_t* row_ptr, uint32_t V, uint32_t source, uint64_t col_key0, int32_t* level,
+              uint32_t prefetch_distance, uint64_t* stats, void* stream) {
+  if (!ctx || !row_ptr || !level || !V) return fail(ctx, AGILE_E_ARG, "null bfs arg");
+  if (source >= V) return fail(ctx, AGILE_E_ARG, "bfs source out of range");
   CK(cudaSetDevice(ctx->device));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const uint32_t nw = (V + 31) / 32;
+  int* fa = scratch<int>(ctx, "bfs.fa", V);
+  int* fb = scratch<int>(ctx, "bfs.fb", V);
+  long long* deg = scratch<long long>(ctx, "bfs.deg", (size_t)V + 1);
+  long long* eoff = scratch<long long>(ctx, "bfs.eoff", (size_t)V + 1);
+  uint32_t* visited = scratch<uint32_t>(ctx, "bfs.visited", nw);
+  uint32_t* next_bits = scratch<uint32_t>(ctx, "bfs.next", nw);
+  uint32_t* wcnt = scratch<uint32_t>(ctx, "bfs.wcnt", nw);
+  uint32_t* wpos = scratch<uint32_t>(ctx, "bfs.wpos", nw);
+  uint32_t* nnext = scratch<uint32_t>(ctx, "bfs.nnext", 1);
+  uint64_t* counters = scratch<uint64_t>(ctx, "bfs.counters", 2);
+  if (!fa || !fb || !deg || !eoff || !visited || !next_bits || !wcnt || !wpos || !nnext || !counters)
+    return fail(ctx, AGILE_E_CUDA, "bfs scratch allocation failed");
+  size_t tb1 = 0, tb2 = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tb1, deg, eoff, (int64_t)V + 1);
+  cub::DeviceScan::ExclusiveSum(nullptr, tb2, wcnt, wpos, (int64_t)nw);
+  void* tmp = scratch<uint8_t>(ctx, "bfs.cubtmp", std::max(tb1, tb2));
+  if (!tmp) return fail(ctx, AGILE_E_CUDA, "bfs scratch allocation failed");
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventRecord(e0, st));
+  CK(cudaMemsetAsync(level, 0xff, (size_t)V * 4, st));   // -1 = unreached
+  CK(cudaMemsetAsync(visited, 0, (size_t)nw * 4, st));
+  CK(cudaMemsetAsync(counters, 0, 16, st));
+  const int zero = 0;
+  const uint32_t sbit = 1u << (source & 31);
+  CK(cudaMemcpyAsync(level + source, &zero, 4, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(visited + source / 32, &sbit, 4, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(fa, &source, 4, cudaMemcpyHostToDevice, st));
+  const uint32_t cap = resident_ctas<BfsWork>(ctx);
+  const uint32_t infra = ctx->d.n_engine_ctas + ctx->d.n_service_ctas;
+  const uint32_t full = cap > infra + 1 ? cap - infra : 1;
+  uint32_t n = 1, levels = 0;
+  int cur = 0;
+  while (n) {
+    frontier_degree_kernel<<<grid_for((uint64_t)n + 1), 256, 0, st>>>(reinterpret_cast<const long long*>(row_ptr), fa, n, deg);
+    size_t tb = tb1;
+    CK(cub::DeviceScan::ExclusiveSum(tmp, tb, deg, eoff, (int64_t)n + 1, st));
+    CK(cudaMemsetAsync(next_bits, 0, (size_t)nw * 4, st));
+    BfsWork w;
+    w.row_ptr = reinterpret_cast<const long long*>(row_ptr);
+    w.frontier = fa;
+    w.eoff = eoff;
+    w.n = n;
+    w.visited = visited;
+    w.next_bits = next_bits;
+    w.level = level;
+    w.cur = cur;
+    w.col_key0 = col_key0;
+    w.pd = prefetch_distance;
+    w.counters = reinterpret_cast<u64*>(counters);
+    // small frontiers need few warps (8 edges-chunks per CTA); the grid never exceeds residency
+    const uint64_t est = (uint64_t)n * 64 / BfsWork::kChunk + 1;
+    const uint32_t users = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(full, (est + kCtaWarps - 1) / kCtaWarps));
+    int rc = launch(ctx, w, users, st);
+    if (rc) return rc;
+    popc_kernel<<<grid_for(nw), 256, 0, st>>>(next_bits, nw, wcnt);
+    tb = tb2;
+    CK(cub::DeviceScan::ExclusiveSum(tmp, tb, wcnt, wpos, (int64_t)nw, st));
+    compact_kernel<<<grid_for(nw), 256, 0, st>>>(next_bits, wcnt, wpos, nw, fb, nnext);
+    CK(cudaMemcpyAsync(&n, nnext, 4, cudaMemcpyDeviceToHost, st));
+    rc = agile_sync(ctx, st);
+    if (rc) return rc;
+    std::swap(fa, fb);
+    ++cur;
+    ++levels;
+  }
+  CK(cudaEventRecord(e1, st));
+  uint64_t cnt[2] = {0, 0};
+  CK(cudaMemcpyAsync(cnt, counters, 16, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (stats) {
+    stats[0] = levels;
+    stats[1] = cnt[0];
+    stats[2] = cnt[1];
+    stats[3] = (uint64_t)((double)ms * 1e6);
+  }
+  return 0;
+}
+
+int agile_spmv(agile_ctx* ctx, const int64_t* row_ptr, uint32_t V, uint64_t E, uint64_t col_key0, uint64_t val_key0,
+               const float* x, float* y, float alpha, float beta, uint32_t prefetch_distance, uint64_t* counters,
+               void* stream) {
+  if (!ctx || !row_ptr || !x || !y || !counters || !V) return fail(ctx, AGILE_E_ARG, "null spmv arg");
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const uint64_t nch = (E + SpmvWork::kChunk - 1) / SpmvWork::kChunk;
+  float* pf = scratch<float>(ctx, "spmv.first", nch);
+  float* pl = scratch<float>(ctx, "spmv.last", nch);
+  uint32_t* lr = scratch<uint32_t>(ctx, "spmv.lastrow", nch);
+  if (!pf || !pl || !lr) return fail(ctx, AGILE_E_CUDA, "spmv scratch allocation failed");
+  fill_f32_kernel<<<grid_for(V), 256, 0, st>>>(y, V, beta);   // rows without edges: alpha * 0 + beta
+  if (!nch) return 0;
+  CK(cudaMemsetAsync(lr, 0xff, nch * 4, st));
   SpmvWork w;
   w.row_ptr = reinterpret_cast<const long long*>(row_ptr);
+  w.V = V;
+  w.E = E;
   w.x = x;
   w.y = y;
-  w.col_key0 = col_key0;
-  w.val_key0 = val_key0;
-  w.V = V;
   w.alpha = alpha;
   w.beta = beta;
-  w.prefetch = prefetch ? 1u : 0u;
+  w.col_key0 = col_key0;
+  w.val_key0 = val_key0;
+  w.part_first = pf;
+  w.part_last = pl;
+  w.last_row = lr;
+  w.pd = prefetch_distance;
   w.counters = reinterpret_cast<u64*>(counters);
   const uint32_t cap = resident_ctas<SpmvWork>(ctx);
   const uint32_t infra = ctx->d.n_engine_ctas + ctx->d.n_service_ctas;
-  return launch(ctx, w, cap > infra + 1 ? cap - infra : 1, reinterpret_cast<cudaStream_t>(stream));
+  const uint32_t full = cap > infra + 1 ? cap - infra : 1;
+  const uint32_t users = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(full, (nch + kCtaWarps - 1) / kCtaWarps));
+  int rc = launch(ctx, w, users, st);
+  if (rc) return rc;
+  spmv_fixup_kernel<<<grid_for(nch), 256, 0, st>>>(reinterpret_cast<const long long*>(row_ptr), lr, pf, pl, nch, E,
+                                                     alpha, beta, y);
+  CK(cudaGetLastError());
+  return 0;
 }
 
 int agile_embbag_host(agile_ctx* ctx, const int64_t* idx, const uint64_t* table_key0, const int64_t* table_rows,

@@ -62,13 +62,52 @@ __device__ __forceinline__ bool probe_key_warp(const DevCtx& c, u64 key, u32& li
 // of W (one lane per way) and each group resolves one key per round with a ballot.  Returns per
 // lane the matching (line, word) or line = NONE.  Used for W <= 32; larger W falls back to the
 // per-key probe.
+__device__ __forceinline__ u32 sig_match8(uint4 v, u32 pat) {
+  // 8 x 16-bit signatures -> 8-bit match mask
+  u32 m = 0;
+  const u32 w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const u32 r = __vcmpeq2(w[i], pat);
+    m |= ((r & 1u) | ((r >> 15) & 2u)) << (2 * i);
+  }
+  return m;
+}
+
 __device__ __forceinline__ void probe_lanes(const DevCtx& c, bool active, u64 key, u32& line, u64& word) {
-  const u32 lane = lane_id();
   line = NONE;
   word = 0;
+  const u32 W = c.ways;
+  if (W <= 32 && (W & 7u) == 0) {
+    // lane-per-key signature probe: each active lane scans its own set's W signatures (2W bytes,
+    // all loads in flight at once), then confirms candidate ways against the tag word with an
+    // acquire load (a READY word read here makes the line's bytes visible to the caller).  A
+    // signature lags its tag word only between a claim's CAS and the signature store; a probe
+    // that misses in that window takes the miss path, which re-probes the full tags under the
+    // set lock, so in-flight de-duplication is unaffected.
+    if (active) {
+      const u64 base = (u64)set_of(c, key) * W;
+      const uint4* sp = reinterpret_cast<const uint4*>(c.sig + base);
+      const u32 pat = sig16(key) * 0x10001u;
+      uint4 v[4];
+#pragma unroll
+      for (u32 q = 0; q < 4; ++q) v[q] = (q * 8 < W) ? __ldcg(sp + q) : make_uint4(0u, 0u, 0u, 0u);
+      u32 m = 0;
+#pragma unroll
+      for (u32 q = 0; q < 4; ++q)
+        if (q * 8 < W) m |= sig_match8(v[q], pat) << (8 * q);
+      while (m) {
+        const u32 wy = __ffs(m) - 1;
+        m &= m - 1;
+        const u64 t = ld_acquire(&c.tags[base + wy]);
+        if (tw_live(t) && tw_key(t) == key) { line = (u32)(base + wy); word = t; break; }
+      }
+    }
+    return;
+  }
+  const u32 lane = lane_id();
   const u32 act = __ballot_sync(FULL, active);
   if (!act) return;
-  const u32 W = c.ways;
   if (W > 32 || (W & (W - 1))) {
     // generic path: one key at a time
     u32 todo = act;
@@ -273,6 +312,7 @@ __device__ int claim_key_warp(const DevCtx& c, u64 key, u32 pin_n, u32 who, u32&
     if (prev != old) continue;   // a hitter touched ref/pins: re-evaluate
     if (W <= 32 && lane < W && ((cleared >> lane) & 1u)) atomicAnd(&c.tags[base + lane], ~REF_BIT);
     if (lane == 0) {
+      c.sig[base + v] = (unsigned short)sig16(key);   // probe hint (the tag word decides)
       st_relaxed(&c.hand[set], new_hand);
       const u32 ost = tw_state(old);
       if (ost == ST_READY || ost == ST_MODIFIED) {
@@ -319,11 +359,30 @@ __device__ int claim_lanes(const DevCtx& c, bool want, u64 key, u32 pin_n, u32 w
       u32 avail = 0, ref1 = 0;
       int found = -1;
       u64 fw = 0;
-      for (u32 w = 0; w < W; ++w) {
-        const u64 t = ld_relaxed(&c.tags[base + w]);
-        if (tw_live(t) && tw_key(t) == key) { found = (int)w; fw = t; }
-        if (tw_state(t) != ST_BUSY && tw_pins(t) == 0) avail |= 1u << w;
-        if (tw_ref(t)) ref1 |= 1u << w;
+      // scan the set 8 ways per round trip (4 x 16 B loads in flight) rather than one dependent
+      // load per way: the set lock is held across this scan
+      for (u32 w0 = 0; w0 < W; w0 += 8) {
+        ulonglong2 q[4];
+#pragma unroll
+        for (u32 j = 0; j < 4; ++j) {
+          if (W & 1u) {   // odd ways: sets are not 16 B aligned
+            const u32 a = w0 + 2 * j, b = a + 1;
+            q[j] = make_ulonglong2(a < W ? ld_relaxed(&c.tags[base + a]) : 0ull,
+                                   b < W ? ld_relaxed(&c.tags[base + b]) : 0ull);
+          }
+          else q[j] = (w0 + 2 * j < W) ? __ldcg(reinterpret_cast<const ulonglong2*>(c.tags + base + w0) + j)
+                                       : make_ulonglong2(0ull, 0ull);
+        }
+#pragma unroll
+        for (u32 j = 0; j < 8; ++j) {
+          const u32 w = w0 + j;
+          const u64 t = (j & 1u) ? q[j >> 1].y : q[j >> 1].x;
+          if (w < W) {
+            if (tw_live(t) && tw_key(t) == key) { found = (int)w; fw = t; }
+            if (tw_state(t) != ST_BUSY && tw_pins(t) == 0) avail |= 1u << w;
+            if (tw_ref(t)) ref1 |= 1u << w;
+          }
+        }
       }
       if (found >= 0) {
         u64 w2 = fw;
@@ -350,6 +409,7 @@ __device__ int claim_lanes(const DevCtx& c, bool want, u64 key, u32 pin_n, u32 w
             const u64 nw = tw_make(ST_BUSY, key, tw_ver(old) + 1, true, pin_n);
             st_relaxed(&c.wl[base + v], ((u64)((tw_ver(old) + 1) & 0x1FFu)) << 55);   // open the waiter list
             if (atom_cas_acqrel(&c.tags[base + v], old, nw) == old) {
+              c.sig[base + v] = (unsigned short)sig16(key);   // probe hint (the tag word decides)
               for (u32 m = cleared; m; m &= m - 1) atomicAnd(&c.tags[base + (__ffs(m) - 1)], ~REF_BIT);
               st_relaxed(&c.hand[set], nh);
               const u32 ost = tw_state(old);
@@ -1437,7 +1497,10 @@ __device__ __forceinline__ void user_done(const DevCtx& c) {
 #define AGILE_MIN_CTAS 2
 #endif
 template <class Work>
-__global__ void __launch_bounds__(kCtaThreads, AGILE_MIN_CTAS) agile_kernel(DevCtx c, Launch L, Work work) {
+// __grid_constant__: the device functions take the context and the workload by reference; without
+// it every thread would copy both structs from the parameter bank into local memory at entry.
+__global__ void __launch_bounds__(kCtaThreads, AGILE_MIN_CTAS)
+    agile_kernel(const __grid_constant__ DevCtx c, const Launch L, const __grid_constant__ Work work) {
   const Role r = take_role(c);
   const u32 warp = threadIdx.x >> 5;
   if (r.kind == 0) {

@@ -179,6 +179,7 @@ struct DevCtx {
   u64 watchdog_ns;
   // cache
   u64* tags;
+  unsigned short* sig;      // per-line 16-bit key signature: probe hint, the tag word decides
   u64* wl;                 // per-line async_read waiter stack (agile_core.cuh WaitNode)
   u32* set_lock;
   u32* hand;
@@ -317,6 +318,9 @@ __host__ __device__ __forceinline__ u32 set_of_key(u64 key, u32 num_sets, u32 po
   return pow2 ? (h & (num_sets - 1)) : (h % num_sets);
 }
 __device__ __forceinline__ u32 set_of(const DevCtx& c, u64 key) { return set_of_key(key, c.num_sets, c.sets_pow2); }
+// 16-bit signature of a key (independent of the set-index bits): a set's W signatures are 2W
+// bytes, so one lane scans a 32-way set with four 16 B loads instead of 32 tag words
+__host__ __device__ __forceinline__ u32 sig16(u64 key) { return (u32)((key * 0x9E3779B97F4A7C15ull) >> 48); }
 __device__ __forceinline__ uint8_t* line_ptr(const DevCtx& c, u32 line) { return c.lines + ((u64)line << kBlockShift); }
 
 }  // namespace agile

@@ -5,6 +5,7 @@
 //   GatherWork     prefetch + array_get gather epochs (bench/sweeps.py:39-88)
 //   EmbBagWork     DLRM embedding-bag over cached rows                    — K5
 #pragma once
+#include <climits>
 #include "agile_core.cuh"
 #undef SPIN_FILE_ID
 #define SPIN_FILE_ID 2
@@ -60,7 +61,7 @@ struct SeqWork {
   uint4* pages;           // optional n * 4 KiB
   uint4* scratch;         // 4 KiB
   WaitNode* nodes;        // 1
-  __device__ void run(const DevCtx& c, u32 uidx, u32 nusers) {
+  __device__ void run(const DevCtx& c, u32 uidx, u32 nusers) const {
     if (uidx != 0 || threadIdx.x >= 32) return;
     const u32 lane = lane_id();
     const u32 who = user_who(0) & ~31u;   // task "u0"
@@ -91,7 +92,7 @@ struct ReadsWork {
   u32 tasks, reads, epochs, async_mode;
   u64 compute_ns;
   static constexpr int MAXR = 64;
-  __device__ void issue(const DevCtx& c, u32 task, bool act, u32 e, u32 set, u32 who, u32 sq_start) {
+  __device__ void issue(const DevCtx& c, u32 task, bool act, u32 e, u32 set, u32 who, u32 sq_start) const {
     for (u32 i = 0; i < reads; ++i) {
       const u64 key = act ? keys[((u64)e * tasks + task) * reads + i] : 0ull;
       const u64 slot = ((u64)task * 2 + set) * reads + i;
@@ -99,7 +100,7 @@ struct ReadsWork {
                       sq_start + i + e * reads);
     }
   }
-  __device__ void wait_set(const DevCtx& c, u32 task, bool act, u32 set, u64& dg) {
+  __device__ void wait_set(const DevCtx& c, u32 task, bool act, u32 set, u64& dg) const {
     for (u32 i = 0; i < reads; ++i) {
       const u64 slot = ((u64)task * 2 + set) * reads + i;
       wait_nodes_warp(c, act, nodes + (act ? slot : 0));
@@ -109,7 +110,7 @@ struct ReadsWork {
       }
     }
   }
-  __device__ void run(const DevCtx& c, u32 uidx, u32 nusers) {
+  __device__ void run(const DevCtx& c, u32 uidx, u32 nusers) const {
     const u32 task = uidx * kCtaThreads + threadIdx.x;
     const bool act = task < tasks;
     const u32 who = user_who(uidx);
@@ -155,7 +156,7 @@ struct LoopWork {
   u64 num_blocks;
   u64 warmup_ns, measure_ns;
   u64 max_per_task;
-  __device__ void run(const DevCtx& c, u32 uidx, u32 nusers) {
+  __device__ void run(const DevCtx& c, u32 uidx, u32 nusers) const {
     const u32 idx = uidx * kCtaThreads + threadIdx.x;
     const bool act = idx < conc;
     const u32 who = user_who(uidx);
@@ -214,13 +215,13 @@ struct GatherWork {
   u64* epoch_t;
   u32 tasks, epochs, gathers, async_mode;
   u64 compute_ns;
-  __device__ void prefetch_epoch(const DevCtx& c, bool act, u32 task, u32 e, u32 who, u32 sq_start) {
+  __device__ void prefetch_epoch(const DevCtx& c, bool act, u32 task, u32 e, u32 who, u32 sq_start) const {
     for (u32 g = 0; g < gathers; ++g) {
       const u64 key = act ? keys[((u64)task * epochs + e) * gathers + g] : 0ull;
       prefetch_warp(c, act, key, who, sq_start + g + e * gathers, false);
     }
   }
-  __device__ void get_epoch(const DevCtx& c, bool act, u32 task, u32 e, u32 who, u32 sq_start) {
+  __device__ void get_epoch(const DevCtx& c, bool act, u32 task, u32 e, u32 who, u32 sq_start) const {
     for (u32 g = 0; g < gathers; ++g) {
       const u64 key = act ? keys[((u64)task * epochs + e) * gathers + g] : 0ull;
       // array_get = read_range loop (software_cache.py:212-219): access, wait READY, read.  The
@@ -253,7 +254,7 @@ struct GatherWork {
       if (act) values[((u64)task * epochs + e) * gathers + g] = val;
     }
   }
-  __device__ void run(const DevCtx& c, u32 uidx, u32 nusers) {
+  __device__ void run(const DevCtx& c, u32 uidx, u32 nusers) const {
     const u32 task = uidx * kCtaThreads + threadIdx.x;
     const bool act = task < tasks;
     const u32 who = user_who(uidx);
@@ -320,7 +321,7 @@ struct EmbBagWork {
     return pool++;
   }
 
-  __device__ void run(const DevCtx& c, u32 uidx, u32 nusers) {
+  __device__ void run(const DevCtx& c, u32 uidx, u32 nusers) const {
     const u32 lane = lane_id();
     const u32 gw = uidx * kCtaWarps + (threadIdx.x >> 5);
     const u32 nbags = B * T;
@@ -393,6 +394,7 @@ struct EmbBagWork {
         if (ready && !tw_ref(word)) atomicOr(&c.tags[line], REF_BIT);   // on_hit
         u32 need = __ballot_sync(FULL, a && !ready);
         if (need && first) misses_local += __popc(need);
+        const bool waited = need != 0;
         Spin sp;
         while (need) {
           const bool nm = (need >> lane) & 1u;
@@ -420,7 +422,9 @@ struct EmbBagWork {
         }
         if (aborted(c)) break;
         first = false;
-        fence_acq_rel();
+        // hits were confirmed by an acquire load of their READY tag word (probe_lanes); lines
+        // that became READY while we polled them (relaxed) need the fence
+        if (waited) fence_acq_rel();
         // 2. sum the L rows, lane owns dims [4*lane, 4*lane+4): 8 row loads (16 B/lane, 512 B
         //    coalesced each) in flight per chunk, rows added in l order (bit-exact with the oracle)
         acc = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -491,168 +495,451 @@ struct EmbBagWork {
   }
 };
 
-// ------------------------------------------------------------------ paged CSR reads (K6/K7)
-// Read one u32 per active lane from page `key` at byte offset `off` through the cache: batched
-// probe, miss path (claim or find the fill, wait), read, seqlock validation, retry.  Nothing is
-// held across a wait.  Returns the value; lanes that gave up (abort) get 0.
-__device__ u32 read_u32_warp(const DevCtx& c, bool active, u64 key, u32 off, u32 who, u32 sq_start) {
+// ------------------------------------------------------------------ paged arrays (K6/K7)
+// Graph arrays (CSR col_idx, SpMV values) live in the page store, 1024 x 4 B entries per 4 KiB
+// page; key = array key0 + entry / 1024.  Warps walk them in increasing position order, so a
+// warp keeps the two pages it resolved last in registers (PageRegs) and only probes the cache
+// when it crosses into a new page.  Nothing is pinned: reads are validated seqlock-style against
+// the tag word (identity = state | version | key) after the fact, and a pass whose page changed
+// identity under it is redone (a READY line is only reassigned through a fresh claim, which bumps
+// the version).  No lock or pin is held across any wait (gpu_api.py:233-248).
+struct PageRegs {
+  u64 key[2];
+  u32 line[2];
+  u64 word[2];
+  __device__ __forceinline__ void clear() { key[0] = key[1] = ~0ull; }
+};
+
+// Resolve every active lane's page to a READY line.  Lanes sharing a key coalesce
+// (__match_any_sync, lowest lane leads: warp_coalesce, gpu_api.py:40-54); register hits skip the
+// probe; the other leaders probe, and run the miss path (claim or attach to the in-flight fill,
+// submit, wait for READY) when the page is not resident.  Returns false when the run aborts.
+__device__ bool resolve_pages_warp(const DevCtx& c, bool act, u64 key, PageRegs& pr, u32& line, u64& word,
+                                   u32 who, u32 sq, u32& misses) {
   const u32 lane = lane_id();
-  u32 val = 0;
-  bool pend = active;
-  Spin sp;
-  while (__any_sync(FULL, pend)) {
-    u32 line; u64 word;
-    probe_lanes(c, pend, key, line, word);
-    bool ready = pend && line != NONE && (tw_state(word) == ST_READY || tw_state(word) == ST_MODIFIED);
-    if (ready && !tw_ref(word)) atomicOr(&c.tags[line], REF_BIT);
-    const bool nm = pend && !ready;
-    if (__any_sync(FULL, nm)) {
-      const Req r = access_warp(c, nm, key, false, who, sq_start, false);
-      bool got = nm && (r.kind == R_HIT || r.kind == R_FILLING || r.kind == R_MISS);
-      if (got) { line = r.line; word = r.word; }
-      u32 wp = __ballot_sync(FULL, got);
-      Spin s2;
-      while (wp) {
-        bool rd = false, gone = false;
-        if ((wp >> lane) & 1u) {
-          const u64 w = ld_relaxed(&c.tags[line]);
-          if (!tw_live(w) || tw_key(w) != key) gone = true;
-          else if (tw_state(w) == ST_READY || tw_state(w) == ST_MODIFIED) { word = w; rd = true; }
-        }
-        if (gone) got = false;
-        wp &= ~__ballot_sync(FULL, rd || gone);
-        if (wp && !s2.again(c, 1024, __LINE__ + 100000 * SPIN_FILE_ID)) break;
-      }
-      ready = ready || got;
-      fence_acq_rel();
-    }
-    u32 v = 0;
-    if (ready) v = __ldcg(reinterpret_cast<const unsigned int*>(line_ptr(c, line) + off));
-    fence_acq_rel();
-    bool ok = false;
-    if (ready) ok = ((ld_relaxed(&c.tags[line]) ^ word) & IDENT_MASK) == 0;
-    if (ok) { val = v; pend = false; }
-    if (aborted(c)) break;
-    if (__any_sync(FULL, pend) && !__any_sync(FULL, ok) && !sp.again(c, 1024, __LINE__ + 100000 * SPIN_FILE_ID)) break;
+  bool need = act;
+  if (act) {
+    if (key == pr.key[0]) { line = pr.line[0]; word = pr.word[0]; need = false; }
+    else if (key == pr.key[1]) { line = pr.line[1]; word = pr.word[1]; need = false; }
   }
-  return val;
+  if (!__any_sync(FULL, need)) return true;
+  u32 grp = __match_any_sync(FULL, need ? key : ~0ull);
+  if (!need) grp = 0;
+  const bool leader = need && (grp & lanemask_lt()) == 0;
+  u32 l = NONE;
+  u64 w = 0;
+  probe_lanes(c, leader, key, l, w);
+  const bool ready = leader && l != NONE && tw_state(w) >= ST_READY;
+  if (ready && !tw_ref(w)) atomicOr(&c.tags[l], REF_BIT);   // on_hit (software_cache.py:124-126)
+  u32 pend = __ballot_sync(FULL, leader && !ready);
+  misses += __popc(pend);
+  Spin sp;
+  while (pend) {
+    const bool nm = (pend >> lane) & 1u;
+    const Req r = access_warp(c, nm, key, false, who, sq, false);
+    const bool got = nm && (r.kind == R_HIT || r.kind == R_FILLING || r.kind == R_MISS);
+    if (got) { l = r.line; w = r.word; }
+    u32 wp = __ballot_sync(FULL, got);
+    u32 done = 0;
+    Spin s2;
+    while (wp) {
+      bool rd = false, gone = false;
+      if ((wp >> lane) & 1u) {
+        const u64 t = ld_relaxed(&c.tags[l]);
+        if (!tw_live(t) || tw_key(t) != key) gone = true;
+        else if (tw_state(t) >= ST_READY) { w = t; rd = true; }
+      }
+      done |= __ballot_sync(FULL, rd);
+      wp &= ~__ballot_sync(FULL, rd || gone);
+      if (wp && !s2.again(c, 1024, __LINE__ + 100000 * SPIN_FILE_ID)) return false;
+    }
+    pend &= ~done;
+    if (aborted(c)) return false;
+    if (pend && !done && !sp.again(c, 1024, __LINE__ + 100000 * SPIN_FILE_ID)) return false;
+  }
+  fence_acq_rel();   // READY observed above (relaxed) -> the line's bytes are visible
+  const u32 ll = need ? (u32)(__ffs(grp) - 1) : lane;
+  const u32 bl = __shfl_sync(FULL, l, ll);
+  const u64 bw = __shfl_sync(FULL, w, ll);
+  if (need) { line = bl; word = bw; }
+  // keep the pages of the two highest leaders (positions grow with the lane)
+  const u32 lb = __ballot_sync(FULL, leader);
+  const int h1 = 31 - __clz(lb);
+  const u32 rest = lb & ~(1u << h1);
+  const int h0 = rest ? 31 - __clz(rest) : -1;
+  const u64 k1 = __shfl_sync(FULL, key, h1);
+  const u32 l1 = __shfl_sync(FULL, line, h1);
+  const u64 w1 = __shfl_sync(FULL, word, h1);
+  const u64 k0 = __shfl_sync(FULL, key, h0 < 0 ? h1 : h0);
+  const u32 l0 = __shfl_sync(FULL, line, h0 < 0 ? h1 : h0);
+  const u64 w0 = __shfl_sync(FULL, word, h0 < 0 ? h1 : h0);
+  if (h0 < 0) {   // one new page: it replaces the older register entry
+    if (pr.key[1] != k1) { pr.key[0] = pr.key[1]; pr.line[0] = pr.line[1]; pr.word[0] = pr.word[1]; }
+  } else {
+    pr.key[0] = k0; pr.line[0] = l0; pr.word[0] = w0;
+  }
+  pr.key[1] = k1; pr.line[1] = l1; pr.word[1] = w1;
+  return true;
 }
 
-// BFS level (K6): top-down expansion of `frontier` over a CSR whose col_idx array is paged
-// (1024 int32 per 4 KiB page, page p of the array = key col_key0 + p).  Warps take frontier
-// vertices dynamically; lanes walk the vertex's edges 32 at a time, claim unvisited neighbours
-// with a CAS on level[] and append them (warp-aggregated) to the next frontier.  With prefetch,
-// each newly discovered vertex's first col_idx page is pulled toward the cache right away, so the
-// next level's reads overlap this level's expansion (the AGILE async pattern).
+// After reading: every distinct page the warp read must still hold the identity it was read
+// under (one tag load per distinct page).  False -> redo the reads.
+__device__ __forceinline__ bool validate_pages_warp(const DevCtx& c, bool act, u64 key, u32 line, u64 word) {
+  fence_acq_rel();
+  u32 grp = __match_any_sync(FULL, act ? key : ~0ull);
+  const bool leader = act && (grp & lanemask_lt()) == 0;
+  bool bad = false;
+  if (leader) bad = ((ld_relaxed(&c.tags[line]) ^ word) & IDENT_MASK) != 0;
+  return !__any_sync(FULL, bad);
+}
+
+// Largest i in [lo, hi] with a[i] <= x, for non-decreasing a and a[lo] <= x: 32 pivots per
+// round trip, so ~log32(hi - lo) dependent loads.
+__device__ __forceinline__ u64 warp_search_le(const long long* a, u64 lo, u64 hi, long long x) {
+  const u32 lane = lane_id();
+  while (hi - lo >= 32) {
+    const u64 span = hi - lo;
+    const u64 p = lo + (span * lane) / 32;
+    const u32 b = __ballot_sync(FULL, __ldcg(a + p) <= x);
+    const u32 k = 31 - __clz(b | 1u);
+    const u64 nlo = lo + (span * k) / 32;
+    const u64 nhi = k == 31 ? hi : lo + (span * (k + 1)) / 32 - 1;
+    lo = nlo;
+    hi = nhi;
+  }
+  const u64 p = lo + lane;
+  const u32 b = __ballot_sync(FULL, p <= hi && __ldcg(a + p) <= x);
+  return lo + (31 - __clz(b | 1u));
+}
+
+// Largest window slot j in [0, 30] with ev_j <= x (ev non-decreasing across lanes 0..31).
+__device__ __forceinline__ u32 window_slot(long long ev, long long x) {
+  u32 j = 0;
+#pragma unroll
+  for (u32 st = 16; st; st >>= 1) {
+    const u32 p = j + st;
+    const long long e = __shfl_sync(FULL, ev, p > 30 ? 30 : p);
+    if (p <= 30 && e <= x) j = p;
+  }
+  return j;
+}
+
+// BFS level (K6): top-down expansion of a SORTED frontier over a CSR whose col_idx is paged.
+// The frontier's out-edges form one virtual edge list [0, m) (eoff = exclusive scan of frontier
+// degrees); warps take it in chunks of kChunk edges, so consecutive warps walk consecutive CSR
+// positions: each col_idx page is resolved once per warp that needs it.  A window of 31 frontier
+// vertices (lane j: eoff, CSR row start) maps each lane's edge to its CSR position by a 5-step
+// shuffle search.  Discovery: one relaxed read of the visited bitmap (L2-resident: V/8 bytes),
+// atomicOr only for unseen vertices, level[] store, and the next-frontier bitmap.  Async mode
+// (pd > 0): a warp grabs pd chunks ahead and prefetches their pages before expanding the oldest
+// (the AGILE prefetch pattern, gpu_api.py:345-361); pd = 0 is the synchronous baseline.
 struct BfsWork {
   const long long* row_ptr;   // [V+1] (HBM)
-  int* level;                 // [V], -1 = unvisited
-  const int* frontier;        // [n_in]
-  int* next;                  // [V]
-  unsigned int* next_count;
-  u64 col_key0;
-  u32 n_in;
+  const int* frontier;        // [n] ascending
+  const long long* eoff;      // [n+1], eoff[n] = m
+  u32 n;
+  u32* visited;               // [(V+31)/32]
+  u32* next_bits;             // [(V+31)/32]
+  int* level;
   int cur;
-  u32 prefetch;
-  u64* counters;              // [0] edges traversed
-  __device__ void run(const DevCtx& c, u32 uidx, u32 nusers) {
+  u64 col_key0;
+  u32 pd;
+  u64* counters;              // [0] edges expanded, [1] page misses
+  static constexpr u32 kChunk = 2048;
+  static constexpr u32 kMaxPd = 4;
+
+  __device__ __forceinline__ void load_window(u64 i, long long& ev, long long& rp) const {
+    const u64 wi = i + lane_id();
+    ev = wi <= n ? __ldcg(eoff + wi) : LLONG_MAX;
+    rp = wi < n ? __ldg(row_ptr + __ldg(frontier + wi)) : 0;
+  }
+
+  __device__ void prefetch_chunk(const DevCtx& c, u64 ch, u64 m, u32 who, u32 sq) const {
+    const u64 e0 = ch * kChunk, e1 = min(m, e0 + kChunk);
+    const u64 i = warp_search_le(eoff, 0, n, (long long)e0);
+    long long ev, rp;
+    load_window(i, ev, rp);
+    const long long evn = __shfl_down_sync(FULL, ev, 1);
+    // lane j: the page of the first edge of window vertex j that falls in the chunk
+    const bool has = lane_id() < 31 && (u64)ev < e1 && evn > ev && i + lane_id() < n;
+    const long long first = ev < (long long)e0 ? (long long)e0 : ev;
+    const u64 key = col_key0 + (u64)((rp + (first - ev)) >> 10);
+    prefetch_warp(c, has, key, who, sq, true);
+  }
+
+  __device__ void run(const DevCtx& c, u32 uidx, u32 nusers) const {
     const u32 lane = lane_id();
     const u32 gw = uidx * kCtaWarps + (threadIdx.x >> 5);
     const u32 who = user_who(uidx);
+    const u64 m = (u64)__ldcg(eoff + n);
+    const u64 nch = (m + kChunk - 1) / kChunk;
+    const u32 depth = pd > kMaxPd ? kMaxPd : pd;
+    PageRegs pr;
+    pr.clear();
+    u32 misses = 0;
     u64 edges = 0;
-    while (true) {
-      u32 i = 0;
-      if (lane == 0) i = (u32)atomicAdd(&c.run->work_next, 1ull);
-      i = __shfl_sync(FULL, i, 0);
-      if (i >= n_in || aborted(c)) break;
-      const int v = frontier[i];
-      const long long s = row_ptr[v], e = row_ptr[v + 1];
-      edges += (u64)(e - s);
-      for (long long b = s; b < e; b += 32) {
-        const long long ed = b + lane;
-        const bool act = ed < e;
-        const u64 key = col_key0 + (u64)(act ? (ed >> 10) : 0);
-        const u32 u = read_u32_warp(c, act, key, (u32)(act ? (ed & 1023) * 4 : 0), who, gw);
-        bool disc = false;
-        if (act && ld_relaxed(reinterpret_cast<const u32*>(level) + u) == 0xffffffffu)
-          disc = atomicCAS(level + u, -1, cur + 1) == -1;
-        const u32 db = __ballot_sync(FULL, disc);
-        if (db) {
-          u32 base = 0;
-          if (lane == __ffs(db) - 1) base = atomicAdd(next_count, (u32)__popc(db));
-          base = __shfl_sync(FULL, base, __ffs(db) - 1);
-          if (disc) next[base + __popc(db & lanemask_lt())] = (int)u;
-          if (prefetch) {
-            u64 pk = 0;
-            if (disc) pk = col_key0 + (u64)(row_ptr[u] >> 10);
-            const bool has = disc && row_ptr[u + 1] > row_ptr[u];
-            prefetch_warp(c, has, pk, who, gw, true);
+    u64 ring[kMaxPd];
+    u32 head = 0, count = 0;
+    auto grab = [&]() -> u64 {
+      u64 g = 0;
+      if (lane == 0) g = atomicAdd(&c.run->work_next, 1ull);
+      return __shfl_sync(FULL, g, 0);
+    };
+    for (u32 k = 0; k < depth; ++k) {
+      const u64 g = grab();
+      if (g >= nch) break;
+      prefetch_chunk(c, g, m, who, gw + k);
+      ring[(head + count) % kMaxPd] = g;
+      ++count;
+    }
+    while (!aborted(c)) {
+      u64 ch;
+      if (depth) {
+        if (!count) break;
+        ch = ring[head];
+        head = (head + 1) % kMaxPd;
+        --count;
+        const u64 g = grab();
+        if (g < nch) {
+          prefetch_chunk(c, g, m, who, gw + (u32)g);
+          ring[(head + count) % kMaxPd] = g;
+          ++count;
+        }
+      } else {
+        ch = grab();
+        if (ch >= nch) break;
+      }
+      const u64 e0 = ch * kChunk, e1 = min(m, e0 + kChunk);
+      edges += e1 - e0;
+      u64 i = warp_search_le(eoff, 0, n, (long long)e0);
+      long long ev, rp;
+      load_window(i, ev, rp);
+      for (u64 e = e0; e < e1 && !aborted(c); e += 32) {
+        const long long my = (long long)(e + lane);
+        bool unloc = (u64)my < e1;
+        Spin sp;
+        while (__any_sync(FULL, unloc)) {
+          const long long wend = __shfl_sync(FULL, ev, 31);
+          bool inw = unloc && my < wend;
+          if (!__any_sync(FULL, inw)) {
+            // the earliest unlocated edge lies past the window: slide (one reload), else search
+            const long long x = __shfl_sync(FULL, my, __ffs(__ballot_sync(FULL, unloc)) - 1);
+            i += 31;
+            load_window(i, ev, rp);
+            if (x >= __shfl_sync(FULL, ev, 31)) {
+              i = warp_search_le(eoff, i, n, x);
+              load_window(i, ev, rp);
+            }
+            continue;
           }
+          const u32 k = window_slot(ev, my);
+          const long long pos = __shfl_sync(FULL, rp, k) + (my - __shfl_sync(FULL, ev, k));
+          const u64 key = col_key0 + (u64)(pos >> 10);
+          u32 line = 0;
+          u64 word = 0;
+          if (!resolve_pages_warp(c, inw, key, pr, line, word, who, gw, misses)) return;
+          u32 u = 0;
+          if (inw) u = __ldcg(reinterpret_cast<const unsigned int*>(line_ptr(c, line) + ((u32)pos & 1023u) * 4));
+          if (!validate_pages_warp(c, inw, key, line, word)) {
+            pr.clear();   // a page changed identity under the read: resolve again
+            if (!sp.again(c, 256, __LINE__ + 100000 * SPIN_FILE_ID)) return;
+            continue;
+          }
+          if (inw) {
+            const u32 bit = 1u << (u & 31u);
+            u32* vw = visited + (u >> 5);
+            if (!(ld_relaxed(vw) & bit) && !(atomicOr(vw, bit) & bit)) {
+              level[u] = cur + 1;
+              atomicOr(next_bits + (u >> 5), bit);
+            }
+          }
+          unloc = unloc && !inw;
         }
       }
     }
-    if (lane == 0 && edges) atomicAdd(&counters[0], edges);
+    if (lane == 0) {
+      if (edges) atomicAdd(&counters[0], edges);
+      if (misses) atomicAdd(&counters[1], (u64)misses);
+    }
   }
 };
 
-// SpMV over a paged CSR (K7): y[r] = alpha * sum_e val[e] * x[col[e]] + beta, col (int32) and val
-// (fp32) paged (1024 per page; val_key0 = ~0 -> unit weights, the PageRank A^T case).  Warps take
-// blocks of 32 rows dynamically; the next block's first pages are prefetched before the current
-// block is processed (next-chunk prefetch).  One warp per row: lanes over the edges, warp sum.
+// SpMV over a paged CSR (K7): y[r] = alpha * sum_e val[e] * x[col[e]] + beta.  col (int32) and val
+// (fp32; val_key0 = ~0 -> unit weights, the PageRank A^T case) are paged; the edge list is cut
+// into page-aligned chunks of 1024 edges, so one chunk = one col page (+ one val page) resolved
+// once.  Lanes read 4 passes of 32 consecutive entries before touching x (ILP), map edges to rows
+// through a window of 31 row starts, and sum rows with a segmented warp scan in a fixed order.
+// Rows wholly inside a chunk are written directly; a row crossing a chunk boundary leaves its
+// chunk partials in part_first / part_last, summed in chunk order by spmv_fixup_kernel
+// (deterministic run to run).  Async mode (pd > 0) prefetches the pages of the chunks a warp
+// grabbed ahead.
 struct SpmvWork {
-  const long long* row_ptr;
+  const long long* row_ptr;   // [V+1]
+  u32 V;
+  u64 E;
   const float* x;
   float* y;
-  u64 col_key0, val_key0;
-  u32 V;
   float alpha, beta;
-  u32 prefetch;
-  u64* counters;   // [0] edges
-  __device__ void run(const DevCtx& c, u32 uidx, u32 nusers) {
+  u64 col_key0, val_key0;
+  float* part_first;          // [nchunks] partial of the chunk's first row if it began earlier
+  float* part_last;           // [nchunks] partial of the chunk's last row if it continues
+  u32* last_row;              // [nchunks]
+  u32 pd;
+  u64* counters;              // [0] edges, [1] page misses
+  static constexpr u32 kChunk = 1024;
+  static constexpr u32 kMaxPd = 4;
+
+  __device__ void run(const DevCtx& c, u32 uidx, u32 nusers) const {
     const u32 lane = lane_id();
     const u32 gw = uidx * kCtaWarps + (threadIdx.x >> 5);
     const u32 who = user_who(uidx);
-    const u32 nblocks = (V + 31) / 32;
+    const u64 nch = (E + kChunk - 1) / kChunk;
+    const bool weighted = val_key0 != ~0ull;
+    const u32 depth = pd > kMaxPd ? kMaxPd : pd;
+    PageRegs pr;
+    pr.clear();
+    u32 misses = 0;
     u64 edges = 0;
-    u32 blk = 0;
-    if (lane == 0) blk = (u32)atomicAdd(&c.run->work_next, 1ull);
-    blk = __shfl_sync(FULL, blk, 0);
-    while (blk < nblocks && !aborted(c)) {
-      u32 nxt = 0;
-      if (lane == 0) nxt = (u32)atomicAdd(&c.run->work_next, 1ull);
-      nxt = __shfl_sync(FULL, nxt, 0);
-      if (prefetch && nxt < nblocks) {
-        // pull the next block's edge pages (col, and val when weighted) toward the cache
-        const u32 r0 = nxt * 32, r1 = min(V, r0 + 32);
-        const long long s0 = row_ptr[r0], s1 = row_ptr[r1];
-        const long long p0 = s0 >> 10, p1 = (s1 + 1023) >> 10;
-        const long long np = p1 - p0;
-        const bool h = (long long)lane < np;
-        prefetch_warp(c, h, col_key0 + (u64)(p0 + lane), who, gw + 1, true);
-        if (val_key0 != ~0ull) prefetch_warp(c, h, val_key0 + (u64)(p0 + lane), who, gw + 2, true);
-      }
-      const u32 r0 = blk * 32, r1 = min(V, r0 + 32);
-      for (u32 r = r0; r < r1; ++r) {
-        const long long s = row_ptr[r], e = row_ptr[r + 1];
-        float acc = 0.f;
-        for (long long b = s; b < e; b += 32) {
-          const long long ed = b + lane;
-          const bool act = ed < e;
-          const u64 pg = (u64)(act ? (ed >> 10) : 0);
-          const u32 off = (u32)(act ? (ed & 1023) * 4 : 0);
-          const u32 col = read_u32_warp(c, act, col_key0 + pg, off, who, gw);
-          float w = 1.f;
-          if (val_key0 != ~0ull) w = __uint_as_float(read_u32_warp(c, act, val_key0 + pg, off, who, gw));
-          if (act) acc += w * __ldg(x + col);
-        }
-#pragma unroll
-        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
-        if (lane == 0) y[r] = alpha * acc + beta;
-        edges += (u64)(e - s);
-      }
-      blk = nxt;
+    u64 ring[kMaxPd];
+    u32 head = 0, count = 0;
+    auto grab = [&]() -> u64 {
+      u64 g = 0;
+      if (lane == 0) g = atomicAdd(&c.run->work_next, 1ull);
+      return __shfl_sync(FULL, g, 0);
+    };
+    auto prefetch = [&](u64 g, u32 sq) {
+      const u64 key = (lane == 0) ? col_key0 + g : val_key0 + g;
+      prefetch_warp(c, lane == 0 || (lane == 1 && weighted), key, who, sq, true);
+    };
+    for (u32 k = 0; k < depth; ++k) {
+      const u64 g = grab();
+      if (g >= nch) break;
+      prefetch(g, gw + k);
+      ring[(head + count) % kMaxPd] = g;
+      ++count;
     }
-    if (lane == 0 && edges) atomicAdd(&counters[0], edges);
+    while (!aborted(c)) {
+      u64 ch;
+      if (depth) {
+        if (!count) break;
+        ch = ring[head];
+        head = (head + 1) % kMaxPd;
+        --count;
+        const u64 g = grab();
+        if (g < nch) {
+          prefetch(g, gw + (u32)g);
+          ring[(head + count) % kMaxPd] = g;
+          ++count;
+        }
+      } else {
+        ch = grab();
+        if (ch >= nch) break;
+      }
+      const u64 e0 = ch * kChunk, e1 = min(E, e0 + kChunk);
+      edges += e1 - e0;
+      const u64 r0 = warp_search_le(row_ptr, 0, V, (long long)e0);
+      Spin sp;
+      while (true) {   // one attempt per chunk; redone if a page changed identity meanwhile
+        // resolve the chunk's col page (lane 0) and val page (lane 1)
+        const bool pa = lane == 0 || (lane == 1 && weighted);
+        const u64 pkey = lane == 0 ? col_key0 + ch : val_key0 + ch;
+        u32 pl = 0;
+        u64 pw = 0;
+        if (!resolve_pages_warp(c, pa, pkey, pr, pl, pw, who, gw, misses)) return;
+        const uint8_t* colp = line_ptr(c, __shfl_sync(FULL, pl, 0));
+        const uint8_t* valp = weighted ? line_ptr(c, __shfl_sync(FULL, pl, 1)) : nullptr;
+        u64 r = r0;
+        long long ev = (r + lane <= V) ? __ldcg(row_ptr + r + lane) : LLONG_MAX;
+        u64 carry_row = ~0ull;
+        float carry = 0.f;
+        for (u32 p0 = 0; p0 < kChunk / 32; p0 += 4) {
+          u32 col[4];
+          float val[4], xv[4];
+#pragma unroll
+          for (u32 j = 0; j < 4; ++j) {
+            const u64 e = e0 + (p0 + j) * 32 + lane;
+            col[j] = 0; val[j] = 1.f;
+            if (e < e1) {
+              col[j] = __ldcg(reinterpret_cast<const unsigned int*>(colp) + ((p0 + j) * 32 + lane));
+              if (weighted) val[j] = __ldcg(reinterpret_cast<const float*>(valp) + ((p0 + j) * 32 + lane));
+            }
+          }
+#pragma unroll
+          for (u32 j = 0; j < 4; ++j) {
+            const u64 e = e0 + (p0 + j) * 32 + lane;
+            xv[j] = e < e1 ? __ldg(x + col[j]) : 0.f;
+          }
+#pragma unroll
+          for (u32 j = 0; j < 4; ++j) {
+            const u64 pe0 = e0 + (p0 + j) * 32;
+            if (pe0 >= e1) break;
+            const long long my = (long long)(pe0 + lane);
+            bool unloc = (u64)my < e1 && (u64)my < pe0 + 32;
+            const float v0 = unloc ? val[j] * xv[j] : 0.f;
+            // sub-rounds: the lanes whose edge the 31-row window covers (normally all of them)
+            while (__any_sync(FULL, unloc)) {
+              const long long x0 = __shfl_sync(FULL, my, __ffs(__ballot_sync(FULL, unloc)) - 1);
+              long long wend = __shfl_sync(FULL, ev, 31);
+              if (x0 >= wend) {
+                r = warp_search_le(row_ptr, r + 31, V, x0);
+                ev = (r + lane <= V) ? __ldcg(row_ptr + r + lane) : LLONG_MAX;
+              } else {
+                const u32 s0 = window_slot(ev, x0);
+                if (s0 >= 16) {   // slide so the window starts at the current row
+                  r += s0;
+                  ev = (r + lane <= V) ? __ldcg(row_ptr + r + lane) : LLONG_MAX;
+                }
+              }
+              wend = __shfl_sync(FULL, ev, 31);
+              const bool inw = unloc && my < wend;
+              const u32 k = window_slot(ev, my);
+              const u64 row = inw ? r + k : ~0ull - lane;   // inactive lanes: distinct sentinels
+              const long long rend = __shfl_sync(FULL, ev, k + 1 > 31 ? 31 : k + 1);
+              float v = inw ? v0 : 0.f;
+              const u32 ib = __ballot_sync(FULL, inw);
+              const int fl = __ffs(ib) - 1, ll = 31 - __clz(ib);
+              if ((int)lane == fl && row == carry_row) v += carry;
+              float sum = v;
+#pragma unroll
+              for (u32 d = 1; d < 32; d <<= 1) {   // segmented inclusive scan, fixed order
+                const float t = __shfl_up_sync(FULL, sum, d);
+                const u64 rr = __shfl_up_sync(FULL, row, d);
+                if (lane >= d && rr == row) sum += t;
+              }
+              const u64 rnext = __shfl_down_sync(FULL, row, 1);
+              const bool seg_end = inw && ((int)lane == ll || rnext != row);
+              const long long sub_end = __shfl_sync(FULL, my, ll) + 1;
+              // the last segment continues past this sub-round but inside the chunk: carry it
+              const bool cont = (int)lane == ll && rend > sub_end && (u64)sub_end < e1;
+              carry_row = ~0ull;
+              if (__any_sync(FULL, cont)) {
+                carry_row = __shfl_sync(FULL, row, ll);
+                carry = __shfl_sync(FULL, sum, ll);
+              }
+              if (seg_end && !cont) {
+                const long long rstart = __ldcg(row_ptr + row);
+                if (rstart < (long long)e0) {
+                  part_first[ch] = sum;                     // began in an earlier chunk
+                } else if (rend > (long long)e1) {
+                  part_last[ch] = sum;                      // continues into later chunks
+                  last_row[ch] = (u32)row;
+                } else {
+                  y[row] = alpha * sum + beta;              // wholly inside this chunk
+                }
+              }
+              unloc = unloc && !inw;
+            }
+          }
+        }
+        if (validate_pages_warp(c, pa, pkey, pl, pw)) break;
+        pr.clear();
+        if (!sp.again(c, 256, __LINE__ + 100000 * SPIN_FILE_ID)) return;
+      }
+    }
+    if (lane == 0) {
+      if (edges) atomicAdd(&counters[0], edges);
+      if (misses) atomicAdd(&counters[1], (u64)misses);
+    }
   }
 };
 

@@ -335,22 +335,27 @@ class AgileSystem:
                     "embbag_host")
         return out, cnt
 
-    def bfs_level(self, row_ptr, level, frontier, n_in, nxt, next_count, col_key0, cur, prefetch, counters, stream=None):
+    def bfs(self, row_ptr, V, source, col_key0, level, prefetch_distance=0, stream=None):
+        """Whole BFS over a paged CSR (one fused launch per level); returns the stats dict."""
         import torch
         st = stream if stream is not None else torch.cuda.current_stream(row_ptr.device).cuda_stream
-        self._check(self._lib.agile_bfs_level(self._ctx, row_ptr.data_ptr(), level.data_ptr(), frontier.data_ptr(),
-                                              n_in, nxt.data_ptr(), next_count.data_ptr(), col_key0, cur,
-                                              int(prefetch), counters.data_ptr(), st), "bfs_level")
+        stats = np.zeros(4, dtype=np.uint64)
+        self._check(self._lib.agile_bfs(self._ctx, row_ptr.data_ptr(), V, source, col_key0, level.data_ptr(),
+                                        prefetch_distance, stats.ctypes.data, st), "bfs")
+        return {"levels": int(stats[0]), "edges": int(stats[1]), "page_misses": int(stats[2]),
+                "ms": int(stats[3]) / 1e6}
 
-    def spmv(self, row_ptr, V, col_key0, val_key0, x, y, alpha=1.0, beta=0.0, prefetch=True, counters=None,
-             stream=None):
+    def spmv(self, row_ptr, V, E, col_key0, val_key0, x, y, alpha=1.0, beta=0.0, prefetch_distance=0,
+             counters=None, stream=None):
+        """y = alpha * A x + beta over a paged CSR (async launch)."""
         import torch
         st = stream if stream is not None else torch.cuda.current_stream(row_ptr.device).cuda_stream
         if counters is None:
             counters = torch.zeros(2, dtype=torch.int64, device=row_ptr.device)
         vk = (1 << 64) - 1 if val_key0 is None else val_key0
-        self._check(self._lib.agile_spmv(self._ctx, row_ptr.data_ptr(), V, col_key0, vk, x.data_ptr(), y.data_ptr(),
-                                         float(alpha), float(beta), int(prefetch), counters.data_ptr(), st), "spmv")
+        self._check(self._lib.agile_spmv(self._ctx, row_ptr.data_ptr(), V, E, col_key0, vk, x.data_ptr(),
+                                         y.data_ptr(), float(alpha), float(beta), prefetch_distance,
+                                         counters.data_ptr(), st), "spmv")
         return counters
 
     def embbag_grid(self):

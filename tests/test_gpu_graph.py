@@ -1,11 +1,13 @@
-"""GPU parity of BFS (levels bit-exact) and SpMV / PageRank (1e-5 relative) over a paged CSR."""
+"""GPU parity of BFS (levels bit-exact) and SpMV / PageRank (1e-5 relative) over a paged CSR,
+against the CPU restatement in oracle/graph.py, for sync (prefetch distance 0) and async modes and
+for caches smaller and larger than the paged arrays."""
 
 import numpy as np
 import pytest
 import torch
 
 from oracle.graph import bfs_levels, pagerank, spmv
-from paper_2504_19365_b200.bench.graph import (build_csr, edge_values, pages_for, rmat_edges, run_bfs,
+from paper_2504_19365_b200.bench.graph import (edge_values, pages_for, pick_source, rmat_csr, run_bfs,
                                                run_pagerank, run_spmv, write_paged)
 
 pytestmark = pytest.mark.gpu
@@ -13,31 +15,59 @@ pytestmark = pytest.mark.gpu
 
 def _graph(scale, seed=1, transpose=False):
     dev = torch.device("cuda", 0)
-    src, dst, V = rmat_edges(scale, 16, seed, dev)
-    row_ptr, col = build_csr(dst, src, V) if transpose else build_csr(src, dst, V)
-    return dev, src, dst, V, row_ptr, col
+    row_ptr, col, outdeg = rmat_csr(scale, 16, seed, dev, transpose=transpose, chunk=1 << 16)
+    return dev, row_ptr, col, outdeg
 
 
-@pytest.mark.parametrize("prefetch", [False, True])
+def test_rmat_csr_is_sorted_and_deterministic():
+    dev, rp, col, od = _graph(12, seed=9)
+    _, rp2, col2, _ = _graph(12, seed=9)
+    assert torch.equal(rp, rp2) and torch.equal(col, col2)
+    r, c = rp.cpu().numpy(), col.cpu().numpy()
+    assert r[0] == 0 and r[-1] == len(c) == (1 << 12) * 16
+    for v in range(0, 1 << 12, 97):   # ascending within rows
+        seg = c[r[v]:r[v + 1]]
+        assert np.all(seg[1:] >= seg[:-1])
+    assert int(od.sum()) == len(c)
+
+
+@pytest.mark.parametrize("pd", [0, 2])
 @pytest.mark.parametrize("frac", [0.25, 1.5])
-def test_bfs_levels_match_oracle(gpu_system, prefetch, frac):
-    dev, src, dst, V, row_ptr, col = _graph(13)
+def test_bfs_levels_match_oracle(gpu_system, pd, frac):
+    dev, row_ptr, col, _ = _graph(14)
+    V = row_ptr.numel() - 1
     E = col.numel()
     lines = max(64, int(frac * pages_for(E)) // 32 * 32)
     s = gpu_system(cache_lines=lines, ways=32, blocks=pages_for(E) + 8, pairs=16, engine_warps=16, warps=8)
     write_paged(s, 0, 0, col)
     rp = row_ptr.cpu().numpy()
-    deg = np.diff(rp)
-    source = int(np.nonzero(deg)[0][7])
-    level, st = run_bfs(s, row_ptr, V, source, 0, prefetch)
-    exp = bfs_levels(rp, col.cpu().numpy(), source)
-    assert np.array_equal(level.cpu().numpy(), exp)
-    assert st["edges"] == int(deg[exp >= 0].sum())      # every reached vertex is expanded once
+    for seed in (0, 1):
+        s.reset()
+        source = pick_source(row_ptr, seed)
+        level, st = run_bfs(s, row_ptr, V, source, 0, pd)
+        exp = bfs_levels(rp, col.cpu().numpy(), source)
+        assert np.array_equal(level.cpu().numpy(), exp)
+        deg = np.diff(rp)
+        assert st["edges"] == int(deg[exp >= 0].sum())      # every reached vertex is expanded once
+        assert st["levels"] == int(exp.max()) + 1          # one launch per non-empty frontier
 
 
-@pytest.mark.parametrize("prefetch", [False, True])
-def test_spmv_matches_oracle(gpu_system, prefetch):
-    dev, src, dst, V, row_ptr, col = _graph(12, seed=3)
+def test_bfs_isolated_source(gpu_system):
+    # a source without out-edges: one level, only the source reached
+    rp = torch.tensor([0, 0, 2, 3], dtype=torch.int64, device="cuda")
+    col = torch.tensor([0, 2, 1], dtype=torch.int32, device="cuda")
+    s = gpu_system(cache_lines=64, ways=32, blocks=8, pairs=4, engine_warps=4, warps=2)
+    write_paged(s, 0, 0, col)
+    level, st = run_bfs(s, rp, 3, 0, 0, 0)
+    assert level.cpu().tolist() == [0, -1, -1]
+    level, st = run_bfs(s, rp, 3, 1, 0, 1)
+    assert level.cpu().tolist() == [1, 0, 1]
+
+
+@pytest.mark.parametrize("pd", [0, 2])
+def test_spmv_matches_oracle(gpu_system, pd):
+    dev, row_ptr, col, _ = _graph(13, seed=3)
+    V = row_ptr.numel() - 1
     E = col.numel()
     vals = edge_values(E, 3, dev)
     npg = pages_for(E)
@@ -46,21 +76,44 @@ def test_spmv_matches_oracle(gpu_system, prefetch):
     nxt = write_paged(s, 0, 0, col)
     write_paged(s, 0, nxt, vals)
     x = torch.rand(V, device=dev)
-    y, st = run_spmv(s, row_ptr, V, 0, nxt, x, 1, prefetch)
+    y, st = run_spmv(s, row_ptr, V, E, 0, nxt, x, 1, pd)
     exp = spmv(row_ptr.cpu().numpy(), col.cpu().numpy(), vals.cpu().numpy(), x.cpu().numpy())
     got = y.cpu().numpy().astype(np.float64)
     assert np.max(np.abs(got - exp) / np.maximum(np.abs(exp), 1.0)) < 1e-5
     assert st["edges"] == E
+    # deterministic summation order: a second run is bit-identical
+    y2, _ = run_spmv(s, row_ptr, V, E, 0, nxt, x, 1, pd)
+    assert torch.equal(y, y2)
+
+
+def test_spmv_hub_rows_span_chunks(gpu_system):
+    # rows far longer than a 1024-edge chunk, empty rows between them, a last partial chunk
+    dev = torch.device("cuda", 0)
+    deg = torch.tensor([0, 5000, 0, 0, 3, 2500, 1, 0, 1024, 7], dtype=torch.int64)
+    rp = torch.zeros(len(deg) + 1, dtype=torch.int64)
+    rp[1:] = torch.cumsum(deg, 0)
+    E = int(rp[-1])
+    g = torch.Generator().manual_seed(4)
+    col = torch.randint(0, len(deg), (E,), generator=g, dtype=torch.int32)
+    vals = torch.rand(E, generator=g) * 2 - 1
+    x = torch.rand(len(deg), generator=g)
+    npg = pages_for(E)
+    s = gpu_system(cache_lines=64, ways=32, blocks=2 * npg + 8, pairs=4, engine_warps=4, warps=2)
+    nxt = write_paged(s, 0, 0, col.to(dev))
+    write_paged(s, 0, nxt, vals.to(dev))
+    y, _ = run_spmv(s, rp.to(dev), len(deg), E, 0, nxt, x.to(dev), 1, 1)
+    exp = spmv(rp.numpy(), col.numpy(), vals.numpy(), x.numpy())
+    assert np.max(np.abs(y.cpu().numpy() - exp) / np.maximum(np.abs(exp), 1.0)) < 1e-5
 
 
 def test_pagerank_matches_oracle(gpu_system):
-    dev, src, dst, V, rowT, colT = _graph(12, seed=5, transpose=True)
-    outdeg = torch.bincount(src, minlength=V)
+    dev, rowT, colT, outdeg = _graph(12, seed=5, transpose=True)
+    V = rowT.numel() - 1
     E = colT.numel()
     s = gpu_system(cache_lines=max(64, (pages_for(E) // 4) // 32 * 32), ways=32, blocks=pages_for(E) + 8,
                    pairs=16, engine_warps=16, warps=8)
     write_paged(s, 0, 0, colT)
-    r, st = run_pagerank(s, rowT, V, 0, outdeg, 10)
+    r, st = run_pagerank(s, rowT, V, E, 0, outdeg, 10, prefetch_distance=2)
     exp = pagerank(rowT.cpu().numpy(), colT.cpu().numpy(), outdeg.cpu().numpy(), 10)
     got = r.cpu().numpy().astype(np.float64)
     assert np.max(np.abs(got - exp) / np.maximum(np.abs(exp), 1e-12)) < 1e-4
