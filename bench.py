@@ -51,6 +51,8 @@ def _args():
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--engine-warps", type=int, default=128)
     p.add_argument("--service-warps", type=int, default=48)
+    p.add_argument("--side-ctas", type=int, default=64,
+                   help="user CTAs of the side-stream gather in the async DLRM pipeline")
     p.add_argument("--warm-batches", type=int, default=-1,
                    help="untimed cache warm-up batches at setup (-1: enough to fill the cache)")
     return p.parse_args()
@@ -365,29 +367,35 @@ def main():
             f9 = mlp_graph_ms(model.capture(dense, out, 9))
             per_rep = max((f9 - f1) / 8, 1e-3)          # top-MLP cost per pass
             gather_ms = ms / args.steps
+            out_b = torch.empty_like(out)
             pipe_rows = []
             for ctc in (0.0, 0.5, 0.75, 1.0, 1.5, 2.0):
                 rep = max(1, int(round((ctc * gather_ms - f1) / per_rep)) + 1) if ctc > 0 else 1
-                mlp = model.capture(dense, out, rep)
-                mlp_ms = mlp_graph_ms(mlp, 3)
+                mlps = [model.capture(dense, o, rep) for o in (out, out_b)]
+                mlp_ms = mlp_graph_ms(mlps[0], 3)
                 res = {}
-                for mode in ("sync", "async"):
+                for mode in ("sync", "async", "prefetch"):
                     bat = [gpu_zipf_batch(gen, shard.rows, B, L, ALPHA, scatter, dev) for _ in range(args.steps)]
-                    res[mode] = run_pipeline(system, bat, key0, rows, mlp, out, mode, prefetch_distance=args.prefetch)
+                    res[mode] = run_pipeline(system, bat, key0, rows, mlps, (out, out_b), mode,
+                                             side_ctas=args.side_ctas, prefetch_distance=args.prefetch)
                 t_s = res["sync"]["ms"] / args.steps
                 pipe_rows.append({"target_ctc": ctc, "mlp_repeat": rep, "mlp_ms": mlp_ms,
                                   "ctc": mlp_ms / max(1e-9, t_s - mlp_ms),
                                   "sync_ms_per_step": t_s,
                                   "async_ms_per_step": res["async"]["ms"] / args.steps,
+                                  "prefetch_ms_per_step": res["prefetch"]["ms"] / args.steps,
                                   "speedup": res["sync"]["ms"] / res["async"]["ms"],
+                                  "speedup_prefetch": res["sync"]["ms"] / res["prefetch"]["ms"],
                                   "ideal": 1.0 + min(mlp_ms, t_s - mlp_ms) / max(mlp_ms, t_s - mlp_ms)})
-                del mlp
+                del mlps
             line["dlrm_pipeline"] = {"what": ("full DLRM forward per batch (bottom MLP 13-512-256-128, pairwise dot "
                                               "interaction, top MLP 479-1024-1024-512-256-1 repeated to set the "
                                               "compute/communication ratio; bf16 torch, captured as one CUDA graph); "
-                                              "sync = gather then MLPs, async = batch i+1 prefetched on a side "
-                                              "stream (24 user CTAs) beside the MLPs of batch i; ctc = MLP time / "
-                                              "sync gather time; ideal = Eq. 1 (bench/__init__.py:35-41)"),
+                                              "sync = gather then MLPs on one stream; async = gather of batch i+1 "
+                                              f"({args.side_ctas} user CTAs, high-priority side stream, double-buffered "
+                                              "pooled output) beside the MLPs of batch i; prefetch = AGILE batch "
+                                              "prefetch of i+1 beside MLPs(i), then a full-grid gather; ctc = MLP time "
+                                              "/ sync gather time; ideal = Eq. 1 (bench/__init__.py:35-41)"),
                                      "mlp_ms_forward": f1, "mlp_ms_per_top_repeat": per_rep,
                                      "gather_ms": gather_ms, "points": pipe_rows}
             mid = [r for r in pipe_rows if r["target_ctc"] == 1.0][0]
@@ -396,6 +404,9 @@ def main():
         hb = nb + n_sync - 1
         h0 = torch.cuda.Event(enable_timing=True)
         h1 = torch.cuda.Event(enable_timing=True)
+        # one untimed pass makes every page of the batch resident (it was last touched two
+        # phases ago and may have lost pages since); the timed passes are then pure hits
+        system.embbag(dbat[hb], key0, rows, out, cnt, prefetch_distance=0, stream=stream.cuda_stream)
         cnt.zero_()
         h0.record(stream)
         reps = 5

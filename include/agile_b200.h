@@ -107,6 +107,12 @@ int agile_run_gather(agile_ctx* ctx, const uint64_t* keys, uint32_t tasks, uint3
 int agile_embbag(agile_ctx* ctx, const int64_t* idx, const uint64_t* table_key0, const int64_t* table_rows,
                  float* out, uint64_t* counters, uint32_t B, uint32_t T, uint32_t L, uint32_t D,
                  uint32_t out_b_stride, uint32_t out_t_stride, uint32_t prefetch_distance, void* stream);
+/* Same, with the launch bounded to user_ctas user CTAs (0 = every resident slot): a gather issued
+ * on a side stream beside compute (the DLRM MLPs) leaves the remaining SMs to that compute. */
+int agile_embbag_ctas(agile_ctx* ctx, const int64_t* idx, const uint64_t* table_key0, const int64_t* table_rows,
+                      float* out, uint64_t* counters, uint32_t B, uint32_t T, uint32_t L, uint32_t D,
+                      uint32_t out_b_stride, uint32_t out_t_stride, uint32_t prefetch_distance, uint32_t user_ctas,
+                      void* stream);
 /* Same, host buffers (end-to-end through the C-ABI: H2D of indices, kernel, D2H of pooled out). */
 int agile_embbag_host(agile_ctx* ctx, const int64_t* idx, const uint64_t* table_key0, const int64_t* table_rows,
                       float* out, uint64_t* counters, uint32_t B, uint32_t T, uint32_t L, uint32_t D,

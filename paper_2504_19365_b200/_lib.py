@@ -12,7 +12,7 @@ import os
 
 from .errors import CODE_TO_EXC, NativeUnavailable
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libagile_b200.so")
+LIB_PATH = os.environ.get("AGILE_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libagile_b200.so")
 
 _u32, _u64, _i64, _int, _vp, _cp = C.c_uint32, C.c_uint64, C.c_int64, C.c_int, C.c_void_p, C.c_char_p
 _pu32, _pu64, _pi64, _pi8, _pf = (C.POINTER(C.c_uint32), C.POINTER(C.c_uint64), C.POINTER(C.c_int64),
@@ -39,6 +39,7 @@ SIGNATURES = {
     "agile_run_loop": (_int, [_vp, _u32, _u64, _u64, _u64, _vp, _vp, _vp]),
     "agile_run_gather": (_int, [_vp, _vp, _u32, _u32, _u32, _int, _u64, _vp, _vp, _vp]),
     "agile_embbag": (_int, [_vp, _vp, _vp, _vp, _vp, _vp, _u32, _u32, _u32, _u32, _u32, _u32, _u32, _vp]),
+    "agile_embbag_ctas": (_int, [_vp, _vp, _vp, _vp, _vp, _vp, _u32, _u32, _u32, _u32, _u32, _u32, _u32, _u32, _vp]),
     "agile_embbag_host": (_int, [_vp, _vp, _vp, _vp, _vp, _vp, _u32, _u32, _u32, _u32, _u32]),
     "agile_embbag_grid": (_int, [_vp, C.POINTER(_u32), C.POINTER(_u32)]),
     "agile_bfs": (_int, [_vp, _vp, _u32, _u32, _u64, _vp, _u32, _vp, _vp]),

@@ -187,20 +187,25 @@ def mlp_graph_ms(graph, reps: int = 10) -> float:
     return a.elapsed_time(b) / reps
 
 
-def run_pipeline(system, batches, key0, rows, mlp, out, mode: str, prefetch_ctas: int = 24,
+def run_pipeline(system, batches, key0, rows, mlps, outs, mode: str, side_ctas: int = 64,
                  prefetch_distance: int = 0):
-    """Time len(batches) DLRM steps; `mlp` is a captured forward graph reading `out` (the pooled
-    [B, T, D] buffer the gathers write).  sync: gather(i) then MLPs(i) (bench/ctc.py:27-44
-    shape: compute starts once the data arrived).  async: batch i+1 is prefetched on a side stream
-    by a launch bounded to `prefetch_ctas` user CTAs while MLPs(i) run; gather(i+1) then finds its
-    pages resident (bench/ctc.py:47-70 shape).  Two AGILE launches never overlap (events order
-    them); gather(i+1) overwrites `out` only after MLPs(i) consumed it (same stream)."""
+    """Time len(batches) DLRM steps.  `mlps[k]` is a captured forward graph reading the pooled
+    buffer `outs[k]` ([B, T, D], k = 0, 1: double buffering).
+      sync:     gather(i) -> MLPs(i) on one stream (bench/ctc.py:27-44: compute starts once the
+                epoch's data arrived), always buffer 0.
+      async:    gather(i+1) runs on a high-priority side stream, bounded to `side_ctas` user CTAs,
+                into the other buffer while MLPs(i) run on the main stream (bench/ctc.py:47-70: the
+                next epoch's reads are issued before this epoch's compute); a step costs
+                max(gather, MLPs) instead of their sum.
+      prefetch: batch-level AGILE prefetch (gpu_api.py:139-162) of batch i+1 beside MLPs(i), then
+                a full-grid gather(i+1) that finds its pages resident.
+    Two AGILE launches never overlap (one context: same stream, or ordered by events)."""
     import torch
     dev = batches[0].device
     B, T, L = batches[0].shape
-    D = out.shape[-1]
+    D = outs[0].shape[-1]
     main = torch.cuda.current_stream(dev)
-    side = torch.cuda.Stream(dev)
+    side = torch.cuda.Stream(dev, priority=-1)   # lower = higher: its CTAs dispatch ahead of the MLPs'
     cnt = torch.zeros(2, dtype=torch.int64, device=dev)
     pcnt = torch.zeros(2, dtype=torch.int64, device=dev)
     n = len(batches)
@@ -210,23 +215,44 @@ def run_pipeline(system, batches, key0, rows, mlp, out, mode: str, prefetch_ctas
     t0.record(main)
     if mode == "sync":
         for i in range(n):
-            system.embbag(batches[i], key0, rows, out, cnt, prefetch_distance=prefetch_distance, stream=main.cuda_stream)
-            mlp.replay()
-    else:
+            system.embbag(batches[i], key0, rows, outs[0], cnt, prefetch_distance=prefetch_distance,
+                          stream=main.cuda_stream)
+            mlps[0].replay()
+    elif mode == "async":
+        ev_g = [torch.cuda.Event() for _ in range(n)]
+        ev_m = [torch.cuda.Event() for _ in range(n)]
+        side.wait_event(t0)
+        system.embbag(batches[0], key0, rows, outs[0], cnt, prefetch_distance=prefetch_distance,
+                      stream=side.cuda_stream, user_ctas=side_ctas)
+        ev_g[0].record(side)
+        for i in range(n):
+            if i + 1 < n:
+                # buffer (i+1)%2 was last read by MLPs(i-1)
+                if i >= 1:
+                    side.wait_event(ev_m[i - 1])
+                system.embbag(batches[i + 1], key0, rows, outs[(i + 1) % 2], cnt, prefetch_distance=prefetch_distance,
+                              stream=side.cuda_stream, user_ctas=side_ctas)
+                ev_g[i + 1].record(side)
+            main.wait_event(ev_g[i])
+            mlps[i % 2].replay()
+            ev_m[i].record(main)
+    elif mode == "prefetch":
         ev_p = [torch.cuda.Event() for _ in range(n)]
         ev_e = [torch.cuda.Event() for _ in range(n)]
         side.wait_event(t0)
-        system.embbag_prefetch(batches[0], key0, rows, D, pcnt, prefetch_ctas, stream=side.cuda_stream)
+        system.embbag_prefetch(batches[0], key0, rows, D, pcnt, side_ctas, stream=side.cuda_stream)
         ev_p[0].record(side)
         for i in range(n):
             main.wait_event(ev_p[i])
-            system.embbag(batches[i], key0, rows, out, cnt, prefetch_distance=0, stream=main.cuda_stream)
+            system.embbag(batches[i], key0, rows, outs[0], cnt, prefetch_distance=0, stream=main.cuda_stream)
             ev_e[i].record(main)
             if i + 1 < n:
                 side.wait_event(ev_e[i])
-                system.embbag_prefetch(batches[i + 1], key0, rows, D, pcnt, prefetch_ctas, stream=side.cuda_stream)
+                system.embbag_prefetch(batches[i + 1], key0, rows, D, pcnt, side_ctas, stream=side.cuda_stream)
                 ev_p[i + 1].record(side)
-            mlp.replay()
+            mlps[0].replay()
+    else:
+        raise ValueError(f"unknown pipeline mode {mode!r}")
     t1.record(main)
     torch.cuda.synchronize()
     system.sync(main.cuda_stream)
@@ -254,15 +280,16 @@ def run_dlrm(cfg, trace: bool = False):
         system.fill_store(0, sc.seed, kind="f32")
         model = DlrmModel(dev, cfg.dlrm_dim, cfg.dlrm_tables)
         dense = torch.randn(cfg.dlrm_batch, 13, device=dev, dtype=torch.bfloat16)
-        out = torch.zeros((cfg.dlrm_batch, cfg.dlrm_tables, cfg.dlrm_dim), dtype=torch.float32, device=dev)
-        mlp = model.capture(dense, out, 1)
+        outs = [torch.zeros((cfg.dlrm_batch, cfg.dlrm_tables, cfg.dlrm_dim), dtype=torch.float32, device=dev)
+                for _ in range(2)]
+        mlps = [model.capture(dense, o, 1) for o in outs]
         k0 = torch.from_numpy(key0.view(np.int64)).to(dev)
         r = torch.from_numpy(rows).to(dev)
         nb = cfg.dlrm_batches
         for mode, base in (("sync", 0), ("async", nb)):
             bat = [torch.from_numpy(make_batch(sc.seed, base + i, rows, cfg.dlrm_batch, cfg.dlrm_pooling,
                                                cfg.dlrm_zipf, cfg.dlrm_scatter)).to(dev) for i in range(nb)]
-            res = run_pipeline(system, bat, k0, r, mlp, out, mode)
+            res = run_pipeline(system, bat, k0, r, mlps, outs, mode)
             result.rows.append((mode, nb, int(res["ms"] * 1e6), round(res["lookups_per_s"], 3), res["miss_lookups"]))
     return result
 

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <cub/cub.cuh>
 #include <algorithm>
+#include <type_traits>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -145,25 +146,81 @@ WaitNode* get_nodes(agile_ctx* ctx, size_t n) {
   return reinterpret_cast<WaitNode*>(ctx->nodes);
 }
 
+// dynamic shared memory of a workload's launch (W::kDynSmem when it declares one: the embedding-
+// bag row stages); set once per instantiation above the 48 KiB default
+template <class W, class = void>
+struct DynSmem { static constexpr size_t bytes = 0; };
+template <class W>
+struct DynSmem<W, std::void_t<decltype(W::kDynSmem)>> { static constexpr size_t bytes = W::kDynSmem; };
+
+template <class W>
+size_t dyn_smem() {
+  constexpr size_t b = DynSmem<W>::bytes;
+  if (b > 48 * 1024) {
+    static bool set = false;
+    if (!set) {
+      cudaFuncSetAttribute(agile_user_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b);
+      set = true;
+    }
+  }
+  return b;
+}
+
+// Lazy module loading would load the user kernel at its first launch, i.e. while the infra grid
+// it must run beside is already spinning — loading can wait for the device to drain, and the two
+// grids would deadlock.  Touching both functions first loads them before any run starts.
+template <class W>
+void load_kernels() {
+  static bool loaded = false;
+  if (loaded) return;
+  cudaFuncAttributes a{};
+  cudaFuncGetAttributes(&a, agile_infra_kernel);
+  cudaFuncGetAttributes(&a, agile_user_kernel<W>);
+  loaded = true;
+}
+
 template <class W>
 int launch(agile_ctx* ctx, const W& work, uint32_t n_user_ctas, cudaStream_t st) {
   if (n_user_ctas == 0) n_user_ctas = 1;
+  load_kernels<W>();
+  dyn_smem<W>();
   CK(cudaMemsetAsync(ctx->d.run, 0, sizeof(RunWords), st));
   Launch L;
   L.n_user_ctas = n_user_ctas;
   L.pad = 0;
-  const uint32_t grid = ctx->d.n_engine_ctas + ctx->d.n_service_ctas + n_user_ctas;
-  agile_kernel<W><<<grid, kCtaThreads, 0, st>>>(ctx->d, L, work);
+  const uint32_t ninfra = ctx->d.n_engine_ctas + ctx->d.n_service_ctas;
+  agile_infra_kernel<<<ninfra, kCtaThreads, 0, st>>>(ctx->d, L);
   CK(cudaGetLastError());
+  // the user grid may start once every infra CTA executed griddepcontrol.launch_dependents
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(n_user_ctas);
+  cfg.blockDim = dim3(kCtaThreads);
+  cfg.dynamicSmemBytes = dyn_smem<W>();
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, agile_user_kernel<W>, ctx->d, L, work));
   return 0;
 }
 
+// user CTAs of workload W that are co-resident with the infra grid: the user grid's occupancy
+// over all SMs minus the user CTAs each infra CTA displaces on its SM (registers bound both)
 template <class W>
 uint32_t resident_ctas(agile_ctx* ctx) {
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, agile_kernel<W>, kCtaThreads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, agile_user_kernel<W>, kCtaThreads, dyn_smem<W>());
   if (per_sm < 1) per_sm = 1;
-  return (uint32_t)per_sm * (uint32_t)ctx->sms;
+  cudaFuncAttributes ua{}, ia{};
+  cudaFuncGetAttributes(&ua, agile_user_kernel<W>);
+  cudaFuncGetAttributes(&ia, agile_infra_kernel);
+  const uint32_t ur = (uint32_t)std::max(1, ua.numRegs), ir = (uint32_t)std::max(1, ia.numRegs);
+  const uint32_t displaced = (ir + ur - 1) / ur;
+  const uint32_t total = (uint32_t)per_sm * (uint32_t)ctx->sms;
+  const uint32_t taken = (ctx->d.n_engine_ctas + ctx->d.n_service_ctas) * displaced;
+  return total > taken + 1 ? total - taken : 1;
 }
 
 __global__ void fill_store_kernel(uint8_t* base, uint64_t seed, uint32_t dev, uint64_t first, uint64_t nblk, int kind) {
@@ -546,7 +603,7 @@ int agile_run_reads(agile_ctx* ctx, const uint64_t* keys, uint32_t tasks, uint32
   if (!w.nodes) return fail(ctx, AGILE_E_CUDA, "node allocation failed");
   const uint32_t users = (tasks + kCtaThreads - 1) / kCtaThreads;
   const uint32_t cap = resident_ctas<ReadsWork>(ctx);
-  if (users + ctx->d.n_engine_ctas + ctx->d.n_service_ctas > cap)
+  if (users > cap)
     return fail(ctx, AGILE_E_ARG, "tasks exceed co-resident capacity for the epoch barrier");
   return launch(ctx, w, users, reinterpret_cast<cudaStream_t>(stream));
 }
@@ -584,16 +641,12 @@ int agile_run_gather(agile_ctx* ctx, const uint64_t* keys, uint32_t tasks, uint3
   w.compute_ns = compute_ns;
   const uint32_t users = (tasks + kCtaThreads - 1) / kCtaThreads;
   const uint32_t cap = resident_ctas<GatherWork>(ctx);
-  if (users + ctx->d.n_engine_ctas + ctx->d.n_service_ctas > cap)
+  if (users > cap)
     return fail(ctx, AGILE_E_ARG, "tasks exceed co-resident capacity for the epoch barrier");
   return launch(ctx, w, users, reinterpret_cast<cudaStream_t>(stream));
 }
 
-static uint32_t embbag_users(agile_ctx* ctx) {
-  const uint32_t cap = resident_ctas<EmbBagWork>(ctx);
-  const uint32_t infra = ctx->d.n_engine_ctas + ctx->d.n_service_ctas;
-  return cap > infra + 1 ? cap - infra : 1;
-}
+static uint32_t embbag_users(agile_ctx* ctx) { return resident_ctas<EmbBagWork>(ctx); }
 
 int agile_embbag_grid(agile_ctx* ctx, uint32_t* user_ctas, uint32_t* infra_ctas) {
   if (!ctx) return AGILE_E_ARG;
@@ -605,6 +658,14 @@ int agile_embbag_grid(agile_ctx* ctx, uint32_t* user_ctas, uint32_t* infra_ctas)
 int agile_embbag(agile_ctx* ctx, const int64_t* idx, const uint64_t* table_key0, const int64_t* table_rows,
                  float* out, uint64_t* counters, uint32_t B, uint32_t T, uint32_t L, uint32_t D,
                  uint32_t out_b_stride, uint32_t out_t_stride, uint32_t prefetch_distance, void* stream) {
+  return agile_embbag_ctas(ctx, idx, table_key0, table_rows, out, counters, B, T, L, D, out_b_stride, out_t_stride,
+                           prefetch_distance, 0, stream);
+}
+
+int agile_embbag_ctas(agile_ctx* ctx, const int64_t* idx, const uint64_t* table_key0, const int64_t* table_rows,
+                      float* out, uint64_t* counters, uint32_t B, uint32_t T, uint32_t L, uint32_t D,
+                      uint32_t out_b_stride, uint32_t out_t_stride, uint32_t prefetch_distance, uint32_t user_ctas,
+                      void* stream) {
   if (!ctx || !idx || !table_key0 || !table_rows || !out || !counters) return fail(ctx, AGILE_E_ARG, "null embbag arg");
   if (L == 0 || L > 32) return fail(ctx, AGILE_E_ARG, "pooling factor L must be in [1, 32]");
   if (D == 0 || D > 128 || D % 4 || (1024u % D) != 0) return fail(ctx, AGILE_E_ARG, "D must divide 1024, be a multiple of 4 and <= 128");
@@ -623,7 +684,8 @@ int agile_embbag(agile_ctx* ctx, const int64_t* idx, const uint64_t* table_key0,
   w.rows_per_page_shift = sh;
   w.out_b_stride = out_b_stride ? out_b_stride : T * D;
   w.out_t_stride = out_t_stride ? out_t_stride : D;
-  const uint32_t users = embbag_users(ctx);
+  const uint32_t full = embbag_users(ctx);
+  const uint32_t users = user_ctas ? std::min(user_ctas, full) : full;
   w.nwarps_total = users * kCtaWarps;
   w.prefetch_only = 0;
   return launch(ctx, w, users, reinterpret_cast<cudaStream_t>(stream));
@@ -764,8 +826,7 @@ int agile_bfs(agile_ctx* ctx, const int64_t* row_ptr, uint32_t V, uint32_t sourc
   CK(cudaMemcpyAsync(visited + source / 32, &sbit, 4, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(fa, &source, 4, cudaMemcpyHostToDevice, st));
   const uint32_t cap = resident_ctas<BfsWork>(ctx);
-  const uint32_t infra = ctx->d.n_engine_ctas + ctx->d.n_service_ctas;
-  const uint32_t full = cap > infra + 1 ? cap - infra : 1;
+  const uint32_t full = cap;
   uint32_t n = 1, levels = 0;
   int cur = 0;
   while (n) {
@@ -848,8 +909,7 @@ int agile_spmv(agile_ctx* ctx, const int64_t* row_ptr, uint32_t V, uint64_t E, u
   w.pd = prefetch_distance;
   w.counters = reinterpret_cast<u64*>(counters);
   const uint32_t cap = resident_ctas<SpmvWork>(ctx);
-  const uint32_t infra = ctx->d.n_engine_ctas + ctx->d.n_service_ctas;
-  const uint32_t full = cap > infra + 1 ? cap - infra : 1;
+  const uint32_t full = cap;
   const uint32_t users = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(full, (nch + kCtaWarps - 1) / kCtaWarps));
   int rc = launch(ctx, w, users, st);
   if (rc) return rc;

@@ -2,9 +2,15 @@
 // All user-facing functions are warp-collective: every lane of the warp calls them, each lane
 // carrying its own request (or none); the warp coalesces, probes and submits cooperatively.
 #pragma once
+#include <type_traits>
 #include "agile_dev.cuh"
 #undef SPIN_FILE_ID
 #define SPIN_FILE_ID 1
+
+// CTAs per SM the fused kernel's register budget targets (__launch_bounds__ min blocks)
+#ifndef AGILE_MIN_CTAS
+#define AGILE_MIN_CTAS 2
+#endif
 
 namespace agile {
 
@@ -74,6 +80,9 @@ __device__ __forceinline__ u32 sig_match8(uint4 v, u32 pat) {
   return m;
 }
 
+// kAcquire = false: the confirming tag load is relaxed; the caller issues a fence before it reads
+// the line's bytes (one fence then covers every key of the warp).
+template <bool kAcquire = true>
 __device__ __forceinline__ void probe_lanes(const DevCtx& c, bool active, u64 key, u32& line, u64& word) {
   line = NONE;
   word = 0;
@@ -99,7 +108,7 @@ __device__ __forceinline__ void probe_lanes(const DevCtx& c, bool active, u64 ke
       while (m) {
         const u32 wy = __ffs(m) - 1;
         m &= m - 1;
-        const u64 t = ld_acquire(&c.tags[base + wy]);
+        const u64 t = kAcquire ? ld_acquire(&c.tags[base + wy]) : ld_relaxed(&c.tags[base + wy]);
         if (tw_live(t) && tw_key(t) == key) { line = (u32)(base + wy); word = t; break; }
       }
     }
@@ -1013,6 +1022,7 @@ __device__ void service_main(const DevCtx& c, const Launch& L, u32 sw) {
   const u32 nown = n > sw ? (n - sw + S - 1) / S : 0;
   if (sw == 0 && lane == 0) log_ev(c, who, M_SVC, A_START, S);
   if (nown > 32 * kMaxCqPerLane) set_error(c, E_PROTOCOL, nown, 0);
+  const u64 t_enter = gtimer();
   u64 off[kMaxCqPerLane];
   u32 msk[kMaxCqPerLane];
 #pragma unroll
@@ -1063,6 +1073,12 @@ __device__ void service_main(const DevCtx& c, const Launch& L, u32 sw) {
       const bool users = ld_acquire(&c.run->users_done) >= L.n_user_ctas;
       const u64 out = ld_acquire(&c.pw->outstanding);
       stop = (users && out == 0) || aborted(c);
+      // the user grid never started (its launch was not allowed to overlap this grid): report
+      // instead of waiting forever
+      if (!stop && ld_relaxed(&c.run->users_started) == 0 && gtimer() - t_enter > c.watchdog_ns) {
+        set_error(c, E_LIVELOCK, 0, __LINE__ + 100000 * SPIN_FILE_ID);
+        stop = 1;
+      }
       if (users && atomicCAS(&c.run->stop_logged, 0u, 1u) == 0u) log_ev(c, who, M_SVC, A_STOP);
     }
     if (__shfl_sync(FULL, stop, 0)) break;
@@ -1240,6 +1256,13 @@ __device__ void model_schedule_rr(const DevCtx& c, bool want, u32 dev, u32 op, u
   }
 }
 
+// pages one engine warp moves per pass (in registers: 32 per page per lane); the register budget
+// of the fused kernel (AGILE_MIN_CTAS) decides what fits without spilling
+#ifndef AGILE_ENGINE_PAGES
+#define AGILE_ENGINE_PAGES (AGILE_MIN_CTAS > 2 ? 1 : 2)
+#endif
+constexpr int kEnginePages = AGILE_ENGINE_PAGES;
+
 __device__ void engine_main(const DevCtx& c, u32 ew) {
   const u32 lane = lane_id();
   const u32 E = c.engine_warps;
@@ -1264,7 +1287,7 @@ __device__ void engine_main(const DevCtx& c, u32 ew) {
     if (tocopy) {
       did = true;
       l0 = oldest_lane(pv && !pcp, pseq);   // oldest first: no lane starves behind new fetches
-      l1 = oldest_lane(pv && !pcp && (int)lane != l0, pseq);
+      l1 = kEnginePages > 1 ? oldest_lane(pv && !pcp && (int)lane != l0, pseq) : -1;
       const int s1l = l1 < 0 ? l0 : l1;
       const u32 op0 = __shfl_sync(FULL, pop, l0), op1 = __shfl_sync(FULL, pop, s1l);
       const u32 d0 = __shfl_sync(FULL, pdev, l0), d1 = __shfl_sync(FULL, pdev, s1l);
@@ -1463,57 +1486,62 @@ __device__ void engine_main(const DevCtx& c, u32 ew) {
 }
 
 // ======================================================================= launch skeleton
-// Role by arrival ticket: the first CTAs to actually start become the device engine and the
-// completion service, so every spinning user CTA waits only on CTAs that are already resident
-// (forward progress by construction; PAPER.md:811-819 draft: the service is the first block).
-struct Role {
-  int kind;   // 0 engine, 1 service, 2 user
-  u32 idx;
-};
-
-__device__ __forceinline__ Role take_role(const DevCtx& c) {
-  __shared__ u32 s_ticket;
-  if (threadIdx.x == 0) s_ticket = atomicAdd(&c.run->ticket, 1u);
-  __syncthreads();
-  u32 t = s_ticket;
-  Role r;
-  if (t < c.n_engine_ctas) { r.kind = 0; r.idx = t; return r; }
-  t -= c.n_engine_ctas;
-  if (t < c.n_service_ctas) { r.kind = 1; r.idx = t; return r; }
-  r.kind = 2;
-  r.idx = t - c.n_service_ctas;
-  return r;
-}
+// One AGILE run = two grids on one stream:
+//   infra grid  [engine CTAs][service CTAs]  — register-rich (no spills in the engine/service),
+//   user grid   the workload's CTAs           — its own register budget (UserMinCtas<Work>).
+// The user grid is launched with programmatic stream serialization (PDL) and every infra CTA
+// executes griddepcontrol.launch_dependents as its first instruction, so no user CTA starts
+// before every engine and service CTA is resident: a spinning user waits only on CTAs that are
+// already running (forward progress by construction; PAPER.md:811-819 puts the service in the
+// first scheduled block for the same reason).  The user grid never calls griddepcontrol.wait.
+// The last user CTA out waits for the infra CTAs to exit, so the next run on the stream (which
+// resets the run words) cannot overlap this run's infra grid.
 
 __device__ __forceinline__ void user_done(const DevCtx& c) {
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
-    atomicAdd(&c.run->users_done, 1u);
+    const u32 n = atomicAdd(&c.run->users_done, 1u) + 1;
+    if (n == gridDim.x) {
+      const u32 ninfra = c.n_engine_ctas + c.n_service_ctas;
+      Spin sp;
+      while (ld_acquire(&c.run->infra_exited) < ninfra)
+        if (!sp.again(c, 1024, __LINE__ + 100000 * SPIN_FILE_ID)) break;
+    }
   }
 }
 
-#ifndef AGILE_MIN_CTAS
-#define AGILE_MIN_CTAS 2
-#endif
+__global__ void __launch_bounds__(kCtaThreads, 1) agile_infra_kernel(const __grid_constant__ DevCtx c, const Launch L) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const u32 warp = threadIdx.x >> 5;
+  if (blockIdx.x < c.n_engine_ctas) {
+    const u32 ew = blockIdx.x * kCtaWarps + warp;
+    if (ew < c.engine_warps) engine_main(c, ew);
+  } else {
+    const u32 sw = (blockIdx.x - c.n_engine_ctas) * kCtaWarps + warp;
+    if (sw < c.service_warps) service_main(c, L, sw);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(&c.run->infra_exited, 1u);
+  }
+}
+
+// CTAs per SM a workload's user grid targets (its register budget): AGILE_MIN_CTAS unless the
+// workload declares kMinCtas
+template <class W, class = void>
+struct UserMinCtas { static constexpr int v = AGILE_MIN_CTAS; };
+template <class W>
+struct UserMinCtas<W, std::void_t<decltype(W::kMinCtas)>> { static constexpr int v = W::kMinCtas; };
+
 template <class Work>
 // __grid_constant__: the device functions take the context and the workload by reference; without
 // it every thread would copy both structs from the parameter bank into local memory at entry.
-__global__ void __launch_bounds__(kCtaThreads, AGILE_MIN_CTAS)
-    agile_kernel(const __grid_constant__ DevCtx c, const Launch L, const __grid_constant__ Work work) {
-  const Role r = take_role(c);
-  const u32 warp = threadIdx.x >> 5;
-  if (r.kind == 0) {
-    const u32 ew = r.idx * kCtaWarps + warp;
-    if (ew < c.engine_warps) engine_main(c, ew);
-    return;
-  }
-  if (r.kind == 1) {
-    const u32 sw = r.idx * kCtaWarps + warp;
-    if (sw < c.service_warps) service_main(c, L, sw);
-    return;
-  }
-  work.run(c, r.idx, L.n_user_ctas);
+__global__ void __launch_bounds__(kCtaThreads, UserMinCtas<Work>::v)
+    agile_user_kernel(const __grid_constant__ DevCtx c, const Launch L, const __grid_constant__ Work work) {
+  if (threadIdx.x == 0) atomicAdd(&c.run->users_started, 1u);
+  work.run(c, blockIdx.x, L.n_user_ctas);
   user_done(c);
 }
 

@@ -135,8 +135,9 @@ struct CmdCtx {      // side table indexed by (sq, slot) == CommandContext (nvme
 };
 
 struct alignas(64) RunWords {   // reset before every launch
-  u32 ticket;
+  u32 users_started;
   u32 users_done;
+  u32 infra_exited;
   u32 svc_exited;
   u32 engine_stop;
   u32 abort;

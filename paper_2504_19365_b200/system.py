@@ -301,15 +301,17 @@ class AgileSystem:
         return {"t_ns": int(e[1] - e[0]), "values": vals.cpu().numpy().view(np.uint32)}
 
     def embbag(self, idx, table_key0, table_rows, out, counters, prefetch_distance=1, stream=None,
-               out_b_stride=0, out_t_stride=0):
-        """Device-tensor embedding-bag (sum pooling) through the page cache; async launch."""
+               out_b_stride=0, out_t_stride=0, user_ctas=0):
+        """Device-tensor embedding-bag (sum pooling) through the page cache; async launch.
+        user_ctas bounds the user CTAs of the launch (0 = every resident slot)."""
         import torch
         B, T, L = idx.shape
         D = out.shape[-1]
         st = stream if stream is not None else torch.cuda.current_stream(idx.device).cuda_stream
-        self._check(self._lib.agile_embbag(self._ctx, idx.data_ptr(), table_key0.data_ptr(), table_rows.data_ptr(),
-                                           out.data_ptr(), counters.data_ptr(), B, T, L, D, out_b_stride,
-                                           out_t_stride, prefetch_distance, st), "embbag")
+        self._check(self._lib.agile_embbag_ctas(self._ctx, idx.data_ptr(), table_key0.data_ptr(),
+                                                table_rows.data_ptr(), out.data_ptr(), counters.data_ptr(), B, T, L,
+                                                D, out_b_stride, out_t_stride, prefetch_distance, user_ctas, st),
+                    "embbag")
 
     def embbag_prefetch(self, idx, table_key0, table_rows, D, counters, user_ctas=0, stream=None):
         """Pull every page of the batch into the cache (async launch on `stream`)."""

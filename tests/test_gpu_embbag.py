@@ -73,3 +73,27 @@ def test_embbag_host_entry_matches_device_entry(gpu_system):
     ref = embbag_reference(4, 0, k0, idx, 128)
     assert np.max(np.abs(out - ref) / np.maximum(np.abs(ref), 1)) < 1e-5
     assert int(cnt[0]) == 16 * 2 * 20
+
+
+@pytest.mark.parametrize("user_ctas,pd", [(1, 0), (2, 3), (5, 0)])
+def test_embbag_bounded_grid(gpu_system, user_ctas, pd):
+    """A gather bounded to a few user CTAs (the async DLRM pipeline's side-stream launch) gives
+    the same sums; tiny cache so bags see evictions while they are read."""
+    s = gpu_system(cache_lines=128, ways=8, blocks=1 << 13, pairs=4, engine_warps=4, warps=2)
+    s.fill_store(0, seed=12, kind="f32")
+    rng = np.random.default_rng(user_ctas * 10 + pd)
+    rows = [4000, 900, 2500]
+    idx = np.stack([rng.integers(0, r, size=(96, 20)) for r in rows], axis=1).astype(np.int64)
+    rpp = 8
+    k0 = np.concatenate([[0], np.cumsum([(r + rpp - 1) // rpp for r in rows])[:-1]]).astype(np.uint64)
+    dev = torch.device("cuda", 0)
+    out = torch.full((96, 3, 128), float("nan"), dtype=torch.float32, device=dev)
+    cnt = torch.zeros(2, dtype=torch.int64, device=dev)
+    s.embbag(torch.from_numpy(idx).to(dev), torch.from_numpy(k0.view(np.int64)).to(dev),
+             torch.tensor(rows, dtype=torch.int64, device=dev), out, cnt, prefetch_distance=pd,
+             user_ctas=user_ctas)
+    s.sync(torch.cuda.current_stream(dev).cuda_stream)
+    ref = embbag_reference(12, 0, k0, idx, 128)
+    o = out.cpu().numpy()
+    assert np.max(np.abs(o - ref) / np.maximum(np.abs(ref), 1.0)) < 1e-5
+    assert int(cnt.cpu()[0]) == 96 * 3 * 20

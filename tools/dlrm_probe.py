@@ -78,8 +78,9 @@ def main():
                                      prefetch_distance=0, stream=st.cuda_stream), st) for _ in range(4)]
         print(json.dumps({"full_gather_fresh_ms": float(np.median(ms))}))
     else:
-        # every page resident: tables 1 GiB in a 4 GiB cache
-        s, rows_np, key0, rows = system(4, 1)
+        # every page resident: tables 1 GiB in a 4 GiB cache (hit/hitprof: L2-friendly), or 10 GiB
+        # of tables in the bench's 16 GiB cache (hitbig: the rows stream from HBM)
+        s, rows_np, key0, rows = system(16, 10) if mode == "hitbig" else system(4, 1)
         bat = gpu_zipf_batch(gen, rows_np, B, L, 1.05, True, dev)
         for _ in range(3):
             s.embbag(bat, key0, rows, out, cnt, prefetch_distance=0, stream=st.cuda_stream)
@@ -90,7 +91,7 @@ def main():
                             for _ in range(reps)], st) / reps
         alg = B * T * L * (D * 4 + 8) + B * T * D * 4
         c = cnt.cpu().numpy()
-        print(json.dumps({"hit_ms": ms, "lookups_per_s": B * T * L / ms * 1e3, "alg_gbs": alg / ms / 1e6,
+        print(json.dumps({"mode": mode, "hit_ms": ms, "lookups_per_s": B * T * L / ms * 1e3, "alg_gbs": alg / ms / 1e6,
                           "miss_lookups": int(c[1]), "grid": s.embbag_grid()}))
     s.close()
 
