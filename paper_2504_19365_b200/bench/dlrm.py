@@ -153,13 +153,25 @@ class DlrmModel:
             out = self._run(self.top, x)
         return torch.sigmoid(out)
 
-    def capture(self, dense, pooled, repeat: int):
+    def capture(self, dense, pooled, repeat: int, sm_carveout: int = 0):
         """The forward as one CUDA graph over the fixed `pooled` buffer.  Eager, the MLPs are
         host-launch-bound (~10 small GEMMs per top-MLP pass at batch 2048): the GPU would idle
         between kernels and a "compute" phase would really be CPU time.  Replaying a graph makes
         the MLP phase GPU time, so the compute/communication ratio is the device's."""
         import torch
         self.repeat = repeat
+        # sm_carveout: SMs cuBLAS leaves free (CUBLASLT_MATMUL_DESC_SM_COUNT_TARGET), for a graph
+        # that runs beside a gather holding those SMs; persistent GEMMs sized to all 148 SMs
+        # would otherwise need a second wave
+        prev = torch._C._get_sm_carveout_experimental()
+        torch._C._set_sm_carveout_experimental(sm_carveout if sm_carveout else None)
+        try:
+            return self._capture(dense, pooled)
+        finally:
+            torch._C._set_sm_carveout_experimental(prev)
+
+    def _capture(self, dense, pooled):
+        import torch
         side = torch.cuda.Stream(dense.device)
         side.wait_stream(torch.cuda.current_stream(dense.device))
         with torch.cuda.stream(side):
@@ -187,8 +199,8 @@ def mlp_graph_ms(graph, reps: int = 10) -> float:
     return a.elapsed_time(b) / reps
 
 
-def run_pipeline(system, batches, key0, rows, mlps, outs, mode: str, side_ctas: int = 64,
-                 prefetch_distance: int = 0):
+def run_pipeline(system, batches, key0, rows, mlps, outs, mode: str, side_ctas: int = 16,
+                 prefetch_distance: int = 0, profile: bool = False):
     """Time len(batches) DLRM steps.  `mlps[k]` is a captured forward graph reading the pooled
     buffer `outs[k]` ([B, T, D], k = 0, 1: double buffering).
       sync:     gather(i) -> MLPs(i) on one stream (bench/ctc.py:27-44: compute starts once the
@@ -237,8 +249,9 @@ def run_pipeline(system, batches, key0, rows, mlps, outs, mode: str, side_ctas: 
             mlps[i % 2].replay()
             ev_m[i].record(main)
     elif mode == "prefetch":
-        ev_p = [torch.cuda.Event() for _ in range(n)]
-        ev_e = [torch.cuda.Event() for _ in range(n)]
+        ev_p = [torch.cuda.Event(enable_timing=profile) for _ in range(n)]
+        ev_e = [torch.cuda.Event(enable_timing=profile) for _ in range(n)]
+        ev_m = [torch.cuda.Event(enable_timing=profile) for _ in range(n)]
         side.wait_event(t0)
         system.embbag_prefetch(batches[0], key0, rows, D, pcnt, side_ctas, stream=side.cuda_stream)
         ev_p[0].record(side)
@@ -251,14 +264,23 @@ def run_pipeline(system, batches, key0, rows, mlps, outs, mode: str, side_ctas: 
                 system.embbag_prefetch(batches[i + 1], key0, rows, D, pcnt, side_ctas, stream=side.cuda_stream)
                 ev_p[i + 1].record(side)
             mlps[0].replay()
+            ev_m[i].record(main)
     else:
         raise ValueError(f"unknown pipeline mode {mode!r}")
     t1.record(main)
     torch.cuda.synchronize()
     system.sync(main.cuda_stream)
     c = cnt.cpu().numpy()
-    return {"ms": t0.elapsed_time(t1), "lookups": int(c[0]), "miss_lookups": int(c[1]),
-            "lookups_per_s": n * B * T * L / (t0.elapsed_time(t1) / 1e3)}
+    res = {"ms": t0.elapsed_time(t1), "lookups": int(c[0]), "miss_lookups": int(c[1]),
+           "lookups_per_s": n * B * T * L / (t0.elapsed_time(t1) / 1e3)}
+    if profile and mode == "prefetch" and n > 2:
+        # per step under overlap: prefetch(i+1) = ev_e[i] -> ev_p[i+1]; MLPs(i) = ev_e[i] -> ev_m[i];
+        # gather(i+1) = max(ev_p[i+1], ev_m[i]) -> ev_e[i+1]
+        pf = [ev_e[i].elapsed_time(ev_p[i + 1]) for i in range(1, n - 1)]
+        ml = [ev_e[i].elapsed_time(ev_m[i]) for i in range(1, n - 1)]
+        ga = [ev_m[i].elapsed_time(ev_e[i + 1]) for i in range(1, n - 1)]
+        res.update({"prefetch_ms": sum(pf) / len(pf), "mlp_ms": sum(ml) / len(ml), "gather_ms": sum(ga) / len(ga)})
+    return res
 
 
 def run_dlrm(cfg, trace: bool = False):

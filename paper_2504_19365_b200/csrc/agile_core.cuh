@@ -1256,10 +1256,10 @@ __device__ void model_schedule_rr(const DevCtx& c, bool want, u32 dev, u32 op, u
   }
 }
 
-// pages one engine warp moves per pass (in registers: 32 per page per lane); the register budget
-// of the fused kernel (AGILE_MIN_CTAS) decides what fits without spilling
+// pages one engine warp moves per pass, held in registers (32 per page per lane) while the pass
+// posts completions and fetches new SQEs; the infra grid runs one CTA per SM, so 4 pages fit
 #ifndef AGILE_ENGINE_PAGES
-#define AGILE_ENGINE_PAGES (AGILE_MIN_CTAS > 2 ? 1 : 2)
+#define AGILE_ENGINE_PAGES 4
 #endif
 constexpr int kEnginePages = AGILE_ENGINE_PAGES;
 
@@ -1280,30 +1280,30 @@ __device__ void engine_main(const DevCtx& c, u32 ew) {
     // ---- start moving the bytes of the two oldest fetched commands: the loads (host link
     //      latency) stay in flight while this pass posts completions and fetches new SQEs
     const u32 tocopy = __ballot_sync(FULL, pv && !pcp);
-    int l0 = -1, l1 = -1;
-    uint4 v0[8], v1[8];
-    uint4* t0 = nullptr;
-    uint4* t1 = nullptr;
+    int lk[kEnginePages];
+    uint4 v[kEnginePages][8];
+    uint4* tk[kEnginePages];
+#pragma unroll
+    for (int p = 0; p < kEnginePages; ++p) { lk[p] = -1; tk[p] = nullptr; }
     if (tocopy) {
       did = true;
-      l0 = oldest_lane(pv && !pcp, pseq);   // oldest first: no lane starves behind new fetches
-      l1 = kEnginePages > 1 ? oldest_lane(pv && !pcp && (int)lane != l0, pseq) : -1;
-      const int s1l = l1 < 0 ? l0 : l1;
-      const u32 op0 = __shfl_sync(FULL, pop, l0), op1 = __shfl_sync(FULL, pop, s1l);
-      const u32 d0 = __shfl_sync(FULL, pdev, l0), d1 = __shfl_sync(FULL, pdev, s1l);
-      const u64 b0 = __shfl_sync(FULL, pblk, l0), b1 = __shfl_sync(FULL, pblk, s1l);
-      const u64 p0 = __shfl_sync(FULL, prp, l0), p1 = __shfl_sync(FULL, prp, s1l);
-      const uint4* s0 = op0 == OP_READ ? reinterpret_cast<const uint4*>(c.store[d0] + (b0 << kBlockShift))
-                                       : reinterpret_cast<const uint4*>(p0);
-      t0 = op0 == OP_READ ? reinterpret_cast<uint4*>(p0) : reinterpret_cast<uint4*>(c.store_w[d0] + (b0 << kBlockShift));
-      const uint4* s1 = op1 == OP_READ ? reinterpret_cast<const uint4*>(c.store[d1] + (b1 << kBlockShift))
-                                       : reinterpret_cast<const uint4*>(p1);
-      t1 = op1 == OP_READ ? reinterpret_cast<uint4*>(p1) : reinterpret_cast<uint4*>(c.store_w[d1] + (b1 << kBlockShift));
+      u32 taken = 0;   // lanes already picked this pass
 #pragma unroll
-      for (int k = 0; k < 8; ++k) v0[k] = __ldcg(s0 + lane + 32 * k);
-      if (l1 >= 0) {
+      for (int p = 0; p < kEnginePages; ++p) {
+        // oldest first: no lane starves behind new fetches
+        const int l = oldest_lane(pv && !pcp && !((taken >> lane) & 1u), pseq);
+        lk[p] = l;
+        if (l < 0) break;
+        taken |= 1u << l;
+        const u32 op = __shfl_sync(FULL, pop, l);
+        const u32 d = __shfl_sync(FULL, pdev, l);
+        const u64 b = __shfl_sync(FULL, pblk, l);
+        const u64 pr = __shfl_sync(FULL, prp, l);
+        const uint4* src = op == OP_READ ? reinterpret_cast<const uint4*>(c.store[d] + (b << kBlockShift))
+                                         : reinterpret_cast<const uint4*>(pr);
+        tk[p] = op == OP_READ ? reinterpret_cast<uint4*>(pr) : reinterpret_cast<uint4*>(c.store_w[d] + (b << kBlockShift));
 #pragma unroll
-        for (int k = 0; k < 8; ++k) v1[k] = __ldcg(s1 + lane + 32 * k);
+        for (int k = 0; k < 8; ++k) v[p][k] = __ldcg(src + lane + 32 * k);
       }
     }
     const u64 now = gtimer();
@@ -1449,16 +1449,18 @@ __device__ void engine_main(const DevCtx& c, u32 ew) {
       if (lane == 0) atomicAdd(&c.stats[S_FETCHED], (u64)__popc(nb));
     }
     // ---- finish the page moves started at the top of the pass
-    if (l0 >= 0) {
+    if (lk[0] >= 0) {
+      u32 moved = 0;
 #pragma unroll
-      for (int k = 0; k < 8; ++k) __stcg(t0 + lane + 32 * k, v0[k]);
-      if (l1 >= 0) {
+      for (int p = 0; p < kEnginePages; ++p) {
+        if (lk[p] < 0) break;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) __stcg(t1 + lane + 32 * k, v1[k]);
+        for (int k = 0; k < 8; ++k) __stcg(tk[p] + lane + 32 * k, v[p][k]);
+        moved |= 1u << lk[p];
       }
       __threadfence();   // page bytes visible before the CQE release of these commands
       __syncwarp();
-      if ((int)lane == l0 || (int)lane == l1) pcp = true;
+      if ((moved >> lane) & 1u) pcp = true;
     }
     // ---- exit once the service is done and nothing is in service
     const bool busy = __ballot_sync(FULL, pv) != 0;

@@ -629,15 +629,34 @@ struct EmbBagWork {
     u32 gpool = 0, gleft = 0;
     if (prefetch_only) {
       // batch-level async (AGILE prefetch, gpu_api.py:345-361): submit every missing page of the
-      // batch and return; the service keeps the launch alive until all fills completed
+      // batch and return; the service keeps the launch alive until all fills completed.  The
+      // batch's lookups are taken as one flat stream, 32 per warp pass (lane = lookup, coalesced
+      // index loads), so every lane probes — a bag-per-warp walk would idle 32 - L lanes.
+      const u64 nlk = (u64)nbags * L;
+      u64 base = 0;
+      u32 left = 0;
+      u32 pass = 0;
       while (true) {
-        const u32 nb = grab(c, gpool, gleft);
-        if (nb >= nbags) break;
+        if (!left) {
+          u64 b = 0;
+          if (lane == 0) b = atomicAdd(&c.run->work_next, (u64)kGrab * 32);
+          base = __shfl_sync(FULL, b, 0);
+          left = kGrab;
+        }
+        const u64 g = base + lane;
+        base += 32;
+        --left;
+        if (g - lane >= nlk) break;
+        const bool act = g < nlk;
         u64 key = 0; u32 off = 0;
-        const bool a = bag_keys(nb, lact, key, off);
-        prefetch_warp(c, a, key, who, gw + nb, false);
-        lookups_local += L;
-        if (aborted(c)) break;
+        bool a = false;
+        if (act) {
+          const u32 bag = (u32)(g / L);
+          a = bag_key_of(bag, true, __ldg(idx + g), key, off);
+        }
+        prefetch_warp(c, a, key, who, gw + (++pass), false);
+        lookups_local += __popc(__ballot_sync(FULL, act));
+        if ((pass & 15u) == 0 && aborted(c)) break;
       }
       if (lane == 0) atomicAdd(&lookups_miss[0], (u64)lookups_local);
       return;

@@ -97,3 +97,29 @@ def test_embbag_bounded_grid(gpu_system, user_ctas, pd):
     o = out.cpu().numpy()
     assert np.max(np.abs(o - ref) / np.maximum(np.abs(ref), 1.0)) < 1e-5
     assert int(cnt.cpu()[0]) == 96 * 3 * 20
+
+
+@pytest.mark.parametrize("user_ctas", [1, 3])
+def test_embbag_prefetch_then_gather_all_hits(gpu_system, user_ctas):
+    """Batch-level prefetch (AgileApi.prefetch, gpu_api.py:139-162) pulls every page of the batch
+    into the cache; the gather that follows takes no miss path and matches the oracle."""
+    s = gpu_system(cache_lines=4096, ways=32, blocks=1 << 13, pairs=8, engine_warps=8, warps=2)
+    s.fill_store(0, seed=17, kind="f32")
+    rng = np.random.default_rng(5 + user_ctas)
+    rows = [6000, 1500, 800]
+    idx = np.stack([rng.integers(0, r, size=(100, 20)) for r in rows], axis=1).astype(np.int64)
+    k0 = np.concatenate([[0], np.cumsum([(r + 7) // 8 for r in rows])[:-1]]).astype(np.uint64)
+    dev = torch.device("cuda", 0)
+    di = torch.from_numpy(idx).to(dev)
+    dk = torch.from_numpy(k0.view(np.int64)).to(dev)
+    dr = torch.tensor(rows, dtype=torch.int64, device=dev)
+    pc = torch.zeros(2, dtype=torch.int64, device=dev)
+    s.embbag_prefetch(di, dk, dr, 128, pc, user_ctas=user_ctas)
+    out = torch.full((100, 3, 128), float("nan"), dtype=torch.float32, device=dev)
+    cnt = torch.zeros(2, dtype=torch.int64, device=dev)
+    s.embbag(di, dk, dr, out, cnt, prefetch_distance=0)
+    s.sync(torch.cuda.current_stream(dev).cuda_stream)
+    assert int(pc.cpu()[0]) == 100 * 3 * 20
+    assert int(cnt.cpu()[1]) == 0
+    ref = embbag_reference(17, 0, k0, idx, 128)
+    assert np.max(np.abs(out.cpu().numpy() - ref) / np.maximum(np.abs(ref), 1.0)) < 1e-5

@@ -1,10 +1,11 @@
 """DLRM async-pipeline probe on one GPU (GPU-box tool, not part of the product).
 
-For each (engine warps, service warps) context and each side-stream user-CTA bound, time the
-sync and async DLRM pipelines at a compute/communication ratio near 1, plus the MLP graph alone
-while an idle bounded gather context holds its SMs.
+For each (engine warps, service warps) context: calibrate the MLP graph to a compute/communication
+ratio near 1, pick the fastest MLP graph over cuBLAS SM carve-outs for the sync baseline, then time
+the async (bounded side-stream gather) and prefetch (bounded AGILE prefetch + full gather)
+pipelines for each side-CTA bound and carve-out.
 
-  python tools/pipe_probe.py [cache_gib] [table_gib]
+  COMBOS=128/48,64/16 UCS=16,32,64 CARVE=0,16,32 python tools/pipe_probe.py [cache_gib] [table_gib]
 """
 import json
 import os
@@ -50,47 +51,45 @@ def main():
     cnt = torch.zeros(2, dtype=torch.int64, device=dev)
     model = DlrmModel(dev, D, T)
     dense = torch.randn(B, 13, device=dev, dtype=torch.bfloat16)
-    combos = [tuple(int(x) for x in c.split("/")) for c in os.environ.get("COMBOS", "128/48,64/16,32/8").split(",")]
-    pds = [int(x) for x in os.environ.get("PDS", "0").split(",")]
-    ucs = [int(x) for x in os.environ.get("UCS", "8,16,32,64,0").split(",")]
+    combos = [tuple(int(x) for x in c.split("/")) for c in os.environ.get("COMBOS", "128/48,64/16").split(",")]
+    ucs = [int(x) for x in os.environ.get("UCS", "16,32,64").split(",")]
+    cos = [int(x) for x in os.environ.get("CARVE", "0,16,32").split(",")]
+    modes = os.environ.get("MODES", "async,prefetch").split(",")
+    n = 10
     for ew, sw in combos:
         s, rows_np, key0, rows = make(cache_gib, table_gib, ew, sw)
         full, infra = s.embbag_grid()
         for _ in range(int(1.3 * s.num_lines / 69000) + 4):
             s.embbag(gpu_zipf_batch(gen, rows_np, B, L, 1.05, True, dev), key0, rows, outs[0], cnt, prefetch_distance=0)
         s.sync(st.cuda_stream)
-        # gather time on fresh batches (full grid)
-        bat = [gpu_zipf_batch(gen, rows_np, B, L, 1.05, True, dev) for _ in range(8)]
         f1 = mlp_graph_ms(model.capture(dense, outs[0], 1))
         f9 = mlp_graph_ms(model.capture(dense, outs[0], 9))
         per = max((f9 - f1) / 8, 1e-3)
+        bat = [gpu_zipf_batch(gen, rows_np, B, L, 1.05, True, dev) for _ in range(n)]
         r = run_pipeline(s, bat, key0, rows, [model.capture(dense, o, 1) for o in outs], outs, "sync")
-        g_ms = r["ms"] / len(bat) - f1
+        g_ms = r["ms"] / n - f1
         rep = max(1, int(round((g_ms - f1) / per)) + 1)
-        mlps = [model.capture(dense, o, rep) for o in outs]
-        mlp_ms = mlp_graph_ms(mlps[0], 3)
-        for uc, pd in [(u if u else full, p) for u in ucs for p in pds]:
-            res = {}
-            for mode in ("sync", "async"):
-                bat = [gpu_zipf_batch(gen, rows_np, B, L, 1.05, True, dev) for _ in range(10)]
-                res[mode] = run_pipeline(s, bat, key0, rows, mlps, outs, mode, side_ctas=uc,
-                                         prefetch_distance=pd)["ms"] / 10
-            # gather alone with this bound (fresh batches)
-            bat = [gpu_zipf_batch(gen, rows_np, B, L, 1.05, True, dev) for _ in range(6)]
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(st)
-            for x in bat:
-                s.embbag(x, key0, rows, outs[0], cnt, prefetch_distance=pd, user_ctas=uc, stream=st.cuda_stream)
-            b.record(st)
-            torch.cuda.synchronize()
-            gb = a.elapsed_time(b) / len(bat)
-            print(json.dumps({"engine_warps": ew, "service_warps": sw, "infra_ctas": infra, "user_ctas": uc, "pd": pd,
-                              "gather_ms_full": g_ms, "gather_ms_bounded": gb, "mlp_ms": mlp_ms,
-                              "sync_ms": res["sync"], "async_ms": res["async"],
-                              "speedup": res["sync"] / res["async"],
-                              "ideal": (g_ms + mlp_ms) / max(g_ms, mlp_ms)}), flush=True)
+        graphs, mlp_ms = {}, {}
+        for co in cos:
+            graphs[co] = [model.capture(dense, o, rep, sm_carveout=co) for o in outs]
+            mlp_ms[co] = mlp_graph_ms(graphs[co][0], 3)
+        best = min(cos, key=lambda k: mlp_ms[k])
+        bat = [gpu_zipf_batch(gen, rows_np, B, L, 1.05, True, dev) for _ in range(n)]
+        sync_ms = run_pipeline(s, bat, key0, rows, graphs[best], outs, "sync")["ms"] / n
+        print(json.dumps({"engine_warps": ew, "service_warps": sw, "infra_ctas": infra, "gather_ms": g_ms,
+                          "mlp_ms_by_carveout": mlp_ms, "sync_carveout": best, "sync_ms": sync_ms}), flush=True)
+        for mode in modes:
+            for uc in ucs:
+                for co in cos:
+                    bat = [gpu_zipf_batch(gen, rows_np, B, L, 1.05, True, dev) for _ in range(n)]
+                    rr = run_pipeline(s, bat, key0, rows, graphs[co], outs, mode, side_ctas=uc, profile=True)
+                    ms = rr["ms"] / n
+                    print(json.dumps({"ew": ew, "sw": sw, "mode": mode, "user_ctas": uc, "carveout": co,
+                                      "ms": ms, "speedup": sync_ms / ms, "parts": {k: rr[k] for k in
+                                      ("prefetch_ms", "mlp_ms", "gather_ms") if k in rr},
+                                      "ideal": (g_ms + mlp_ms[best]) / max(g_ms, mlp_ms[best])}), flush=True)
         s.close()
-        del mlps
+        del graphs
 
 
 if __name__ == "__main__":
