@@ -288,10 +288,17 @@ def main():
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
+    prof_step = int(os.environ.get("AGILE_PROFILE_STEP", "-1"))   # ncu --replay-mode range target
     for k in range(args.steps):
+        if k == prof_step:
+            torch.cuda.synchronize()
+            torch.cuda.profiler.start()
         ev[k][0].record(stream)
         step(args.warmup + k, args.prefetch)
         ev[k][1].record(stream)
+        if k == prof_step:
+            torch.cuda.synchronize()
+            torch.cuda.profiler.stop()
     e1.record(stream)
     barrier()
     clk = clocks.stop()

@@ -34,6 +34,9 @@ struct agile_ctx {
   void* d_stage = nullptr;
   size_t d_stage_bytes = 0;
   cudaStream_t stream = nullptr;
+  // launch mode: false = split (infra grid + PDL user grid, the default), true = one fused grid
+  // with roles by arrival ticket (AGILE_LAUNCH=fused: what a kernel-serialising profiler captures)
+  bool fused = false;
   // async_read WaitNodes (AgileBuf barriers) for the reads / loop / seq workloads
   void* nodes = nullptr;
   size_t nodes_cap = 0;
@@ -160,6 +163,7 @@ size_t dyn_smem() {
     static bool set = false;
     if (!set) {
       cudaFuncSetAttribute(agile_user_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b);
+      cudaFuncSetAttribute(agile_fused_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b);
       set = true;
     }
   }
@@ -176,6 +180,7 @@ void load_kernels() {
   cudaFuncAttributes a{};
   cudaFuncGetAttributes(&a, agile_infra_kernel);
   cudaFuncGetAttributes(&a, agile_user_kernel<W>);
+  cudaFuncGetAttributes(&a, agile_fused_kernel<W>);
   loaded = true;
 }
 
@@ -189,6 +194,11 @@ int launch(agile_ctx* ctx, const W& work, uint32_t n_user_ctas, cudaStream_t st)
   L.n_user_ctas = n_user_ctas;
   L.pad = 0;
   const uint32_t ninfra = ctx->d.n_engine_ctas + ctx->d.n_service_ctas;
+  if (ctx->fused) {
+    agile_fused_kernel<W><<<ninfra + n_user_ctas, kCtaThreads, dyn_smem<W>(), st>>>(ctx->d, L, work);
+    CK(cudaGetLastError());
+    return 0;
+  }
   agile_infra_kernel<<<ninfra, kCtaThreads, 0, st>>>(ctx->d, L);
   CK(cudaGetLastError());
   // the user grid may start once every infra CTA executed griddepcontrol.launch_dependents
@@ -210,6 +220,13 @@ int launch(agile_ctx* ctx, const W& work, uint32_t n_user_ctas, cudaStream_t st)
 // over all SMs minus the user CTAs each infra CTA displaces on its SM (registers bound both)
 template <class W>
 uint32_t resident_ctas(agile_ctx* ctx) {
+  if (ctx->fused) {
+    int f = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&f, agile_fused_kernel<W>, kCtaThreads, dyn_smem<W>());
+    const uint32_t tot = (uint32_t)std::max(1, f) * (uint32_t)ctx->sms;
+    const uint32_t ninfra = ctx->d.n_engine_ctas + ctx->d.n_service_ctas;
+    return tot > ninfra + 1 ? tot - ninfra : 1;
+  }
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, agile_user_kernel<W>, kCtaThreads, dyn_smem<W>());
   if (per_sm < 1) per_sm = 1;
@@ -263,6 +280,7 @@ int agile_create(const char* config_text, int cuda_device, agile_ctx** out) {
   int sms = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cuda_device));
   ctx->sms = sms;
+  if (const char* lm = getenv("AGILE_LAUNCH")) ctx->fused = std::string(lm) == "fused";
   Cfg cfg;
   cfg.kv = parse_kv(config_text);
   DevCtx& d = ctx->d;

@@ -1263,6 +1263,7 @@ __device__ void model_schedule_rr(const DevCtx& c, bool want, u32 dev, u32 op, u
 #endif
 constexpr int kEnginePages = AGILE_ENGINE_PAGES;
 
+template <int kPages = kEnginePages>
 __device__ void engine_main(const DevCtx& c, u32 ew) {
   const u32 lane = lane_id();
   const u32 E = c.engine_warps;
@@ -1280,16 +1281,16 @@ __device__ void engine_main(const DevCtx& c, u32 ew) {
     // ---- start moving the bytes of the two oldest fetched commands: the loads (host link
     //      latency) stay in flight while this pass posts completions and fetches new SQEs
     const u32 tocopy = __ballot_sync(FULL, pv && !pcp);
-    int lk[kEnginePages];
-    uint4 v[kEnginePages][8];
-    uint4* tk[kEnginePages];
+    int lk[kPages];
+    uint4 v[kPages][8];
+    uint4* tk[kPages];
 #pragma unroll
-    for (int p = 0; p < kEnginePages; ++p) { lk[p] = -1; tk[p] = nullptr; }
+    for (int p = 0; p < kPages; ++p) { lk[p] = -1; tk[p] = nullptr; }
     if (tocopy) {
       did = true;
       u32 taken = 0;   // lanes already picked this pass
 #pragma unroll
-      for (int p = 0; p < kEnginePages; ++p) {
+      for (int p = 0; p < kPages; ++p) {
         // oldest first: no lane starves behind new fetches
         const int l = oldest_lane(pv && !pcp && !((taken >> lane) & 1u), pseq);
         lk[p] = l;
@@ -1452,7 +1453,7 @@ __device__ void engine_main(const DevCtx& c, u32 ew) {
     if (lk[0] >= 0) {
       u32 moved = 0;
 #pragma unroll
-      for (int p = 0; p < kEnginePages; ++p) {
+      for (int p = 0; p < kPages; ++p) {
         if (lk[p] < 0) break;
 #pragma unroll
         for (int k = 0; k < 8; ++k) __stcg(tk[p] + lane + 32 * k, v[p][k]);
@@ -1499,12 +1500,12 @@ __device__ void engine_main(const DevCtx& c, u32 ew) {
 // The last user CTA out waits for the infra CTAs to exit, so the next run on the stream (which
 // resets the run words) cannot overlap this run's infra grid.
 
-__device__ __forceinline__ void user_done(const DevCtx& c) {
+__device__ __forceinline__ void user_done(const DevCtx& c, u32 n_users) {
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
     const u32 n = atomicAdd(&c.run->users_done, 1u) + 1;
-    if (n == gridDim.x) {
+    if (n == n_users) {
       const u32 ninfra = c.n_engine_ctas + c.n_service_ctas;
       Spin sp;
       while (ld_acquire(&c.run->infra_exited) < ninfra)
@@ -1518,7 +1519,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1) agile_infra_kernel(const __gri
   const u32 warp = threadIdx.x >> 5;
   if (blockIdx.x < c.n_engine_ctas) {
     const u32 ew = blockIdx.x * kCtaWarps + warp;
-    if (ew < c.engine_warps) engine_main(c, ew);
+    if (ew < c.engine_warps) engine_main<kEnginePages>(c, ew);
   } else {
     const u32 sw = (blockIdx.x - c.n_engine_ctas) * kCtaWarps + warp;
     if (sw < c.service_warps) service_main(c, L, sw);
@@ -1544,7 +1545,40 @@ __global__ void __launch_bounds__(kCtaThreads, UserMinCtas<Work>::v)
     agile_user_kernel(const __grid_constant__ DevCtx c, const Launch L, const __grid_constant__ Work work) {
   if (threadIdx.x == 0) atomicAdd(&c.run->users_started, 1u);
   work.run(c, blockIdx.x, L.n_user_ctas);
-  user_done(c);
+  user_done(c, L.n_user_ctas);
+}
+
+// Fused single-grid launch (config `launch.mode = fused`): the roles are taken by arrival ticket —
+// the first CTAs to start become the engine and the service — so users again wait only on
+// resident CTAs.  One register budget for all roles (2 CTAs per SM, 2-page engine passes).  This
+// is the mode a kernel-serialising profiler can capture (ncu replays one kernel at a time, which
+// the two co-running grids of the split launch cannot survive); the split launch is the default.
+template <class Work>
+__global__ void __launch_bounds__(kCtaThreads, 2)
+    agile_fused_kernel(const __grid_constant__ DevCtx c, const Launch L, const __grid_constant__ Work work) {
+  __shared__ u32 s_ticket;
+  if (threadIdx.x == 0) s_ticket = atomicAdd(&c.run->ticket, 1u);
+  __syncthreads();
+  u32 t = s_ticket;
+  const u32 warp = threadIdx.x >> 5;
+  if (t < c.n_engine_ctas + c.n_service_ctas) {
+    if (t < c.n_engine_ctas) {
+      const u32 ew = t * kCtaWarps + warp;
+      if (ew < c.engine_warps) engine_main<2>(c, ew);
+    } else {
+      const u32 sw = (t - c.n_engine_ctas) * kCtaWarps + warp;
+      if (sw < c.service_warps) service_main(c, L, sw);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(&c.run->infra_exited, 1u);
+    }
+    return;
+  }
+  if (threadIdx.x == 0) atomicAdd(&c.run->users_started, 1u);
+  work.run(c, t - c.n_engine_ctas - c.n_service_ctas, L.n_user_ctas);
+  user_done(c, L.n_user_ctas);
 }
 
 }  // namespace agile

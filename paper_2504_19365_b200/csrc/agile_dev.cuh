@@ -135,6 +135,7 @@ struct CmdCtx {      // side table indexed by (sq, slot) == CommandContext (nvme
 };
 
 struct alignas(64) RunWords {   // reset before every launch
+  u32 ticket;        // fused launch: role by arrival order
   u32 users_started;
   u32 users_done;
   u32 infra_exited;

@@ -1183,7 +1183,9 @@ struct SpmvWork {
 #pragma unroll
           for (u32 j = 0; j < 4; ++j) {
             const u64 e = e0 + (p0 + j) * 32 + lane;
-            xv[j] = e < e1 ? __ldg(x + col[j]) : 0.f;
+            // col is speculative until the page is validated below: an index read from a line
+            // that changed identity mid-read must not address outside x (the pass is redone)
+            xv[j] = (e < e1 && col[j] < V) ? __ldg(x + col[j]) : 0.f;
           }
 #pragma unroll
           for (u32 j = 0; j < 4; ++j) {

@@ -123,3 +123,14 @@ def test_embbag_prefetch_then_gather_all_hits(gpu_system, user_ctas):
     assert int(cnt.cpu()[1]) == 0
     ref = embbag_reference(17, 0, k0, idx, 128)
     assert np.max(np.abs(out.cpu().numpy() - ref) / np.maximum(np.abs(ref), 1.0)) < 1e-5
+
+
+def test_fused_launch_mode_matches(gpu_system, monkeypatch):
+    """AGILE_LAUNCH=fused (one grid, roles by arrival ticket: the profiling mode) computes the same
+    embedding-bag sums as the default split launch."""
+    monkeypatch.setenv("AGILE_LAUNCH", "fused")
+    s = gpu_system(cache_lines=512, ways=16, blocks=1 << 13, pairs=4, engine_warps=8, warps=2)
+    s.fill_store(0, seed=23, kind="f32")
+    err, cnt = _run(s, 23, 3, [3000, 700, 1200], 48, 20, 128, 0, np.random.default_rng(3))
+    assert err < 1e-5
+    assert cnt[0] == 48 * 3 * 20 and cnt[1] > 0

@@ -1,10 +1,11 @@
 #!/bin/bash
-# ncu evidence for the embedding-bag fused kernel (1 GPU): launch list of a bench run + one full
-# capture of a steady-state timed launch (2 GiB cache config so replays stay cheap)
+# ncu evidence for the embedding-bag step.  The production launch runs two grids concurrently
+# (infra + PDL user grid); ncu serialises kernels, so the captures use the fused single-grid mode
+# (AGILE_LAUNCH=fused: same device code, roles by arrival ticket, one register budget).
 mkdir -p gpurun_out
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
-  python bench.py --quick --steps 6 --warmup 3 --cache-gib 2 --warm-batches 8 > gpurun_out/prof_bench_launches.json 2>&1
-timeout 1200 ncu --set full --import-source on --clock-control none -k regex:agile_kernel -s 11 -c 1 \
-  -o gpurun_out/prof_embbag python bench.py --quick --steps 2 --warmup 3 --cache-gib 2 --warm-batches 8 \
-  > gpurun_out/prof_full.log 2>&1
-ls -la gpurun_out/*.ncu-rep
+export AGILE_LAUNCH=fused
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
+  python bench.py --quick --steps 6 --warmup 3 ${BENCH_ARGS} > gpurun_out/prof_bench_launches.json 2>&1; echo "launches rc=$?"
+timeout 1200 ncu --set full --import-source on --clock-control none -k regex:agile_fused_kernel -s ${SKIP:-12} -c 1 \
+  -o gpurun_out/prof_embbag python bench.py --quick --steps 3 --warmup 3 ${BENCH_ARGS} > gpurun_out/prof_full.log 2>&1; echo "full rc=$?"
+tail -2 gpurun_out/prof_full.log
