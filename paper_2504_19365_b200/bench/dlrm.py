@@ -15,6 +15,8 @@ from __future__ import annotations
 import math
 from dataclasses import dataclass
 
+import os
+
 import numpy as np
 
 # Criteo Kaggle categorical cardinalities (26 sparse features)
@@ -217,7 +219,8 @@ def run_pipeline(system, batches, key0, rows, mlps, outs, mode: str, side_ctas: 
     B, T, L = batches[0].shape
     D = outs[0].shape[-1]
     main = torch.cuda.current_stream(dev)
-    side = torch.cuda.Stream(dev, priority=-1)   # lower = higher: its CTAs dispatch ahead of the MLPs'
+    # lower = higher: the side launch's CTAs dispatch ahead of the MLPs' (AGILE_SIDE_PRIORITY=0: equal)
+    side = torch.cuda.Stream(dev, priority=int(os.environ.get("AGILE_SIDE_PRIORITY", "-1")))
     cnt = torch.zeros(2, dtype=torch.int64, device=dev)
     pcnt = torch.zeros(2, dtype=torch.int64, device=dev)
     n = len(batches)
