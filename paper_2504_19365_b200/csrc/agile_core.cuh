@@ -492,6 +492,9 @@ __device__ bool ring_doorbell_until(const DevCtx& c, u32 q, u64 target, u32 who)
         const u32 b = __ballot_sync(FULL, upd);
         const u32 prefix = (~b) ? (u32)(__ffs(~b) - 1) : 32u;
         if (lane < prefix) {
+          // per-lane acq_rel CAS: each lane's flip is itself a release (a relaxed store made
+          // visible only through lane 0's doorbell release is not cumulative in practice — the
+          // engine then saw the doorbell before the ISSUED word)
           if (atom_cas_acqrel(&c.sq_state[idx], SQ_UPDATED, SQ_ISSUED) != SQ_UPDATED)
             set_error(c, E_PROTOCOL, q, vi);
           log_ev(c, who, M_NVME, A_SQE_ISSUED, q, vi & (D - 1), vi & (D - 1));
@@ -510,6 +513,7 @@ __device__ bool ring_doorbell_until(const DevCtx& c, u32 q, u64 target, u32 who)
         st_release(&s->db_lock, 0u);
       }
       __syncwarp();
+      if (v >= target) return true;   // published past our entries: no re-read of the doorbell
       continue;
     }
     if (!sp.again(c, 256, __LINE__ + 100000 * SPIN_FILE_ID)) return false;
@@ -579,8 +583,15 @@ __device__ bool submit_warp(const DevCtx& c, bool has, u32 dev, u64 blk, u32 lin
       x->kind = kind;
       x->buf = buf;
       log_ev(c, who, M_NVME, A_ENQUEUE, q, slot, slot, op, dev, blk);
-      if (atom_cas_acqrel(&c.sq_state[idx], SQ_EMPTY, SQ_UPDATED) != SQ_EMPTY)
-        set_error(c, E_PROTOCOL, q, v);   // mark_updated on a non-EMPTY entry (nvme_queue.py:160-162)
+      // EMPTY -> UPDATED publishes the SQE and its context (release).  The reserved slot is EMPTY
+      // by construction (tail - head <= depth - 1, head advances over released entries only);
+      // debug runs verify it with a CAS (mark_updated, nvme_queue.py:160-162).
+      if (c.trace) {
+        if (atom_cas_acqrel(&c.sq_state[idx], SQ_EMPTY, SQ_UPDATED) != SQ_EMPTY)
+          set_error(c, E_PROTOCOL, q, v);
+      } else {
+        st_release(&c.sq_state[idx], SQ_UPDATED);
+      }
       log_ev(c, who, M_NVME, A_SQE_UPDATED, q, slot);
     }
     __syncwarp();

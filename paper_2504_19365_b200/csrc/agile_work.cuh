@@ -109,12 +109,23 @@ struct ReadsWork {
   u32 tasks, reads, epochs, async_mode;
   u64 compute_ns;
   static constexpr int MAXR = 64;
+  // A warp's tasks issue their reads as one flat list of (task, i) requests, 32 per pass: with
+  // fewer than 32 active tasks in the warp (the reference's 16-task default) every pass still
+  // fills the warp, so the issue takes ceil(n * reads / 32) access passes instead of `reads`.
+  // Each request keeps its task's node and buffer; ordering within a task is unchanged.
   __device__ void issue(const DevCtx& c, u32 task, bool act, u32 e, u32 set, u32 who, u32 sq_start) const {
-    for (u32 i = 0; i < reads; ++i) {
-      const u64 key = act ? keys[((u64)e * tasks + task) * reads + i] : 0ull;
-      const u64 slot = ((u64)task * 2 + set) * reads + i;
-      async_read_warp(c, act, key, nodes + (act ? slot : 0), bufs + (act ? slot : 0) * 256, who,
-                      sq_start + i + e * reads);
+    const u32 lane = lane_id();
+    const u32 nact = __popc(__ballot_sync(FULL, act));   // active tasks are the warp's low lanes
+    const u32 base_task = task - lane;
+    const u32 total = nact * reads;
+    for (u32 k = 0; k * 32 < total; ++k) {
+      const u32 f = k * 32 + lane;
+      const bool a = f < total;
+      const u32 t = base_task + (a ? f / reads : 0), i = a ? f % reads : 0;
+      const u64 key = a ? keys[((u64)e * tasks + t) * reads + i] : 0ull;
+      const u64 slot = ((u64)t * 2 + set) * reads + i;
+      async_read_warp(c, a, key, nodes + (a ? slot : 0), bufs + (a ? slot : 0) * 256, who,
+                      sq_start + k + e * reads);
     }
   }
   __device__ void wait_set(const DevCtx& c, u32 task, bool act, u32 set, u64& dg) const {
@@ -145,6 +156,11 @@ struct ReadsWork {
       }
     } else {
       issue(c, task, act, 0, 0, who, sq_start);
+      // every task's epoch-0 reads are queued before any epoch-1 read: a task that finished its
+      // issue early would otherwise interleave epoch-1 commands into the device FIFO ahead of
+      // other tasks' epoch-0 commands and delay the first wait by a whole epoch (the reference's
+      // cooperative scheduler issues epoch 0 in one uninterrupted pass, bench/ctc.py:47-58)
+      if (!user_grid_barrier(c, nusers)) return;
       for (u32 e = 0; e < epochs; ++e) {
         const u32 cur = e & 1u;
         // the next epoch's fetches ride under this epoch's compute (bench/ctc.py:47-70)

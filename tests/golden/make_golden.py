@@ -57,7 +57,8 @@ class SetAssocClock(CachePolicy):
 
     def set_of(self, key):
         dev, blk = key
-        return (((blk * 0x9E3779B1) ^ (dev * 0x85EBCA77)) & 0xFFFFFFFF) % self.S
+        x = ((blk ^ (dev << 40)) * 0x9E3779B97F4A7C15) & 0xFFFFFFFFFFFFFFFF   # oracle/cache.py:set_of
+        return ((x >> 32) * self.S) >> 32
 
     def on_hit(self, i):
         self.ref[i] = 1

@@ -55,7 +55,9 @@ def bfs(scale, frac):
         for seed in range(3):
             s.reset()
             src = pick_source(row_ptr, seed)
+            f0 = s.stats()["fills"]
             level, st = run_bfs(s, row_ptr, V, src, 0, pd)
+            st["fills"] = s.stats()["fills"] - f0   # every page the engine moved (prefetches too)
             if pd == 0 and seed == 0:
                 ref = level.clone()
             if pd == 2 and seed == 0:
@@ -63,7 +65,7 @@ def bfs(scale, frac):
             runs.append(st)
         ms = sum(r["ms"] for r in runs) / len(runs)
         edges = sum(r["edges"] for r in runs) / len(runs)
-        misses = sum(r["page_misses"] for r in runs) / len(runs)
+        misses = sum(r["fills"] for r in runs) / len(runs)
         out[pd] = {"ms": ms, "gteps": edges / ms / 1e6, "edges": edges, "levels": runs[0]["levels"],
                    "page_fills": misses, "link_gbs": misses * 4096 / ms / 1e6,
                    "link_frac": misses * 4096 / ms / 1e6 / LINK_PEAK,
@@ -93,10 +95,14 @@ def spmv(scale, frac, iters):
     ys = {}
     for pd in (0, 2):
         s.reset()
+        f0 = s.stats()["fills"]
         y, st = run_spmv(s, rowT, V, E, 0, nxt, x, 1, pd)
+        st["page_misses"] = s.stats()["fills"] - f0   # engine fills, prefetches included
         ys[pd] = y
         s.reset()
+        f0 = s.stats()["fills"]
         _, pr = run_pagerank(s, rowT, V, E, 0, outdeg, iters, prefetch_distance=pd)
+        pr["page_misses"] = s.stats()["fills"] - f0
         res[pd] = {"spmv_ms": st["ms"], "spmv_gflops": st["gflops"], "spmv_page_fills": st["page_misses"],
                    "spmv_link_gbs": st["page_misses"] * 4096 / st["ms"] / 1e6,
                    "spmv_link_frac": st["page_misses"] * 4096 / st["ms"] / 1e6 / LINK_PEAK,
