@@ -39,8 +39,9 @@ static inline uint64_t splitmix64(uint64_t x) {
 }
 
 static inline uint32_t set_of(uint64_t dev, uint64_t blk, uint64_t sets) {
-  const uint64_t x = (blk ^ (dev << 40)) * 0x9E3779B97F4A7C15ull;   /* Fibonacci hashing */
-  return (uint32_t)(((x >> 32) * sets) >> 32);
+  const uint32_t x = (uint32_t)blk * 0x9E3779B9u + (uint32_t)(blk >> 32) * 0x85EBCA77u +
+                     (uint32_t)dev * 0xC2B2AE35u;   /* Fibonacci hashing */
+  return (uint32_t)(((uint64_t)x * sets) >> 32);
 }
 
 void* oracle_cache_create(uint64_t lines, uint64_t ways, uint64_t seed) {

@@ -7,7 +7,7 @@ cache's observable sequence:
     unavailable lines, clearing ref bits, returning the first line with ref 0; a READY victim is
     reset (evict_reset, software_cache.py:339-346) and the new block inserted with ref 1.
 The set-associative generalisation is SURVEY A.2's plug-in with a Fibonacci set index:
-set = hi32((blk ^ dev<<40) * 0x9E3779B97F4A7C15) * S >> 32 (SURVEY A.2 used the low bits of a
+set = ((blk * 0x9E3779B9 + (blk >> 32) * 0x85EBCA77 + dev * 0xC2B2AE35) mod 2^32) * S >> 32 (SURVEY A.2 used the low bits of a
 32-bit multiplicative hash, which fold strided block ids onto a few sets), one hand per set, sweep
 restricted to the set's ways.
 With S = 1 it is the reference's built-in clock.  In serialized mode no line is ever BUSY at
@@ -18,11 +18,11 @@ from __future__ import annotations
 
 
 def set_of(dev: int, blk: int, num_sets: int) -> int:
-    """Fibonacci hashing: the high 32 bits of (blk ^ dev<<40) * 2^64/phi, scaled to [0, S) by a
-    multiply-high.  Arithmetic progressions of block ids (sequential epochs, strided pages) land
+    """Fibonacci hashing: x = blk * 2^32/phi (+ high block bits and device) mod 2^32, scaled to
+    [0, S) by a multiply-high.  Arithmetic progressions of block ids (sequential epochs, strided pages) land
     with near-minimal discrepancy, so sets fill evenly."""
-    x = ((blk ^ (dev << 40)) * 0x9E3779B97F4A7C15) & 0xFFFFFFFFFFFFFFFF
-    return ((x >> 32) * num_sets) >> 32
+    x = ((blk & 0xFFFFFFFF) * 0x9E3779B9 + (blk >> 32) * 0x85EBCA77 + dev * 0xC2B2AE35) & 0xFFFFFFFF
+    return (x * num_sets) >> 32
 
 
 def clock_sequence(accesses, lines: int, ways: int | None = None):

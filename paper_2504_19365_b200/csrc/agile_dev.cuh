@@ -314,12 +314,14 @@ __device__ __forceinline__ void stat_warp(const DevCtx& c, int slot, u32 n) {
 // ---------------------------------------------------------------- cache geometry
 // set index: the plug-in hash of SURVEY A.2 (constants of share_table.py:66-68)
 __host__ __device__ __forceinline__ u32 set_of_key(u64 key, u32 num_sets, u32 pow2) {
-  // Fibonacci hashing (oracle/cache.py:set_of): high 32 bits of (blk ^ dev<<40) * 2^64/phi, scaled
-  // to [0, S) by a multiply-high; arithmetic progressions of block ids spread with near-minimal
-  // discrepancy (the low bits of a 32-bit multiplicative hash fold strided ids onto a few sets)
-  const u64 x = (key_blk(key) ^ ((u64)key_dev(key) << 40)) * 0x9E3779B97F4A7C15ull;
+  // Fibonacci hashing (oracle/cache.py:set_of): x = blk * 2^32/phi (+ the high block bits and the
+  // device, other odd constants) mod 2^32, scaled to [0, S) by a multiply-high: arithmetic
+  // progressions of block ids spread with near-minimal discrepancy (the LOW bits of a
+  // multiplicative hash fold strided ids onto a few sets)
+  const u64 blk = key_blk(key);
+  const u32 x = (u32)blk * 0x9E3779B9u + (u32)(blk >> 32) * 0x85EBCA77u + key_dev(key) * 0xC2B2AE35u;
   (void)pow2;
-  return (u32)(((x >> 32) * (u64)num_sets) >> 32);
+  return (u32)(((u64)x * num_sets) >> 32);
 }
 __device__ __forceinline__ u32 set_of(const DevCtx& c, u64 key) { return set_of_key(key, c.num_sets, c.sets_pow2); }
 // 16-bit signature of a key (independent of the set-index bits): a set's W signatures are 2W

@@ -57,8 +57,8 @@ class SetAssocClock(CachePolicy):
 
     def set_of(self, key):
         dev, blk = key
-        x = ((blk ^ (dev << 40)) * 0x9E3779B97F4A7C15) & 0xFFFFFFFFFFFFFFFF   # oracle/cache.py:set_of
-        return ((x >> 32) * self.S) >> 32
+        x = ((blk & 0xFFFFFFFF) * 0x9E3779B9 + (blk >> 32) * 0x85EBCA77 + dev * 0xC2B2AE35) & 0xFFFFFFFF
+        return (x * self.S) >> 32                     # oracle/cache.py:set_of (Fibonacci hashing)
 
     def on_hit(self, i):
         self.ref[i] = 1
