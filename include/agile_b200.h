@@ -96,6 +96,18 @@ int agile_run_reads(agile_ctx* ctx, const uint64_t* keys, uint32_t tasks, uint32
 int agile_run_loop(agile_ctx* ctx, uint32_t conc, uint64_t warmup_ns, uint64_t measure_ns,
                    uint64_t max_per_task, void* bufs, uint64_t* counters, void* stream);
 
+/* Same, write_mode != 0: each requester keeps one async_write (bench/bandwidth.py:20-42 write
+ * mode): its buffer (bytes idx & 0xFF) lands in the cache line and is written through to the
+ * device; counters[0] counts completed writes. */
+int agile_run_loop_rw(agile_ctx* ctx, uint32_t conc, uint64_t warmup_ns, uint64_t measure_ns,
+                      uint64_t max_per_task, void* bufs, uint64_t* counters, int write_mode, void* stream);
+
+/* async_write + wait of n whole blocks (SoftwareCache.write_block / AgileApi.async_write,
+ * software_cache.py:221-235, gpu_api.py:192-227), one GPU thread per block, host buffers:
+ * pages[n][4096].  Each block lands in its cache line (resident: overwritten in place; else a
+ * victim is claimed) and is written through to the device store before the call returns. */
+int agile_write_blocks(agile_ctx* ctx, const uint32_t* dev, const uint64_t* blk, int64_t n, const void* pages);
+
 /* Gather epochs (bench/sweeps.py:39-88): keys[tasks][epochs][gathers]; values = u32 element 0
  * of every gathered block; epoch_t[2] = start/end. */
 int agile_run_gather(agile_ctx* ctx, const uint64_t* keys, uint32_t tasks, uint32_t epochs, uint32_t gathers,

@@ -20,12 +20,10 @@ def _measure_point(cfg, conc: int, write: bool, trace: bool):
     system_cfg.cache.bytes = 0
     w = system_cfg.cache.ways or system_cfg.cache.lines
     system_cfg.cache.lines = -(-system_cfg.cache.lines // w) * w
-    if write:
-        raise NotImplementedError("rand_write needs the write path (SURVEY 8(f) row 1), not in this build")
     recorder = TraceRecorder() if trace else None
     system = AgileSystem(system_cfg, recorder=recorder)
     try:
-        r = system.run_loop(conc, cfg.warmup_ns, cfg.measure_ns)
+        r = system.run_loop(conc, cfg.warmup_ns, cfg.measure_ns, write=write)
         gbps = r["completions"] * system.block_size / r["window_ns"]
         rec = system.events() if trace else None
     finally:

@@ -604,6 +604,31 @@ int agile_run_seq(agile_ctx* ctx, const uint32_t* dev, const uint64_t* blk, int6
   return rc;
 }
 
+int agile_write_blocks(agile_ctx* ctx, const uint32_t* dev, const uint64_t* blk, int64_t n, const void* pages) {
+  if (!ctx || n < 0 || (n && (!dev || !blk || !pages))) return fail(ctx, AGILE_E_ARG, "bad write args");
+  CK(cudaSetDevice(ctx->device));
+  for (int64_t i = 0; i < n; ++i) {
+    if (dev[i] >= ctx->d.num_devices) return fail(ctx, AGILE_E_OUT_OF_RANGE, "no such device");
+    if (blk[i] >= ctx->store_blocks[dev[i]]) return fail(ctx, AGILE_E_OUT_OF_RANGE, "block out of range");
+  }
+  if (n == 0) return 0;
+  uint32_t* d_dev; uint64_t* d_blk; uint4* d_src;
+  CK(cudaMalloc(&d_dev, n * 4));
+  CK(cudaMalloc(&d_blk, n * 8));
+  CK(cudaMalloc(&d_src, (size_t)n * kBlockBytes));
+  CK(cudaMemcpy(d_dev, dev, n * 4, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(d_blk, blk, n * 8, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(d_src, pages, (size_t)n * kBlockBytes, cudaMemcpyHostToDevice));
+  WriteWork w;
+  w.dev = d_dev; w.blk = reinterpret_cast<const u64*>(d_blk); w.src = d_src; w.n = (u64)n;
+  w.nodes = get_nodes(ctx, (size_t)n);
+  int rc = w.nodes ? 0 : fail(ctx, AGILE_E_CUDA, "node allocation failed");
+  if (!rc) rc = launch(ctx, w, (uint32_t)((n + kCtaThreads - 1) / kCtaThreads), ctx->stream);
+  if (!rc) rc = agile_sync(ctx, ctx->stream);
+  cudaFree(d_dev); cudaFree(d_blk); cudaFree(d_src);
+  return rc;
+}
+
 int agile_run_reads(agile_ctx* ctx, const uint64_t* keys, uint32_t tasks, uint32_t reads, uint32_t epochs,
                     int async_mode, uint64_t compute_ns, void* bufs, uint64_t* digest, uint64_t* epoch_t,
                     void* stream) {
@@ -628,9 +653,15 @@ int agile_run_reads(agile_ctx* ctx, const uint64_t* keys, uint32_t tasks, uint32
 
 int agile_run_loop(agile_ctx* ctx, uint32_t conc, uint64_t warmup_ns, uint64_t measure_ns,
                    uint64_t max_per_task, void* bufs, uint64_t* counters, void* stream) {
+  return agile_run_loop_rw(ctx, conc, warmup_ns, measure_ns, max_per_task, bufs, counters, 0, stream);
+}
+
+int agile_run_loop_rw(agile_ctx* ctx, uint32_t conc, uint64_t warmup_ns, uint64_t measure_ns,
+                      uint64_t max_per_task, void* bufs, uint64_t* counters, int write, void* stream) {
   if (!ctx || !conc || !bufs || !counters) return fail(ctx, AGILE_E_ARG, "bad loop args");
   CK(cudaSetDevice(ctx->device));
   LoopWork w;
+  w.write = write ? 1u : 0u;
   w.bufs = reinterpret_cast<uint4*>(bufs);
   w.counters = reinterpret_cast<unsigned long long*>(counters);
   w.conc = conc;

@@ -865,6 +865,107 @@ __device__ __forceinline__ bool wait_ready_lane(const DevCtx& c, u32 line, u64 k
   return tw_state(w) == ST_READY || tw_state(w) == ST_MODIFIED;
 }
 
+// async_write (gpu_api.py:192-227 -> SoftwareCache._try_write / _install_locked /
+// _allocate_locked, software_cache.py:458-523, eager=True): the 4 KiB at `src` land in the
+// block's cache line and a device write (WB_KEEP) starts at once; the line is BUSY until the
+// write is durable, then READY (complete_io, software_cache.py:533-537).  `node` is the
+// write-back barrier: the service clears it when the write completed (node->dst = 0: no copy).
+// Resident READY/MODIFIED line with no pins: CAS -> BUSY, version + 1 (readers validating the
+// old identity see the change).  Not resident: a victim is claimed exactly like a fill (evicting
+// a READY line; every line is written through, so no MODIFIED victim exists without the share
+// table).  BUSY or pinned lines, and later lanes writing a block an earlier lane of the warp
+// writes, retry (RETRY + ready_wait in the reference).  Warp-collective; no pin is held.
+__device__ void async_write_warp(const DevCtx& c, bool active, u64 key, WaitNode* node, const uint4* src,
+                                 u32 who, u32 sq_start) {
+  const u32 lane = lane_id();
+  if (active) {
+    const u32 dv = key_dev(key);
+    if (dv >= c.num_devices || key_blk(key) >= c.store_blocks[dv]) {   // _check_block
+      set_error(c, E_OUT_OF_RANGE, dv, key_blk(key));
+      active = false;
+    }
+  }
+  if (active) { node->dst = 0; node->done = 0; node->t_issue = gtimer(); }
+  __syncwarp();
+  bool want = active;
+  Spin sp;
+  while (__any_sync(FULL, want)) {
+    // same block twice in the warp: lowest lane first, the others next pass (program order)
+    const u32 grp = __match_any_sync(FULL, want ? key : ~0ull);
+    const u32 wb = __ballot_sync(FULL, want);
+    const bool go = want && (grp & lanemask_lt() & wb) == 0;
+    u32 line = NONE;
+    u64 word = 0;
+    probe_lanes(c, go, key, line, word);
+    bool own = false;
+    u32 ver = 0;
+    if (go && line != NONE) {
+      // resident: take it from READY/MODIFIED with no pins, under the set lock (victim claims
+      // open waiter lists under the same lock, so no list opened here can be clobbered)
+      const u32 set = line / c.ways;
+      if (atom_cas_acquire(&c.set_lock[set], 0u, 1u) == 0u) {
+        const u64 w = ld_relaxed(&c.tags[line]);
+        const u32 st = tw_state(w);
+        if (tw_live(w) && tw_key(w) == key && (st == ST_READY || st == ST_MODIFIED) && tw_pins(w) == 0) {
+          ver = tw_ver(w) + 1;
+          const u64 nw = tw_make(ST_BUSY, key, ver, true, 0);
+          if (atom_cas_acqrel(&c.tags[line], w, nw) == w) {
+            st_relaxed(&c.wl[line], ((u64)(ver & 0x1FFu)) << 55);   // open the waiter list
+            own = true;
+            log_ev(c, who, M_CACHE, A_HIT, key_dev(key), key_blk(key));
+            log_state(c, who, line, st, ST_BUSY, key);
+          }
+        }
+        st_release(&c.set_lock[set], 0u);
+      }
+    }
+    const u32 mb = __ballot_sync(FULL, go && line == NONE);
+    if (mb) {
+      u32 cl = NONE; u64 cw = 0, vk = ~0ull;
+      const bool wl = (mb >> lane) & 1u;
+      const int kind = c.ways <= 32 ? claim_lanes(c, wl, key, 0u, who, cl, cw, vk) : R_RETRY;
+      if (wl && kind == R_MISS) { own = true; line = cl; word = cw; ver = tw_ver(cw); }
+      if (c.ways > 32) {
+        // generic geometry: one key at a time
+        u32 m2 = mb;
+        while (m2) {
+          const int l = __ffs(m2) - 1;
+          m2 &= m2 - 1;
+          u32 l2; u64 w2, v2;
+          const int k2 = claim_key_warp(c, __shfl_sync(FULL, key, l), 0u, __shfl_sync(FULL, who, l), l2, w2, v2);
+          if (lane == (u32)l && k2 == R_MISS) { own = true; line = l2; word = w2; ver = tw_ver(w2); }
+        }
+      }
+    }
+    // owners: register the durability handle, land the bytes, start the write-back
+    bool pushed = false;
+    if (own) pushed = wl_push(c, line, ver, node);
+    u32 ob = __ballot_sync(FULL, own);
+    while (ob) {
+      const int l = __ffs(ob) - 1;
+      ob &= ob - 1;
+      const uint4* s0 = reinterpret_cast<const uint4*>(__shfl_sync(FULL, (u64)(uintptr_t)src, l));
+      uint4* d0 = reinterpret_cast<uint4*>(line_ptr(c, __shfl_sync(FULL, line, l)));
+      copy_page_warp(s0, d0);
+    }
+    __syncwarp();
+    if (__any_sync(FULL, own)) {
+      if (own) log_ev(c, who, M_CACHE, A_INSTALL, key_dev(key), key_blk(key), *reinterpret_cast<const u64*>(src));
+      const u32 nwb = __popc(__ballot_sync(FULL, own));
+      if (lane == 0) atomicAdd(&c.stats[S_WRITEBACKS], (u64)nwb);
+      if (!submit_warp(c, own, key_dev(key), key_blk(key), line, K_WB_KEEP, OP_WRITE, 0, key, who, sq_start)) {
+        if (own) want = false;
+        break;
+      }
+    }
+    if (own) {
+      if (!pushed) st_release(&node->done, 1u);   // cannot happen (the list was opened by us)
+      want = false;
+    }
+    if (__any_sync(FULL, want) && !sp.again(c, 2048, __LINE__ + 100000 * SPIN_FILE_ID)) break;
+  }
+}
+
 // ======================================================================= K3: completion service
 
 __device__ __forceinline__ void advance_head(const DevCtx& c, u32 q, u32 who) {
@@ -951,11 +1052,14 @@ __device__ u32 cq_window_pass(const DevCtx& c, u32 cq, u64& off, u32& mask, u32 
 #pragma unroll
       for (int k = 0; k < 8; ++k) v1[k] = __ldcg(src1 + lane + 32 * k);
     }
+    // dst == 0: a write's durability handle (async_write) — completion only, no copy
     uint4* d0 = reinterpret_cast<uint4*>(n0->dst);
     uint4* d1 = reinterpret_cast<uint4*>(n1->dst);
+    if (d0) {
 #pragma unroll
-    for (int k = 0; k < 8; ++k) __stcg(d0 + lane + 32 * k, v0[k]);
-    if (l1 >= 0) {
+      for (int k = 0; k < 8; ++k) __stcg(d0 + lane + 32 * k, v0[k]);
+    }
+    if (l1 >= 0 && d1) {
 #pragma unroll
       for (int k = 0; k < 8; ++k) __stcg(d1 + lane + 32 * k, v1[k]);
     }

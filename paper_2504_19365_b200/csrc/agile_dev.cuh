@@ -101,7 +101,7 @@ enum : u32 {
   A_ENQUEUE = 0, A_SQE_UPDATED, A_SQE_ISSUED, A_DOORBELL, A_SQE_RELEASE, A_HEAD,
   A_FETCH, A_COMPLETE, A_CQE_POST, A_CQE_STALL,
   A_WINDOW_RING, A_DRAIN_RING, A_STOP, A_START, A_CQE_PROCESS,
-  A_STATE, A_MISS, A_HIT, A_ATTACH, A_EVICT_RESET, A_DRAIN, A_ASYNC_READ, A_PREFETCH
+  A_STATE, A_MISS, A_HIT, A_ATTACH, A_EVICT_RESET, A_DRAIN, A_ASYNC_READ, A_PREFETCH, A_INSTALL
 };
 enum : u32 { WHO_USER = 0u << 30, WHO_SVC = 1u << 30, WHO_DEV = 2u << 30, WHO_HOST = 3u << 30 };
 

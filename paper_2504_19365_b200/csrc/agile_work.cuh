@@ -186,6 +186,7 @@ struct LoopWork {
   WaitNode* nodes;        // [conc]
   unsigned long long* counters;   // [0] completions in window, [1] window start, [2] window end
   u32 conc, ndev;
+  u32 write;              // 1: async_write of the requester's buffer (bytes idx & 0xFF) + wait
   u64 num_blocks;
   u64 warmup_ns, measure_ns;
   u64 max_per_task;
@@ -201,6 +202,10 @@ struct LoopWork {
     u32 inwin = 0;
     uint4* dst = bufs + (u64)(act ? idx : 0) * 256;
     WaitNode* node = nodes + (act ? idx : 0);
+    if (write && act) {   // buf.data[:] = bytes([idx & 0xFF]) * block_size (bench/bandwidth.py:29-30)
+      const u32 b = (idx & 0xFFu) * 0x01010101u;
+      for (u32 k = 0; k < 256; ++k) dst[k] = make_uint4(b, b, b, b);
+    }
     // requesters progress independently: a lane issues its next read as soon as its previous
     // one completed (no warp lockstep), so the in-flight population stays at `conc`
     const u32 lane = lane_id();
@@ -213,8 +218,9 @@ struct LoopWork {
       if (ib) {
         const u32 dev = (idx + (u32)j) % ndev;
         const u64 blk = (j * conc + idx) % num_blocks;
-        async_read_warp(c, issue, make_key(dev, blk), node, dst, who,
-                        sq_start + (u32)__shfl_sync(FULL, j, __ffs(ib) - 1));
+        const u32 sq = sq_start + (u32)__shfl_sync(FULL, j, __ffs(ib) - 1);
+        if (write) async_write_warp(c, issue, make_key(dev, blk), node, dst, who, sq);
+        else async_read_warp(c, issue, make_key(dev, blk), node, dst, who, sq);
         if (issue) { ++j; outst = true; }
       }
       const u32 done = poll_nodes_warp(outst, node);
@@ -236,6 +242,26 @@ struct LoopWork {
     for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
     if (lane_id() == 0 && s) atomicAdd(&counters[0], (u64)s);
     if (uidx == 0 && threadIdx.x == 0) { counters[1] = ws; counters[2] = we; }
+  }
+};
+
+// ------------------------------------------------------------------ WriteWork
+// Every thread writes one block (async_write) and waits for its write-back barrier
+// (gpu_api.py:192-227 + wait, gpu_api.py:233-248): the write path of SoftwareCache.write_block.
+struct WriteWork {
+  const u32* dev;
+  const u64* blk;
+  const uint4* src;       // [n][256] 4 KiB payloads
+  WaitNode* nodes;        // [n]
+  u64 n;
+  __device__ void run(const DevCtx& c, u32 uidx, u32 nusers) const {
+    const u64 i = (u64)uidx * kCtaThreads + threadIdx.x;
+    const bool act = i < n;
+    const u32 who = user_who(uidx);
+    const u32 sq = uidx * kCtaWarps + (threadIdx.x >> 5);
+    async_write_warp(c, act, act ? make_key(dev[i], blk[i]) : 0ull, nodes + (act ? i : 0), src + (act ? i : 0) * 256,
+                     who, sq);
+    wait_nodes_warp(c, act, nodes + (act ? i : 0));
   }
 };
 

@@ -275,17 +275,27 @@ class AgileSystem:
         return {"t_ns": int(e[-1] - e[0]), "epoch_t": e, "digest": digest.cpu().numpy().view(np.uint64),
                 "bufs": bufs}
 
-    def run_loop(self, conc, warmup_ns, measure_ns, max_per_task=0):
+    def run_loop(self, conc, warmup_ns, measure_ns, max_per_task=0, write=False):
+        """Closed-loop 4 KiB requesters (bench/bandwidth.py:20-42): reads, or writes when `write`."""
         import torch
         dev = torch.device("cuda", self.cuda_device)
         bufs = torch.empty(conc * BLOCK, dtype=torch.uint8, device=dev)
         cnt = torch.zeros(4, dtype=torch.int64, device=dev)
         st = torch.cuda.current_stream(dev).cuda_stream
-        self._check(self._lib.agile_run_loop(self._ctx, conc, int(warmup_ns), int(measure_ns), int(max_per_task),
-                                             bufs.data_ptr(), cnt.data_ptr(), st), "run_loop")
+        self._check(self._lib.agile_run_loop_rw(self._ctx, conc, int(warmup_ns), int(measure_ns), int(max_per_task),
+                                                bufs.data_ptr(), cnt.data_ptr(), 1 if write else 0, st), "run_loop")
         self.sync(st)
         c = cnt.cpu().numpy()
         return {"completions": int(c[0]), "window_ns": int(c[2] - c[1])}
+
+    def write_blocks(self, dev, blk, pages: np.ndarray) -> None:
+        """async_write + wait of whole blocks (AgileApi.async_write, gpu_api.py:192-227): each
+        lands in its cache line and is written through to the device store."""
+        dev = np.ascontiguousarray(dev, dtype=np.uint32)
+        blk = np.ascontiguousarray(blk, dtype=np.uint64)
+        pages = np.ascontiguousarray(pages, dtype=np.uint8).reshape(len(blk), BLOCK)
+        self._check(self._lib.agile_write_blocks(self._ctx, dev.ctypes.data, blk.ctypes.data, len(blk),
+                                                 pages.ctypes.data), "write_blocks")
 
     def run_gather(self, keys, tasks, epochs, gathers, async_mode, compute_ns):
         import torch

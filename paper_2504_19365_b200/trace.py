@@ -15,14 +15,14 @@ MODULES = ("nvme", "ssd", "svc", "cache", "api")
 ACTIONS = ("enqueue", "sqe_updated", "sqe_issued", "doorbell", "sqe_release", "head",
            "fetch", "complete", "cqe_post", "cqe_stall",
            "window_ring", "drain_ring", "stop", "start", "cqe_process",
-           "state", "miss", "hit", "attach", "evict_reset", "drain", "async_read", "prefetch")
+           "state", "miss", "hit", "attach", "evict_reset", "drain", "async_read", "prefetch", "install")
 STATES = ("INVALID", "BUSY", "READY", "MODIFIED")
 OPS = ("READ", "WRITE")
 ARITY = {"enqueue": 6, "sqe_updated": 2, "sqe_issued": 3, "doorbell": 4, "sqe_release": 3,
          "head": 2, "fetch": 4, "complete": 5, "cqe_post": 4, "cqe_stall": 3,
          "window_ring": 3, "drain_ring": 3, "stop": 0, "start": 1, "cqe_process": 4,
          "state": 5, "miss": 2, "hit": 2, "attach": 2, "evict_reset": 3, "drain": 2,
-         "async_read": 2, "prefetch": 2}
+         "async_read": 2, "prefetch": 2, "install": 3}
 
 RECORD = np.dtype([("t", "<u8"), ("who", "<u4"), ("modact", "<u4"), ("a", "<u8", (6,))])
 
