@@ -51,8 +51,10 @@ def _args():
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--engine-warps", type=int, default=128)
     p.add_argument("--service-warps", type=int, default=48)
-    p.add_argument("--side-ctas", type=int, default=16,
+    p.add_argument("--side-ctas", type=int, default=24,
                    help="user CTAs of the side-stream launch in the overlapped DLRM pipelines")
+    p.add_argument("--side-engine-warps", type=int, default=64)
+    p.add_argument("--side-service-warps", type=int, default=16)
     p.add_argument("--carveout", type=int, default=48,
                    help="SMs cuBLAS leaves to the side-stream launch while the MLPs run beside it")
     p.add_argument("--warm-batches", type=int, default=-1,
@@ -220,6 +222,8 @@ def main():
     cfg.engine.warps = args.engine_warps
     cfg.service.warps = args.service_warps
     cfg.service.idle_max_ns = 1600
+    cfg.engine.side_warps = args.side_engine_warps      # infra of the bounded side-stream runs
+    cfg.service.side_warps = args.side_service_warps
     cfg.debug_locks = False
     t0 = time.time()
     system = AgileSystem(cfg, device=local)

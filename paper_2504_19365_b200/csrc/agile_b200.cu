@@ -37,6 +37,8 @@ struct agile_ctx {
   // launch mode: false = split (infra grid + PDL user grid, the default), true = one fused grid
   // with roles by arrival ticket (AGILE_LAUNCH=fused: what a kernel-serialising profiler captures)
   bool fused = false;
+  // infra grid of bounded side-stream runs (engine.side_warps / service.side_warps; 0 = full)
+  uint32_t side_engine_warps = 0, side_service_warps = 0;
   // async_read WaitNodes (AgileBuf barriers) for the reads / loop / seq workloads
   void* nodes = nullptr;
   size_t nodes_cap = 0;
@@ -184,22 +186,37 @@ void load_kernels() {
   loaded = true;
 }
 
+// side: a bounded run beside other work (user_ctas given): its infra grid may be smaller
+// (engine.side_warps / service.side_warps).  Engine and service ownership is by stride over the
+// queue pairs and all their state persists in the context, so the infra size can change from run
+// to run.
 template <class W>
-int launch(agile_ctx* ctx, const W& work, uint32_t n_user_ctas, cudaStream_t st) {
+int launch(agile_ctx* ctx, const W& work, uint32_t n_user_ctas, cudaStream_t st, bool side = false) {
   if (n_user_ctas == 0) n_user_ctas = 1;
   load_kernels<W>();
   dyn_smem<W>();
+  DevCtx dc = ctx->d;
+  if (side && !ctx->fused) {
+    if (ctx->side_engine_warps) {
+      dc.engine_warps = ctx->side_engine_warps;
+      dc.n_engine_ctas = (dc.engine_warps + kCtaWarps - 1) / kCtaWarps;
+    }
+    if (ctx->side_service_warps) {
+      dc.service_warps = ctx->side_service_warps;
+      dc.n_service_ctas = (dc.service_warps + kCtaWarps - 1) / kCtaWarps;
+    }
+  }
   CK(cudaMemsetAsync(ctx->d.run, 0, sizeof(RunWords), st));
   Launch L;
   L.n_user_ctas = n_user_ctas;
   L.pad = 0;
-  const uint32_t ninfra = ctx->d.n_engine_ctas + ctx->d.n_service_ctas;
+  const uint32_t ninfra = dc.n_engine_ctas + dc.n_service_ctas;
   if (ctx->fused) {
-    agile_fused_kernel<W><<<ninfra + n_user_ctas, kCtaThreads, dyn_smem<W>(), st>>>(ctx->d, L, work);
+    agile_fused_kernel<W><<<ninfra + n_user_ctas, kCtaThreads, dyn_smem<W>(), st>>>(dc, L, work);
     CK(cudaGetLastError());
     return 0;
   }
-  agile_infra_kernel<<<ninfra, kCtaThreads, 0, st>>>(ctx->d, L);
+  agile_infra_kernel<<<ninfra, kCtaThreads, 0, st>>>(dc, L);
   CK(cudaGetLastError());
   // the user grid may start once every infra CTA executed griddepcontrol.launch_dependents
   cudaLaunchConfig_t cfg = {};
@@ -212,7 +229,7 @@ int launch(agile_ctx* ctx, const W& work, uint32_t n_user_ctas, cudaStream_t st)
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  CK(cudaLaunchKernelEx(&cfg, agile_user_kernel<W>, ctx->d, L, work));
+  CK(cudaLaunchKernelEx(&cfg, agile_user_kernel<W>, dc, L, work));
   return 0;
 }
 
@@ -330,6 +347,10 @@ int agile_create(const char* config_text, int cuda_device, agile_ctx** out) {
   d.sets_pow2 = pow2(d.num_sets) ? 1u : 0u;
   d.n_engine_ctas = (d.engine_warps + kCtaWarps - 1) / kCtaWarps;
   d.n_service_ctas = (d.service_warps + kCtaWarps - 1) / kCtaWarps;
+  ctx->side_engine_warps = (uint32_t)cfg.u("engine.side_warps", 0);
+  ctx->side_service_warps = (uint32_t)cfg.u("service.side_warps", 0);
+  if (ctx->side_service_warps)
+    ctx->side_service_warps = std::max<uint32_t>(ctx->side_service_warps, (d.num_qp + 32 * kMaxCqPerLane - 1) / (32 * kMaxCqPerLane));
   d.trace = 0;
   const uint64_t budget = cfg.u("livelock_budget", 5000000);
   d.watchdog_ns = std::max<uint64_t>(budget, 1000000) * 4000ull;   // events -> ~ns budget (>= 4 s)
@@ -737,7 +758,7 @@ int agile_embbag_ctas(agile_ctx* ctx, const int64_t* idx, const uint64_t* table_
   const uint32_t users = user_ctas ? std::min(user_ctas, full) : full;
   w.nwarps_total = users * kCtaWarps;
   w.prefetch_only = 0;
-  return launch(ctx, w, users, reinterpret_cast<cudaStream_t>(stream));
+  return launch(ctx, w, users, reinterpret_cast<cudaStream_t>(stream), user_ctas != 0);
 }
 
 int agile_embbag_prefetch(agile_ctx* ctx, const int64_t* idx, const uint64_t* table_key0, const int64_t* table_rows,
@@ -761,7 +782,7 @@ int agile_embbag_prefetch(agile_ctx* ctx, const int64_t* idx, const uint64_t* ta
   const uint32_t full = embbag_users(ctx);
   const uint32_t users = user_ctas ? std::min(user_ctas, full) : full;
   w.nwarps_total = users * kCtaWarps;
-  return launch(ctx, w, users, reinterpret_cast<cudaStream_t>(stream));
+  return launch(ctx, w, users, reinterpret_cast<cudaStream_t>(stream), user_ctas != 0);
 }
 
 // ------------------------------------------------------------------ graph drivers (K6 / K7)

@@ -1378,6 +1378,12 @@ __device__ void model_schedule_rr(const DevCtx& c, bool want, u32 dev, u32 op, u
 #endif
 constexpr int kEnginePages = AGILE_ENGINE_PAGES;
 
+// page stores of the engine: cache-streaming (evict-first in L2) so a stream of fills does not
+// evict the working sets of kernels running beside it (AGILE_FILL_STORE=__stcg to compare)
+#ifndef AGILE_FILL_STORE
+#define AGILE_FILL_STORE __stcs
+#endif
+
 template <int kPages = kEnginePages>
 __device__ void engine_main(const DevCtx& c, u32 ew) {
   const u32 lane = lane_id();
@@ -1571,7 +1577,7 @@ __device__ void engine_main(const DevCtx& c, u32 ew) {
       for (int p = 0; p < kPages; ++p) {
         if (lk[p] < 0) break;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) __stcg(tk[p] + lane + 32 * k, v[p][k]);
+        for (int k = 0; k < 8; ++k) AGILE_FILL_STORE(tk[p] + lane + 32 * k, v[p][k]);
         moved |= 1u << lk[p];
       }
       __threadfence();   // page bytes visible before the CQE release of these commands

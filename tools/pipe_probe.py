@@ -34,6 +34,9 @@ def make(cache_gib, table_gib, ew, sw):
     cfg.engine.warps = ew
     cfg.service.warps = sw
     cfg.service.idle_max_ns = 1600
+    side = os.environ.get("SIDE")
+    if side:
+        cfg.engine.side_warps, cfg.service.side_warps = (int(x) for x in side.split("/"))
     cfg.debug_locks = False
     s = AgileSystem(cfg, device=0)
     s.fill_store(0, 5, kind="f32")
