@@ -353,7 +353,9 @@ def main():
                        "parallelism": f"table-wise x{world}" if world > 1 else "single"},
             "roofline": roofline, "roofline_link": roofline_link,
             "hit_rate": 1.0 - miss_lookups / max(1, lookups_local),
-            "gpu_launches": args.steps, "clocks": clk, "setup_s": setup_s,
+            # per step: the infra grid + the PDL user grid of one agile_embbag run (1 in fused mode)
+            "gpu_launches": args.steps * (1 if os.environ.get("AGILE_LAUNCH") == "fused" else 2),
+            "clocks": clk, "setup_s": setup_s,
             "cache_warm": {"batches": warm, "seconds": warm_s}}
 
     if not args.quick:
