@@ -196,6 +196,8 @@ int launch(agile_ctx* ctx, const W& work, uint32_t n_user_ctas, cudaStream_t st,
   load_kernels<W>();
   dyn_smem<W>();
   DevCtx dc = ctx->d;
+  dc.nodes_lo = (u64)(uintptr_t)ctx->nodes;
+  dc.nodes_hi = dc.nodes_lo + (u64)ctx->nodes_cap * sizeof(WaitNode);
   if (side && !ctx->fused) {
     if (ctx->side_engine_warps) {
       dc.engine_warps = ctx->side_engine_warps;

@@ -513,7 +513,7 @@ __device__ bool ring_doorbell_until(const DevCtx& c, u32 q, u64 target, u32 who)
         st_release(&s->db_lock, 0u);
       }
       __syncwarp();
-      if (v >= target) return true;   // published past our entries: no re-read of the doorbell
+      // (re-read the doorbell below: returning on the local v raced with the engine)
       continue;
     }
     if (!sp.again(c, 256, __LINE__ + 100000 * SPIN_FILE_ID)) return false;
@@ -1017,6 +1017,10 @@ __device__ u32 cq_window_pass(const DevCtx& c, u32 cq, u64& off, u32& mask, u32 
       valid = false;
     } else {
       x = c.cmd[idx];
+      if (x.line != NONE && x.line >= c.num_lines) {
+        set_error(c, E_ILLEGAL_STATE, x.line, 0xC0000000ull | (u64)__LINE__);
+        x.line = NONE;
+      }
       const u32 os = atom_cas_acqrel(&c.sq_state[idx], SQ_ISSUED, SQ_EMPTY);
       atomicExch(&c.sq_done_v[idx], x.vidx + 1);
       cache = x.line != NONE && (x.kind == K_FILL || x.kind == K_WB_KEEP);
@@ -1045,6 +1049,16 @@ __device__ u32 cq_window_pass(const DevCtx& c, u32 cq, u64& off, u32& mask, u32 
     const uint4* src1 = reinterpret_cast<const uint4*>(line_ptr(c, __shfl_sync(FULL, x.line, s1)));
     WaitNode* n0 = reinterpret_cast<WaitNode*>(__shfl_sync(FULL, cur, l0) << 4);
     WaitNode* n1 = reinterpret_cast<WaitNode*>(__shfl_sync(FULL, cur, s1) << 4);
+    {
+      // a waiter list only ever links this run's WaitNodes: anything else is a corrupted list
+      const u64 a0 = (u64)(uintptr_t)n0, a1 = (u64)(uintptr_t)n1;
+      const bool bad = a0 < c.nodes_lo || a0 >= c.nodes_hi || a1 < c.nodes_lo || a1 >= c.nodes_hi;
+      if (bad) {
+        if (lane == 0) set_error(c, E_ILLEGAL_STATE, a0, 0xD0000000ull | (u64)__LINE__);
+        if ((int)lane == l0 || (int)lane == l1) cur = 0;
+        continue;
+      }
+    }
     uint4 v0[8], v1[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) v0[k] = __ldcg(src0 + lane + 32 * k);
@@ -1063,13 +1077,13 @@ __device__ u32 cq_window_pass(const DevCtx& c, u32 cq, u64& off, u32& mask, u32 
 #pragma unroll
       for (int k = 0; k < 8; ++k) __stcg(d1 + lane + 32 * k, v1[k]);
     }
+    __threadfence();   // every lane's page stores are performed before any barrier is released
     __syncwarp();
-    if (lane == 0) {
-      st_release(&n0->done, 1u);
-      if (l1 >= 0) st_release(&n1->done, 1u);
-    }
-    if ((int)lane == l0) cur = n0->next;
-    if ((int)lane == l1) cur = n1->next;
+    // The owning lane reads its node's link BEFORE releasing the barrier: once DONE, the
+    // requester may reuse the node at once (its next async_read re-links it into another line's
+    // list), so a link read after the release could walk into a foreign list.
+    if ((int)lane == l0) { cur = n0->next; st_release(&n0->done, 1u); }
+    if ((int)lane == l1) { cur = n1->next; st_release(&n1->done, 1u); }
   }
   if (valid && cache) {
     const u64 ot = atom_add_release(&c.tags[x.line], 1ull << ST_SHIFT);   // BUSY -> READY
@@ -1544,6 +1558,16 @@ __device__ void engine_main(const DevCtx& c, u32 ew) {
           set_error(c, E_OUT_OF_RANGE, pdev, pblk);
           pdev = 0;
           pblk = 0;
+        }
+        {
+          // the PRP of a cache command must be a line of this cache (raw commands carry
+          // caller buffers and are not checked)
+          const u64 lo = (u64)(uintptr_t)c.lines, hi = lo + ((u64)c.num_lines << kBlockShift);
+          const CmdCtx& xc = c.cmd[idx];
+          if (xc.line != NONE && (prp < lo || prp >= hi || ((prp - lo) & 4095u))) {
+            set_error(c, E_ILLEGAL_STATE, prp, 0xE0000000ull | (u64)__LINE__);
+            prp = lo;
+          }
         }
         log_ev(c, WHO_DEV | pdev, M_SSD, A_FETCH, pdev, pq, pslot, pslot);
         arrival = ld_relaxed(&c.sqw[pq].db_time) + c.model.fetch_ns;

@@ -186,6 +186,7 @@ struct DevCtx {
   u32* set_lock;
   u32* hand;
   uint8_t* lines;
+  u64 nodes_lo, nodes_hi;   // this run's WaitNode array (range checks on waiter-list walks)
   // queues
   uint4* sqe;              // num_qp * sq_depth * 4 (64 B each)
   u32* sq_state;
