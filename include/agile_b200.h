@@ -129,6 +129,15 @@ int agile_embbag_ctas(agile_ctx* ctx, const int64_t* idx, const uint64_t* table_
 int agile_embbag_host(agile_ctx* ctx, const int64_t* idx, const uint64_t* table_key0, const int64_t* table_rows,
                       float* out, uint64_t* counters, uint32_t B, uint32_t T, uint32_t L, uint32_t D,
                       uint32_t prefetch_distance);
+/* Asynchronous host-buffer entry, double-buffered (slot 0 / 1): enqueue H2D of the indices, the
+ * run and D2H of the pooled output on the slot's own stream and return.  Runs of the two slots
+ * execute in submission order (one context), while one slot's copies overlap the other's run.
+ * Host buffers should be pinned for the copies to be asynchronous; `out` and `counters` are
+ * valid after agile_embbag_host_wait(slot), which must precede the slot's next submit. */
+int agile_embbag_host_submit(agile_ctx* ctx, const int64_t* idx, const uint64_t* table_key0,
+                             const int64_t* table_rows, float* out, uint64_t* counters, uint32_t B, uint32_t T,
+                             uint32_t L, uint32_t D, uint32_t prefetch_distance, int slot);
+int agile_embbag_host_wait(agile_ctx* ctx, int slot);
 /* Batch-level prefetch (AGILE prefetch): submit every missing page of the batch into the cache
  * and complete once all fills landed; no pooling.  user_ctas (0 = all) bounds the SMs it takes
  * so the DLRM MLPs of the previous batch can run beside it. */

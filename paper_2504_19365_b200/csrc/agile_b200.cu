@@ -34,6 +34,18 @@ struct agile_ctx {
   void* d_stage = nullptr;
   size_t d_stage_bytes = 0;
   cudaStream_t stream = nullptr;
+  // double-buffered host-buffer pipeline (agile_embbag_host_submit / _wait): per slot a stream,
+  // device staging, pinned counters and the event of its run (runs are ordered across slots)
+  struct HostSlot {
+    cudaStream_t st = nullptr;
+    void* d = nullptr;
+    size_t bytes = 0;
+    uint64_t* h_cnt = nullptr;   // pinned [2]
+    uint64_t* user_cnt = nullptr;
+    cudaEvent_t ran = nullptr;
+    bool busy = false;
+  } hs[2];
+  int last_slot = -1;
   // launch mode: false = split (infra grid + PDL user grid, the default), true = one fused grid
   // with roles by arrival ticket (AGILE_LAUNCH=fused: what a kernel-serialising profiler captures)
   bool fused = false;
@@ -413,6 +425,13 @@ int agile_destroy(agile_ctx* ctx) {
   }
   if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
   if (ctx->d_stage) cudaFree(ctx->d_stage);
+  for (auto& h : ctx->hs) {
+    if (h.st) cudaStreamSynchronize(h.st);
+    if (h.d) cudaFree(h.d);
+    if (h.h_cnt) cudaFreeHost(h.h_cnt);
+    if (h.ran) cudaEventDestroy(h.ran);
+    if (h.st) cudaStreamDestroy(h.st);
+  }
   if (ctx->d.log) cudaFree(ctx->d.log);
   if (ctx->nodes) cudaFree(ctx->nodes);
   for (auto& kv : ctx->scratch) cudaFree(kv.second.first);
@@ -989,6 +1008,59 @@ int agile_spmv(agile_ctx* ctx, const int64_t* row_ptr, uint32_t V, uint64_t E, u
                                                      alpha, beta, y);
   CK(cudaGetLastError());
   return 0;
+}
+
+int agile_embbag_host_submit(agile_ctx* ctx, const int64_t* idx, const uint64_t* table_key0,
+                             const int64_t* table_rows, float* out, uint64_t* counters, uint32_t B, uint32_t T,
+                             uint32_t L, uint32_t D, uint32_t prefetch_distance, int slot) {
+  if (!ctx || !idx || !out || slot < 0 || slot > 1) return fail(ctx, AGILE_E_ARG, "bad embbag_host_submit arg");
+  CK(cudaSetDevice(ctx->device));
+  auto& h = ctx->hs[slot];
+  if (h.busy) return fail(ctx, AGILE_E_ARG, "slot busy: agile_embbag_host_wait it first");
+  if (!h.st) {
+    CK(cudaStreamCreateWithFlags(&h.st, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&h.ran, cudaEventDisableTiming));
+    CK(cudaHostAlloc(&h.h_cnt, 16, cudaHostAllocDefault));
+  }
+  const size_t n_idx = (size_t)B * T * L * 8, n_out = (size_t)B * T * D * 4, n_tab = (size_t)T * 8;
+  const size_t need = n_idx + n_out + 2 * n_tab + 16 + 256;
+  if (h.bytes < need) {
+    if (h.d) { cudaStreamSynchronize(h.st); cudaFree(h.d); }
+    CK(cudaMalloc(&h.d, need));
+    h.bytes = need;
+  }
+  uint8_t* base = reinterpret_cast<uint8_t*>(h.d);
+  int64_t* d_idx = reinterpret_cast<int64_t*>(base);
+  float* d_out = reinterpret_cast<float*>(base + n_idx);
+  uint64_t* d_key = reinterpret_cast<uint64_t*>(base + n_idx + n_out);
+  int64_t* d_rows = reinterpret_cast<int64_t*>(base + n_idx + n_out + n_tab);
+  uint64_t* d_cnt = reinterpret_cast<uint64_t*>(base + n_idx + n_out + 2 * n_tab);
+  // inputs ride in while the other slot's run is on the device; the run itself waits for the
+  // previous run (one context: runs never overlap), its output leaves while the next run starts
+  CK(cudaMemcpyAsync(d_idx, idx, n_idx, cudaMemcpyHostToDevice, h.st));
+  CK(cudaMemcpyAsync(d_key, table_key0, n_tab, cudaMemcpyHostToDevice, h.st));
+  CK(cudaMemcpyAsync(d_rows, table_rows, n_tab, cudaMemcpyHostToDevice, h.st));
+  CK(cudaMemsetAsync(d_cnt, 0, 16, h.st));
+  if (ctx->last_slot >= 0) CK(cudaStreamWaitEvent(h.st, ctx->hs[ctx->last_slot].ran, 0));
+  int rc = agile_embbag(ctx, d_idx, d_key, d_rows, d_out, d_cnt, B, T, L, D, 0, 0, prefetch_distance, h.st);
+  if (rc) return rc;
+  CK(cudaEventRecord(h.ran, h.st));
+  ctx->last_slot = slot;
+  CK(cudaMemcpyAsync(out, d_out, n_out, cudaMemcpyDeviceToHost, h.st));
+  CK(cudaMemcpyAsync(h.h_cnt, d_cnt, 16, cudaMemcpyDeviceToHost, h.st));
+  h.user_cnt = counters;
+  h.busy = true;
+  return 0;
+}
+
+int agile_embbag_host_wait(agile_ctx* ctx, int slot) {
+  if (!ctx || slot < 0 || slot > 1) return fail(ctx, AGILE_E_ARG, "bad slot");
+  auto& h = ctx->hs[slot];
+  if (!h.busy) return 0;
+  h.busy = false;
+  int rc = agile_sync(ctx, h.st);
+  if (!rc && h.user_cnt) { h.user_cnt[0] += h.h_cnt[0]; h.user_cnt[1] += h.h_cnt[1]; }
+  return rc;
 }
 
 int agile_embbag_host(agile_ctx* ctx, const int64_t* idx, const uint64_t* table_key0, const int64_t* table_rows,

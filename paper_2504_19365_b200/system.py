@@ -347,6 +347,19 @@ class AgileSystem:
                     "embbag_host")
         return out, cnt
 
+    def embbag_host_submit(self, idx: np.ndarray, table_key0: np.ndarray, table_rows: np.ndarray, D: int,
+                           out: np.ndarray, counters: np.ndarray, slot: int, prefetch_distance=0):
+        """Asynchronous host-buffer embedding-bag on staging slot 0/1 (copies of one slot overlap
+        the other's run); buffers must stay alive (and should be pinned) until embbag_host_wait."""
+        B, T, L = idx.shape
+        self._check(self._lib.agile_embbag_host_submit(self._ctx, idx.ctypes.data, table_key0.ctypes.data,
+                                                       table_rows.ctypes.data, out.ctypes.data,
+                                                       counters.ctypes.data, B, T, L, D, prefetch_distance,
+                                                       slot), "embbag_host_submit")
+
+    def embbag_host_wait(self, slot: int) -> None:
+        self._check(self._lib.agile_embbag_host_wait(self._ctx, slot), "embbag_host_wait")
+
     def bfs(self, row_ptr, V, source, col_key0, level, prefetch_distance=0, stream=None):
         """Whole BFS over a paged CSR (one fused launch per level); returns the stats dict."""
         import torch

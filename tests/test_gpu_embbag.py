@@ -134,3 +134,29 @@ def test_fused_launch_mode_matches(gpu_system, monkeypatch):
     err, cnt = _run(s, 23, 3, [3000, 700, 1200], 48, 20, 128, 0, np.random.default_rng(3))
     assert err < 1e-5
     assert cnt[0] == 48 * 3 * 20 and cnt[1] > 0
+
+
+def test_embbag_host_async_slots_match(gpu_system):
+    """The pipelined host entry (two staging slots) gives the same sums as the one-call entry."""
+    s = gpu_system(cache_lines=1024, ways=16, blocks=1 << 13, pairs=4, engine_warps=4)
+    s.fill_store(0, seed=6, kind="f32")
+    rng = np.random.default_rng(11)
+    rows = np.array([4000, 2000], dtype=np.int64)
+    k0 = np.array([0, 500], dtype=np.uint64)
+    batches = [np.stack([rng.integers(0, r, size=(24, 20)) for r in rows], axis=1).astype(np.int64) for _ in range(5)]
+    outs = [np.empty((24, 2, 128), dtype=np.float32) for _ in range(2)]
+    cnts = [np.zeros(2, dtype=np.uint64) for _ in range(2)]
+    got = []
+    for k, b in enumerate(batches):
+        slot = k % 2
+        if k >= 2:
+            s.embbag_host_wait(slot)
+            got.append(outs[slot].copy())
+        s.embbag_host_submit(b, k0, rows, 128, outs[slot], cnts[slot], slot)
+    for k in (len(batches) - 2, len(batches) - 1):
+        s.embbag_host_wait(k % 2)
+        got.append(outs[k % 2].copy())
+    for b, o in zip(batches, got):
+        ref = embbag_reference(6, 0, k0, b, 128)
+        assert np.max(np.abs(o - ref) / np.maximum(np.abs(ref), 1)) < 1e-5
+    assert int(cnts[0][0] + cnts[1][0]) == 5 * 24 * 2 * 20
