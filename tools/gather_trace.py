@@ -33,4 +33,8 @@ for mode in ("sync", "async"):
     print("  ", Counter((e[2], e[3]) for e in ev).most_common(12))
     enq = sorted(e[0] for e in ev if e[3] == "enqueue")
     print("   enqueue deciles (us):", [round(enq[int(len(enq) * q / 10)] / 1e3) for q in range(10)] if enq else None)
+    # pass boundaries: every 32 enqueues is one warp pass (32 tasks x one gather)
+    print("   pass starts (us):", [round(enq[i] / 1e3, 1) for i in range(0, min(len(enq), 32 * 40), 32)])
+    hits = sorted(e[0] for e in ev if e[3] == "hit")
+    print("   hit starts (us):", [round(hits[i] / 1e3, 1) for i in range(0, min(len(hits), 32 * 40), 32)])
     s.close()
