@@ -368,9 +368,13 @@ __device__ int claim_lanes(const DevCtx& c, bool want, u64 key, u32 pin_n, u32 w
       u32 avail = 0, ref1 = 0;
       int found = -1;
       u64 fw = 0;
-      // scan the set 8 ways per round trip (4 x 16 B loads in flight) rather than one dependent
-      // load per way: the set lock is held across this scan
-      for (u32 w0 = 0; w0 < W; w0 += 8) {
+      // the set's clock hand rides with the scan (no extra round trip after it)
+      const u32 hand = ld_relaxed(&c.hand[set]);
+      // scan the set with every 16 B load in flight at once for W <= 32 (one round trip while
+      // the set lock is held), 8 ways per round trip beyond
+#pragma unroll
+      for (u32 w0 = 0; w0 < 32; w0 += 8) {
+        if (w0 >= W) break;
         ulonglong2 q[4];
 #pragma unroll
         for (u32 j = 0; j < 4; ++j) {
@@ -406,7 +410,6 @@ __device__ int claim_lanes(const DevCtx& c, bool want, u64 key, u32 pin_n, u32 w
         }
         settled = true;
       } else {
-        const u32 hand = ld_relaxed(&c.hand[set]);
         u32 cleared = 0, nh = hand;
         const int v = clock_pick_vec(W, hand, avail, ref1, cleared, nh);
         if (v < 0) {
@@ -475,9 +478,15 @@ __device__ bool ring_doorbell_until(const DevCtx& c, u32 q, u64 target, u32 who)
   SqWords* s = &c.sqw[q];
   const u32 D = c.sq_depth;
   Spin sp;
+  bool first = true;
   while (true) {
-    const u64 db = ld_acquire(&s->db);
-    if (db >= target) return true;
+    // first pass: go straight for the lock (the caller just made entries UPDATED, so the
+    // doorbell is almost never past them yet); afterwards check the doorbell before retrying
+    if (!first) {
+      const u64 db = ld_acquire(&s->db);
+      if (db >= target) return true;
+    }
+    first = false;
     int got = 0;
     if (lane == 0) got = atom_cas_acquire(&s->db_lock, 0u, 1u) == 0u;
     got = __shfl_sync(FULL, got, 0);
