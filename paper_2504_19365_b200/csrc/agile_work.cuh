@@ -398,267 +398,15 @@ struct EmbBagWork {
     return pool++;
   }
 
-  // ---- staged path (the hot one): rows are staged in shared memory by cp.async (LDGSTS, 16 B
-  // per lane, 512 B coalesced per row, no registers held while in flight) and the bags of a warp
-  // flow through a three-stage software pipeline:
-  //   bag k+2: index load             (issued at the top of iteration k)
-  //   bag k+1: signature probe + relaxed tag confirm, overlapping the row copies of bag k
-  //   bag k  : wait copies, ONE fence, re-read the tag words (seqlock validation, checked one
-  //            iteration later so the reload latency hides under the next probe), sum rows from
-  //            shared memory in l order, then issue the copies of bag k+1 into the same stage
-  // One fence per bag orders both "tag READY seen (k+1) -> row bytes read (k+1)" and "row bytes
-  // read (k) -> tag re-read (k)".  A bag whose page changed identity while it was read is
-  // recomputed row by row (slow_bag).  No pin or lock is ever held across a wait.
-#ifndef AGILE_EMB_STAGED
-#define AGILE_EMB_STAGED 0
-#endif
-#ifndef AGILE_EMB_STAGED_SMEM
-#define AGILE_EMB_STAGED_SMEM AGILE_EMB_STAGED
-#endif
-  // user-grid register budget: 4 CTAs x 8 warps per SM (64 registers per thread)
+  // user-grid register budget: 4 CTAs x 8 warps per SM (64 registers per thread).  (A variant
+  // that staged rows in shared memory through cp.async and pipelined three bags per warp measured
+  // 20-30 % slower than this register path: its 80 KiB of stage per CTA halved the warps per SM.)
 #ifndef AGILE_EMB_MIN_CTAS
 #define AGILE_EMB_MIN_CTAS 4
 #endif
   static constexpr int kMinCtas = AGILE_EMB_MIN_CTAS;
-  static constexpr u32 kStageRows = 20;
-  static constexpr u32 kStageRowBytes = 512;                   // D <= 128 fp32
-  static constexpr u32 kStageWarpBytes = kStageRows * kStageRowBytes;
-  static constexpr u32 kDynSmem = AGILE_EMB_STAGED_SMEM ? kStageWarpBytes * kCtaWarps : 0;  // 80 KiB per CTA
 
-  // every lookup of bag `bag` resolved to a READY line with one heavy-eviction-proof pass per row
-  __device__ float4 slow_bag(const DevCtx& c, u64 key, u32 off, u32 who, u32 gw) const {
-    const u32 lane = lane_id();
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (u32 l = 0; l < L && !aborted(c); ++l) {
-      const u64 kl = __shfl_sync(FULL, key, l);
-      const u32 ol = __shfl_sync(FULL, off, l);
-      Spin s3;
-      while (true) {
-        const Req r = access_warp(c, lane == l, kl, false, who, gw, false);
-        const int kind = __shfl_sync(FULL, r.kind, l);
-        if (kind == R_HIT || kind == R_FILLING || kind == R_MISS) {
-          const u32 ln = __shfl_sync(FULL, r.line, l);
-          u64 w = 0;
-          Spin s4;
-          while (true) {
-            w = ld_acquire(&c.tags[ln]);
-            if (!tw_live(w) || tw_key(w) != kl) break;
-            if (tw_state(w) == ST_READY || tw_state(w) == ST_MODIFIED) break;
-            if (!s4.again(c, 1024, __LINE__ + 100000 * SPIN_FILE_ID)) break;
-          }
-          if (tw_live(w) && tw_key(w) == kl && tw_state(w) >= ST_READY) {
-            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (lane * 4 < D) v = __ldcg(reinterpret_cast<const float4*>(line_ptr(c, ln) + ol) + lane);
-            fence_acq_rel();
-            if (((ld_relaxed(&c.tags[ln]) ^ w) & IDENT_MASK) == 0) {
-              acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
-              break;
-            }
-          }
-        }
-        if (!s3.again(c, 1024, __LINE__ + 100000 * SPIN_FILE_ID)) break;
-      }
-    }
-    return acc;
-  }
-
-  // the miss path of one bag: lanes in `need` claim or find the in-flight fill and wait (relaxed
-  // polls) until their line is READY; returns false when the run aborts.  The caller fences
-  // before reading the bytes of a line that became READY here.
-  __device__ bool resolve_misses(const DevCtx& c, u32 need, u64 key, u32& line, u64& word, u32 who, u32 gw) const {
-    const u32 lane = lane_id();
-    Spin sp;
-    while (need) {
-      const bool nm = (need >> lane) & 1u;
-      const Req r = access_warp(c, nm, key, false, who, gw, false);
-      const bool got = nm && (r.kind == R_HIT || r.kind == R_FILLING || r.kind == R_MISS);
-      if (got) { line = r.line; word = r.word; }
-      u32 wp = __ballot_sync(FULL, got);
-      u32 done = 0;
-      Spin s2;
-      while (wp) {
-        bool rd = false, gone = false;
-        if ((wp >> lane) & 1u) {
-          const u64 w = ld_relaxed(&c.tags[line]);
-          if (!tw_live(w) || tw_key(w) != key) gone = true;
-          else if (tw_state(w) == ST_READY || tw_state(w) == ST_MODIFIED) { word = w; rd = true; }
-        }
-        done |= __ballot_sync(FULL, rd);
-        wp &= ~__ballot_sync(FULL, rd || gone);
-        if (wp && !s2.again(c, 1024, __LINE__ + 100000 * SPIN_FILE_ID)) break;
-      }
-      need &= ~done;
-      if (aborted(c)) return false;
-      if (need && !done && !sp.again(c, 1024, __LINE__ + 100000 * SPIN_FILE_ID)) return false;
-    }
-    return true;
-  }
-
-  __device__ __forceinline__ static void cp_async16(void* smem, const void* g) {
-    const u32 sa = (u32)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(sa), "l"(g) : "memory");
-  }
-
-  // copies of the L rows of a bag into the warp's stage; ru = (line << 8) | (off >> 4), the row's
-  // address in 16 B units from the cache base (32 bits: caches up to 64 GiB)
-  __device__ __forceinline__ void issue_rows(const DevCtx& c, uint4* stage, u32 ru) const {
-    const u32 lane = lane_id();
-    const bool col = lane * 4 < D;
-    const uint4* base = reinterpret_cast<const uint4*>(c.lines) + lane;
-#pragma unroll 4
-    for (u32 l = 0; l < L; ++l) {
-      const u32 r = __shfl_sync(FULL, ru, l);
-      if (col) cp_async16(stage + l * 32 + lane, base + r);
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  }
-
-  // next bag in processing order (sync: straight from the counter; async: the ring of bags
-  // prefetched `depth` ahead)
-  struct BagSeq {
-    u32 ring[kMaxPd];
-    u32 head, count, pool, left, pass;
-  };
-  __device__ __forceinline__ u32 next_bag(const DevCtx& c, BagSeq& q, u32 depth, bool lact, u32 who, u32 gw) const {
-    const u32 nbags = B * T;
-    if (!depth) return grab(c, q.pool, q.left);
-    if (!q.count) return nbags;
-    const u32 bag = q.ring[q.head];
-    q.head = (q.head + 1) % kMaxPd;
-    --q.count;
-    const u32 nb = grab(c, q.pool, q.left);
-    if (nb < nbags) {
-      u64 key = 0; u32 off = 0;
-      const bool a = bag_keys(nb, lact, key, off);
-      prefetch_warp(c, a, key, who, gw + (++q.pass), true);
-      q.ring[(q.head + q.count) % kMaxPd] = nb;
-      ++q.count;
-    }
-    return bag;
-  }
-
-  __device__ void run_staged(const DevCtx& c, u32 uidx) const {
-    extern __shared__ __align__(16) uint4 agile_dyn_smem[];
-    const u32 lane = lane_id();
-    const u32 wic = threadIdx.x >> 5;
-    const u32 gw = uidx * kCtaWarps + wic;
-    const u32 nbags = B * T;
-    const u32 who = user_who(uidx);
-    const bool lact = lane < L;
-    const u32 depth = pd > kMaxPd ? kMaxPd : pd;
-    uint4* stage = agile_dyn_smem + (u64)wic * (kStageWarpBytes / 16);
-    const float4* stagef = reinterpret_cast<const float4*>(stage);
-    u32 misses_local = 0, lookups_local = 0;
-    BagSeq q;
-    q.head = q.count = q.pool = q.left = q.pass = 0;
-    for (u32 k = 0; k < depth; ++k) {
-      const u32 nb = grab(c, q.pool, q.left);
-      if (nb >= nbags) break;
-      u64 key = 0; u32 off = 0;
-      const bool a = bag_keys(nb, lact, key, off);
-      prefetch_warp(c, a, key, who, gw + k, true);
-      q.ring[(q.head + q.count) % kMaxPd] = nb;
-      ++q.count;
-    }
-    // stage k (rows in flight), stage k+1 (keys known), pending k-1 (sum done, validation due)
-    u32 b0 = nbags, b1 = nbags, bp = nbags;
-    u64 key0 = 0, key1 = 0, word0 = 0, wordp = 0, rvp = 0, keyp = 0;   // key1/off1/a1: set in (B)
-    u32 off0 = 0, off1 = 0, line0 = NONE, offp = 0;
-    bool a0 = false, a1 = false, ap = false;
-    float4 accp = make_float4(0.f, 0.f, 0.f, 0.f);
-    b1 = next_bag(c, q, depth, lact, who, gw);
-    long long raw1 = b1 < nbags ? bag_raw(b1, lact) : 0ll;
-    u32 iter = 0;
-    bool ok = true, fenced = false;
-    while (true) {
-      // (A) the bag after next: index load (consumed one iteration later)
-      u32 b2 = nbags;
-      long long raw2 = 0;
-      if (b1 < nbags) {
-        b2 = next_bag(c, q, depth, lact, who, gw);
-        if (b2 < nbags) raw2 = bag_raw(b2, lact);
-      }
-      // (B) probe bag k+1 (relaxed confirm; the fence below orders it before its row reads)
-      u32 line1 = NONE; u64 word1 = 0;
-      bool ready1 = false;
-      if (b1 < nbags) {
-        a1 = bag_key_of(b1, lact, raw1, key1, off1);
-        probe_lanes<false>(c, a1, key1, line1, word1);
-        ready1 = a1 && line1 != NONE && (tw_state(word1) == ST_READY || tw_state(word1) == ST_MODIFIED);
-        if (ready1 && !tw_ref(word1)) atomicOr(&c.tags[line1], REF_BIT);   // on_hit
-      }
-      // (C) bag k: copies landed -> one fence -> tag re-read (checked next iteration) -> sum.
-      //     The fence also waits for this warp's earlier stores, so the output store of bag k-1
-      //     comes after it (its acknowledgement then hides under the next probe).
-      u64 rvc = 0;
-      float4 accc = make_float4(0.f, 0.f, 0.f, 0.f);
-      const bool had0 = b0 < nbags;
-      if (had0) {
-        asm volatile("cp.async.wait_all;" ::: "memory");
-        hit_fence();
-        fenced = true;
-        rvc = a0 ? ld_relaxed(&c.tags[line0]) : 0ull;
-        if (lane * 4 < D) {
-          // packed f32x2 adds (FADD2), rows in l order: bit-identical to scalar adds
-          u64 lo = 0, hi = 0;
-#pragma unroll 4
-          for (u32 l = 0; l < L; ++l) {
-            const ulonglong2 v = reinterpret_cast<const ulonglong2*>(stagef)[l * 32 + lane];
-            asm("add.rn.f32x2 %0, %0, %1;" : "+l"(lo) : "l"(v.x));
-            asm("add.rn.f32x2 %0, %0, %1;" : "+l"(hi) : "l"(v.y));
-          }
-          accc = make_float4(__uint_as_float((u32)lo), __uint_as_float((u32)(lo >> 32)),
-                             __uint_as_float((u32)hi), __uint_as_float((u32)(hi >> 32)));
-        }
-      }
-      // (P) bag k-1: validation (its tag re-read was issued last iteration) and its output
-      if (bp < nbags) {
-        const bool bad = ap && ((rvp ^ wordp) & IDENT_MASK) != 0;
-        if (__any_sync(FULL, bad)) accp = slow_bag(c, keyp, offp, who, gw);
-        const u32 bb = bp / T, tt = bp % T;
-        if (lane * 4 < D) reinterpret_cast<float4*>(out + (u64)bb * out_b_stride + (u64)tt * out_t_stride)[lane] = accp;
-        lookups_local += L;
-        bp = nbags;
-      }
-      if (had0) {
-        bp = b0; ap = a0; wordp = word0; keyp = key0; offp = off0; accp = accc; rvp = rvc;
-        b0 = nbags;
-      }
-      if (b1 >= nbags) {
-        if (bp < nbags) continue;   // flush the pending bag
-        break;
-      }
-      // (B') misses of bag k+1: claim / attach and wait for READY (nothing held meanwhile)
-      const u32 need = __ballot_sync(FULL, a1 && !ready1);
-      if (need) {
-        misses_local += __popc(need);
-        if (!resolve_misses(c, need, key1, line1, word1, who, gw)) { ok = false; break; }
-        hit_fence();   // lines that became READY under relaxed polls
-        fenced = true;
-      }
-      // (C') issue bag k+1's copies into the stage (each lane overwrites only its own slots)
-      if (!fenced) hit_fence();   // first bag: no stage-k fence ran since the probe
-      fenced = false;
-      const u32 ru = a1 ? (line1 << 8) | (off1 >> 4) : 0u;
-      issue_rows(c, stage, ru);
-      b0 = b1; a0 = a1; key0 = key1; off0 = off1; line0 = line1; word0 = word1;
-      b1 = b2; raw1 = raw2;
-      if ((++iter & 15u) == 0 && aborted(c)) { ok = false; break; }
-    }
-    if (!ok) asm volatile("cp.async.wait_all;" ::: "memory");
-    if (lane == 0) {
-      atomicAdd(&lookups_miss[0], (u64)lookups_local);
-      atomicAdd(&lookups_miss[1], (u64)misses_local);
-    }
-  }
-
-  __device__ void run(const DevCtx& c, u32 uidx, u32 nusers) const {
-    if (AGILE_EMB_STAGED && !prefetch_only && L <= kStageRows && D * 4 <= kStageRowBytes && c.num_lines <= (1u << 24)) {
-      run_staged(c, uidx);
-      return;
-    }
-    run_direct(c, uidx, nusers);
-  }
+  __device__ void run(const DevCtx& c, u32 uidx, u32 nusers) const { run_direct(c, uidx, nusers); }
 
   __device__ void run_direct(const DevCtx& c, u32 uidx, u32 nusers) const {
     const u32 lane = lane_id();
