@@ -386,7 +386,6 @@ int agile_create(const char* config_text, int cuda_device, agile_ctx** out) {
   if ((rc = dalloc(ctx, &d.wl, lines))) return rc;
   if ((rc = dalloc(ctx, &d.set_lock, d.num_sets))) return rc;
   if ((rc = dalloc(ctx, &d.hand, d.num_sets))) return rc;
-  if ((rc = dalloc(ctx, &d.refm, d.num_sets))) return rc;
   if ((rc = dalloc(ctx, &d.lines, lines * kBlockBytes))) return rc;
   const size_t nsq = (size_t)d.num_qp * d.sq_depth;
   if ((rc = dalloc(ctx, &d.sqe, nsq * 4))) return rc;
@@ -541,7 +540,6 @@ int agile_reset(agile_ctx* ctx, int flags) {
     CK(cudaMemset(d.sig, 0, (size_t)d.num_lines * 2));
     CK(cudaMemset(d.wl, 0, (size_t)d.num_lines * 8));
     CK(cudaMemset(d.hand, 0, (size_t)d.num_sets * 4));
-    CK(cudaMemset(d.refm, 0, (size_t)d.num_sets * 4));
     CK(cudaMemset(d.set_lock, 0, (size_t)d.num_sets * 4));
   }
   if (flags & 2) {

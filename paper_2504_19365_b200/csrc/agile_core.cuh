@@ -40,20 +40,6 @@ __device__ __forceinline__ u32 nth_set_bit(u32 m, u32 n) {
 
 // ======================================================================= K1: cache
 
-// Clock reference bits (ClockPolicy.ref, software_cache.py:96-126).  W <= 32: bit w of the set's
-// word refm[set] — a sweep clears every way it passed with ONE atomic (with the bit in each tag
-// word, a claim in a hot set issued up to W-1 atomics and the set lock's release fence waited for
-// all of them).  W > 32 (fully associative parity mode): REF_BIT of the tag word.
-// on_hit: `seen` is the set's mask as loaded with the probe (0 = unknown: set it regardless).
-__device__ __forceinline__ void ref_on_hit(const DevCtx& c, u32 line, u64 word, u32 seen) {
-  if (c.ways <= 32) {
-    const u32 set = line / c.ways, w = line - set * c.ways;
-    if (!((seen >> w) & 1u)) atomicOr(&c.refm[set], 1u << w);
-  } else if (!tw_ref(word)) {
-    atomicOr(&c.tags[line], REF_BIT);
-  }
-}
-
 // Probe one key (warp-uniform) across all ways of its set.  Relaxed loads; callers that act
 // on the result re-validate (seqlock) or hold the set lock.
 __device__ __forceinline__ bool probe_key_warp(const DevCtx& c, u64 key, u32& line, u64& word) {
@@ -97,11 +83,9 @@ __device__ __forceinline__ u32 sig_match8(uint4 v, u32 pat) {
 // kAcquire = false: the confirming tag load is relaxed; the caller issues a fence before it reads
 // the line's bytes (one fence then covers every key of the warp).
 template <bool kAcquire = true>
-__device__ __forceinline__ void probe_lanes(const DevCtx& c, bool active, u64 key, u32& line, u64& word,
-                                            u32* refm_seen = nullptr) {
+__device__ __forceinline__ void probe_lanes(const DevCtx& c, bool active, u64 key, u32& line, u64& word) {
   line = NONE;
   word = 0;
-  if (refm_seen) *refm_seen = 0;
   const u32 W = c.ways;
   if (W <= 32 && (W & 7u) == 0) {
     // lane-per-key signature probe: each active lane scans its own set's W signatures (2W bytes,
@@ -111,9 +95,7 @@ __device__ __forceinline__ void probe_lanes(const DevCtx& c, bool active, u64 ke
     // that misses in that window takes the miss path, which re-probes the full tags under the
     // set lock, so in-flight de-duplication is unaffected.
     if (active) {
-      const u32 set = set_of(c, key);
-      const u64 base = (u64)set * W;
-      if (refm_seen) *refm_seen = __ldcg(c.refm + set);   // rides with the signature loads
+      const u64 base = (u64)set_of(c, key) * W;
       const uint4* sp = reinterpret_cast<const uint4*>(c.sig + base);
       const u32 pat = sig16(key) * 0x10001u;
       uint4 v[4];
@@ -294,7 +276,7 @@ __device__ int claim_key_warp(const DevCtx& c, u64 key, u32 pin_n, u32 who, u32&
         if (!w) {
           kind = R_RETRY;
         } else {
-          if (kind == R_HIT) ref_on_hit(c, l, w, 0u);
+          if (kind == R_HIT && !tw_ref(w)) atomicOr(&c.tags[l], REF_BIT);
           kind = tw_state(w) == ST_BUSY ? R_FILLING : R_HIT;
         }
       }
@@ -313,7 +295,7 @@ __device__ int claim_key_warp(const DevCtx& c, u64 key, u32 pin_n, u32 who, u32&
       u64 tw = 0;
       if (lane < W) tw = ld_relaxed(&c.tags[base + lane]);
       const u32 avail = __ballot_sync(FULL, lane < W && tw_state(tw) != ST_BUSY && tw_pins(tw) == 0);
-      const u32 ref1 = ld_relaxed(&c.refm[set]) & ((W == 32) ? FULL : ((1u << W) - 1u));
+      const u32 ref1 = __ballot_sync(FULL, lane < W && tw_ref(tw));
       v = clock_pick_vec(W, hand, avail, ref1, cleared, new_hand);
       if (v >= 0) old = __shfl_sync(FULL, tw, v);
     } else {
@@ -337,10 +319,7 @@ __device__ int claim_key_warp(const DevCtx& c, u64 key, u32 pin_n, u32 who, u32&
     }
     prev = __shfl_sync(FULL, prev, 0);
     if (prev != old) continue;   // a hitter touched ref/pins: re-evaluate
-    if (W <= 32 && lane == 0) {
-      atomicAnd(&c.refm[set], ~cleared);   // swept ways (one atomic for the set)
-      atomicOr(&c.refm[set], 1u << v);     // on_insert (software_cache.py:106-107)
-    }
+    if (W <= 32 && lane < W && ((cleared >> lane) & 1u)) atomicAnd(&c.tags[base + lane], ~REF_BIT);
     if (lane == 0) {
       c.sig[base + v] = (unsigned short)sig16(key);   // probe hint (the tag word decides)
       st_relaxed(&c.hand[set], new_hand);
@@ -391,7 +370,6 @@ __device__ int claim_lanes(const DevCtx& c, bool want, u64 key, u32 pin_n, u32 w
       u64 fw = 0;
       // the set's clock hand rides with the scan (no extra round trip after it)
       const u32 hand = ld_relaxed(&c.hand[set]);
-      const u32 rmask = ld_relaxed(&c.refm[set]);
       // scan the set with every 16 B load in flight at once for W <= 32 (one round trip while
       // the set lock is held), 8 ways per round trip beyond
 #pragma unroll
@@ -415,16 +393,16 @@ __device__ int claim_lanes(const DevCtx& c, bool want, u64 key, u32 pin_n, u32 w
           if (w < W) {
             if (tw_live(t) && tw_key(t) == key) { found = (int)w; fw = t; }
             if (tw_state(t) != ST_BUSY && tw_pins(t) == 0) avail |= 1u << w;
+            if (tw_ref(t)) ref1 |= 1u << w;
           }
         }
       }
-      ref1 = rmask & ((W == 32) ? FULL : ((1u << W) - 1u));
       if (found >= 0) {
         u64 w2 = fw;
         if (pin_n) w2 = pin_line(c, (u32)(base + found), key, pin_n);
         if (w2) {
           kind = tw_state(w2) == ST_BUSY ? R_FILLING : R_HIT;
-          if (kind == R_HIT) ref_on_hit(c, (u32)(base + found), w2, rmask);
+          if (kind == R_HIT && !tw_ref(w2)) atomicOr(&c.tags[base + found], REF_BIT);
           line = (u32)(base + found);
           word = w2;
         } else {
@@ -444,8 +422,7 @@ __device__ int claim_lanes(const DevCtx& c, bool want, u64 key, u32 pin_n, u32 w
             st_relaxed(&c.wl[base + v], ((u64)((tw_ver(old) + 1) & 0x1FFu)) << 55);   // open the waiter list
             if (atom_cas_acqrel(&c.tags[base + v], old, nw) == old) {
               c.sig[base + v] = (unsigned short)sig16(key);   // probe hint (the tag word decides)
-              atomicAnd(&c.refm[set], ~cleared);   // swept ways: one atomic for the set
-              atomicOr(&c.refm[set], 1u << v);     // on_insert (software_cache.py:106-107)
+              for (u32 m = cleared; m; m &= m - 1) atomicAnd(&c.tags[base + (__ffs(m) - 1)], ~REF_BIT);
               st_relaxed(&c.hand[set], nh);
               const u32 ost = tw_state(old);
               if (ost == ST_READY || ost == ST_MODIFIED) {
@@ -680,8 +657,8 @@ __device__ Req access_warp(const DevCtx& c, bool active, u64 key, bool pin, u32 
   const u32 gsize = __popc(grp);
   const u32 lead_lane = grp ? (u32)(__ffs(grp) - 1) : lane;
   // lock-free probe for every leader
-  u32 l; u64 w; u32 rm;
-  probe_lanes(c, leader, key, l, w, &rm);
+  u32 l; u64 w;
+  probe_lanes(c, leader, key, l, w);
   bool resolved = false;
   if (leader && l != NONE) {
     u64 pw = w;
@@ -690,7 +667,7 @@ __device__ Req access_warp(const DevCtx& c, bool active, u64 key, bool pin, u32 
       r.line = l;
       r.word = pw;
       r.kind = tw_state(pw) == ST_BUSY ? R_FILLING : R_HIT;
-      if (r.kind == R_HIT) ref_on_hit(c, l, pw, rm);   // on_hit
+      if (r.kind == R_HIT && !tw_ref(pw)) atomicOr(&c.tags[l], REF_BIT);   // on_hit
       resolved = true;
     }
   }
@@ -943,7 +920,6 @@ __device__ void async_write_warp(const DevCtx& c, bool active, u64 key, WaitNode
           const u64 nw = tw_make(ST_BUSY, key, ver, true, 0);
           if (atom_cas_acqrel(&c.tags[line], w, nw) == w) {
             st_relaxed(&c.wl[line], ((u64)(ver & 0x1FFu)) << 55);   // open the waiter list
-            ref_on_hit(c, line, nw, 0u);
             own = true;
             log_ev(c, who, M_CACHE, A_HIT, key_dev(key), key_blk(key));
             log_state(c, who, line, st, ST_BUSY, key);

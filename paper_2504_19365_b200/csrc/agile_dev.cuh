@@ -181,7 +181,6 @@ struct DevCtx {
   u64 watchdog_ns;
   // cache
   u64* tags;
-  u32* refm;                // W <= 32: clock reference bits of set s (bit w = way w)
   unsigned short* sig;      // per-line 16-bit key signature: probe hint, the tag word decides
   u64* wl;                 // per-line async_read waiter stack (agile_core.cuh WaitNode)
   u32* set_lock;

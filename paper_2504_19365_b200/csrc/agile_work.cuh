@@ -495,10 +495,9 @@ struct EmbBagWork {
         // 1. resolve every lookup to a READY line: batched ballot probe, then the miss path
         //    (claim or find the in-flight fill, wait for it) for the rest
         u32 line; u64 word;
-        u32 rm;
-        probe_lanes<false>(c, a, key, line, word, &rm);
+        probe_lanes<false>(c, a, key, line, word);
         bool ready = a && line != NONE && (tw_state(word) == ST_READY || tw_state(word) == ST_MODIFIED);
-        if (ready) ref_on_hit(c, line, word, rm);   // on_hit
+        if (ready && !tw_ref(word)) atomicOr(&c.tags[line], REF_BIT);   // on_hit
         u32 need = __ballot_sync(FULL, a && !ready);
         if (need && first) misses_local += __popc(need);
         const bool waited = need != 0;
@@ -635,10 +634,9 @@ __device__ bool resolve_pages_warp(const DevCtx& c, bool act, u64 key, PageRegs&
   const bool leader = need && (grp & lanemask_lt()) == 0;
   u32 l = NONE;
   u64 w = 0;
-  u32 rm;
-  probe_lanes(c, leader, key, l, w, &rm);
+  probe_lanes(c, leader, key, l, w);
   const bool ready = leader && l != NONE && tw_state(w) >= ST_READY;
-  if (ready) ref_on_hit(c, l, w, rm);   // on_hit (software_cache.py:124-126)
+  if (ready && !tw_ref(w)) atomicOr(&c.tags[l], REF_BIT);   // on_hit (software_cache.py:124-126)
   u32 pend = __ballot_sync(FULL, leader && !ready);
   misses += __popc(pend);
   Spin sp;
