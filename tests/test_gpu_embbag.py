@@ -160,3 +160,30 @@ def test_embbag_host_async_slots_match(gpu_system):
         ref = embbag_reference(6, 0, k0, b, 128)
         assert np.max(np.abs(o - ref) / np.maximum(np.abs(ref), 1)) < 1e-5
     assert int(cnts[0][0] + cnts[1][0]) == 5 * 24 * 2 * 20
+
+
+def test_side_infra_size_for_bounded_runs():
+    """engine.side_warps / service.side_warps: bounded runs use a smaller infra grid (different
+    queue ownership strides) interleaved with full runs on the same context; sums and counters
+    stay exact."""
+    from paper_2504_19365_b200 import AgileSystem
+    from conftest import small_config
+    cfg = small_config(cache_lines=256, ways=16, blocks=1 << 13, pairs=16, engine_warps=16, warps=8)
+    cfg.engine.side_warps, cfg.service.side_warps = 4, 2
+    with AgileSystem(cfg, device=0) as s2:
+        s2.fill_store(0, seed=31, kind="f32")
+        rng = np.random.default_rng(4)
+        rows = [3000, 1200]
+        k0 = np.array([0, 375], dtype=np.uint64)
+        dev = torch.device("cuda", 0)
+        for user_ctas in (2, 0, 3, 0):
+            idx = np.stack([rng.integers(0, r, size=(64, 20)) for r in rows], axis=1).astype(np.int64)
+            out = torch.full((64, 2, 128), float("nan"), dtype=torch.float32, device=dev)
+            cnt = torch.zeros(2, dtype=torch.int64, device=dev)
+            s2.embbag(torch.from_numpy(idx).to(dev), torch.from_numpy(k0.view(np.int64)).to(dev),
+                      torch.tensor(rows, dtype=torch.int64, device=dev), out, cnt, prefetch_distance=0,
+                      user_ctas=user_ctas)
+            s2.sync(torch.cuda.current_stream(dev).cuda_stream)
+            ref = embbag_reference(31, 0, k0, idx, 128)
+            assert np.max(np.abs(out.cpu().numpy() - ref) / np.maximum(np.abs(ref), 1.0)) < 1e-5
+            assert int(cnt.cpu()[0]) == 64 * 2 * 20
