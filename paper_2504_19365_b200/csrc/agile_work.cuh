@@ -274,14 +274,33 @@ struct GatherWork {
   u64* epoch_t;
   u32 tasks, epochs, gathers, async_mode;
   u64 compute_ns;
-  __device__ void prefetch_epoch(const DevCtx& c, bool act, u32 task, u32 e, u32 who, u32 sq_start) const {
-    for (u32 g = 0; g < gathers; ++g) {
+  // A CTA's tasks sit in its first ntw warps (one task per lane, warp_size=32 as in
+  // run_workload(..., warp_size=32)); its other warps would idle.  Every warp of the CTA therefore
+  // takes the same 32 tasks (warp w: tasks of warp w % ntw) and a 1/nh share of each task's gather
+  // list (gathers g with g % nh == w / ntw, nh = 8 / ntw).  Each task still prefetches all its
+  // blocks before it reads them and the epoch barrier still separates the epochs; only the
+  // per-task command stream is issued by nh warps at once instead of one (a warp pass of 32
+  // misses costs ~30 µs of dependent round trips on the GPU, the reference models 350 ns).
+  __device__ __forceinline__ void share(u32 uidx, u32& task, bool& act, u32& g0, u32& gstep) const {
+    const u32 wid = threadIdx.x >> 5;
+    const u32 cta_tasks = min(tasks - min(tasks, uidx * kCtaThreads), (u32)kCtaThreads);
+    const u32 ntw = max(1u, (cta_tasks + 31) / 32);
+    const u32 nh = max(1u, (u32)kCtaWarps / ntw);
+    task = uidx * kCtaThreads + (wid % ntw) * 32 + lane_id();
+    act = task < tasks && wid < ntw * nh;
+    g0 = wid / ntw;
+    gstep = nh;
+  }
+  __device__ void prefetch_epoch(const DevCtx& c, bool act, u32 task, u32 e, u32 who, u32 sq_start, u32 g0,
+                                 u32 gstep) const {
+    for (u32 g = g0; g < gathers; g += gstep) {
       const u64 key = act ? keys[((u64)task * epochs + e) * gathers + g] : 0ull;
       prefetch_warp(c, act, key, who, sq_start + g + e * gathers, false);
     }
   }
-  __device__ void get_epoch(const DevCtx& c, bool act, u32 task, u32 e, u32 who, u32 sq_start) const {
-    for (u32 g = 0; g < gathers; ++g) {
+  __device__ void get_epoch(const DevCtx& c, bool act, u32 task, u32 e, u32 who, u32 sq_start, u32 g0,
+                            u32 gstep) const {
+    for (u32 g = g0; g < gathers; g += gstep) {
       const u64 key = act ? keys[((u64)task * epochs + e) * gathers + g] : 0ull;
       // array_get = read_range loop (software_cache.py:212-219): access, wait READY, read.  The
       // lane pins only its own line, and only after its claim succeeded (no hold-and-wait).
@@ -314,16 +333,17 @@ struct GatherWork {
     }
   }
   __device__ void run(const DevCtx& c, u32 uidx, u32 nusers) const {
-    const u32 task = uidx * kCtaThreads + threadIdx.x;
-    const bool act = task < tasks;
+    u32 task, g0, gstep;
+    bool act;
+    share(uidx, task, act, g0, gstep);
     const u32 who = user_who(uidx);
-    const u32 sq_start = task / 32;   // thread_idx % nsq start SQ per warp (nvme_queue.py:91-93)
+    const u32 sq_start = task / 32 + g0;   // thread_idx % nsq start SQ per warp (nvme_queue.py:91-93)
     if (uidx == 0 && threadIdx.x == 0) epoch_t[0] = gtimer();
-    if (async_mode) prefetch_epoch(c, act, task, 0, who, sq_start);
+    if (async_mode) prefetch_epoch(c, act, task, 0, who, sq_start, g0, gstep);
     for (u32 e = 0; e < epochs; ++e) {
-      if (!async_mode) prefetch_epoch(c, act, task, e, who, sq_start);
-      else if (e + 1 < epochs) prefetch_epoch(c, act, task, e + 1, who, sq_start);
-      get_epoch(c, act, task, e, who, sq_start);
+      if (!async_mode) prefetch_epoch(c, act, task, e, who, sq_start, g0, gstep);
+      else if (e + 1 < epochs) prefetch_epoch(c, act, task, e + 1, who, sq_start, g0, gstep);
+      get_epoch(c, act, task, e, who, sq_start, g0, gstep);
       if (!user_grid_barrier(c, nusers)) return;
       compute_spin(compute_ns);
     }

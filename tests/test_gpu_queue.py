@@ -80,3 +80,21 @@ def test_async_read_digest_matches_pages_multi_device(gpu_system):
             for i in range(R):
                 exp[t] ^= page_words(1, int(dev[e, t, i]), [int(blk[e, t, i])])[0, 0]
     assert np.array_equal(r["digest"], exp)
+
+
+@pytest.mark.parametrize("tasks,async_mode", [(32, False), (32, True), (300, True)])
+def test_gather_values_match_pages(gpu_system, tasks, async_mode):
+    """Gather sweep driver (bench/sweeps.py:39-77): every array_get returns element 0 of its block,
+    whichever warp of the CTA issued the task's prefetch / read (the CTA's idle warps share each
+    task's gather list)."""
+    from oracle.pages import page_bytes
+    s = gpu_system(cache_lines=2048, ways=32, blocks=1 << 14, pairs=8, sq_depth=64, cq_depth=64,
+                   emulation="model", engine_warps=8, warps=4)
+    s.fill_store(0, seed=9)
+    rng = np.random.default_rng(tasks + int(async_mode))
+    E, G = 3, 16
+    blk = rng.choice(1 << 14, size=tasks * E * G, replace=False).reshape(tasks, E, G)
+    keys = make_key(np.zeros_like(blk), blk)
+    r = s.run_gather(keys, tasks, E, G, async_mode, 20000)
+    exp = page_bytes(9, 0, blk.reshape(-1))[:, :4].copy().view(np.uint32).reshape(-1)
+    assert np.array_equal(r["values"].reshape(-1), exp)
