@@ -109,53 +109,57 @@ struct ReadsWork {
   u32 tasks, reads, epochs, async_mode;
   u64 compute_ns;
   static constexpr int MAXR = 64;
-  // A warp's tasks issue their reads as one flat list of (task, i) requests, 32 per pass: with
-  // fewer than 32 active tasks in the warp (the reference's 16-task default) every pass still
-  // fills the warp, so the issue takes ceil(n * reads / 32) access passes instead of `reads`.
-  // Each request keeps its task's node and buffer; ordering within a task is unchanged.
-  __device__ void issue(const DevCtx& c, u32 task, bool act, u32 e, u32 set, u32 who, u32 sq_start) const {
-    const u32 lane = lane_id();
-    const u32 nact = __popc(__ballot_sync(FULL, act));   // active tasks are the warp's low lanes
-    const u32 base_task = task - lane;
-    const u32 total = nact * reads;
-    for (u32 k = 0; k * 32 < total; ++k) {
-      const u32 f = k * 32 + lane;
+  // A CTA's tasks issue their reads as one flat list of (task, i) requests spread over all of
+  // the CTA's threads (request f = k * 256 + thread): with fewer than 256 tasks (the reference's
+  // 16-task default fills half a warp) the otherwise idle warps issue in parallel, so an epoch's
+  // issue takes ceil(tasks_in_cta * reads / 256) access passes per warp instead of `reads`.
+  // Each request keeps its task's node and buffer; the epoch barrier still separates the epochs.
+  __device__ __forceinline__ u32 cta_tasks(u32 uidx) const {
+    return min(tasks - min(tasks, uidx * kCtaThreads), (u32)kCtaThreads);
+  }
+  __device__ void issue(const DevCtx& c, u32 uidx, u32 e, u32 set, u32 who, u32 sq_start) const {
+    const u32 total = cta_tasks(uidx) * reads;
+    for (u32 k = 0; k * kCtaThreads < total; ++k) {
+      const u32 f = k * kCtaThreads + threadIdx.x;
       const bool a = f < total;
-      const u32 t = base_task + (a ? f / reads : 0), i = a ? f % reads : 0;
+      const u32 t = uidx * kCtaThreads + (a ? f / reads : 0), i = a ? f % reads : 0;
       const u64 key = a ? keys[((u64)e * tasks + t) * reads + i] : 0ull;
       const u64 slot = ((u64)t * 2 + set) * reads + i;
       async_read_warp(c, a, key, nodes + (a ? slot : 0), bufs + (a ? slot : 0) * 256, who,
                       sq_start + k + e * reads);
     }
   }
-  __device__ void wait_set(const DevCtx& c, u32 task, bool act, u32 set, u64& dg) const {
-    for (u32 i = 0; i < reads; ++i) {
-      const u64 slot = ((u64)task * 2 + set) * reads + i;
-      wait_nodes_warp(c, act, nodes + (act ? slot : 0));
-      if (act) {
+  // wait for the requests this thread issued; the first 8 bytes of each page go into its task's
+  // digest (xor: the order of the contributions does not matter)
+  __device__ void wait_set(const DevCtx& c, u32 uidx, u32 set) const {
+    const u32 total = cta_tasks(uidx) * reads;
+    for (u32 k = 0; k * kCtaThreads < total; ++k) {
+      const u32 f = k * kCtaThreads + threadIdx.x;
+      const bool a = f < total;
+      const u32 t = uidx * kCtaThreads + (a ? f / reads : 0), i = a ? f % reads : 0;
+      const u64 slot = ((u64)t * 2 + set) * reads + i;
+      wait_nodes_warp(c, a, nodes + (a ? slot : 0));
+      if (a) {
         const uint2 w = *reinterpret_cast<const uint2*>(bufs + slot * 256);
-        dg ^= (u64)w.x | ((u64)w.y << 32);
+        atomicXor(reinterpret_cast<unsigned long long*>(digest + t), (u64)w.x | ((u64)w.y << 32));
       }
     }
   }
   __device__ void run(const DevCtx& c, u32 uidx, u32 nusers) const {
-    const u32 task = uidx * kCtaThreads + threadIdx.x;
-    const bool act = task < tasks;
     const u32 who = user_who(uidx);
     const u32 sq_start = uidx * kCtaWarps + (threadIdx.x >> 5);
-    u64 dg = 0;
     if (uidx == 0 && threadIdx.x == 0) epoch_t[0] = gtimer();
     if (!async_mode) {
       for (u32 e = 0; e < epochs; ++e) {
-        issue(c, task, act, e, 0, who, sq_start);
-        wait_set(c, task, act, 0, dg);
+        issue(c, uidx, e, 0, who, sq_start);
+        wait_set(c, uidx, 0);
         // compute starts only after every task's data arrived (bench/ctc.py:80-83)
         if (!user_grid_barrier(c, nusers)) return;
         if (uidx == 0 && threadIdx.x == 0) epoch_t[e + 1] = gtimer();
         compute_spin(compute_ns);
       }
     } else {
-      issue(c, task, act, 0, 0, who, sq_start);
+      issue(c, uidx, 0, 0, who, sq_start);
       // every task's epoch-0 reads are queued before any epoch-1 read: a task that finished its
       // issue early would otherwise interleave epoch-1 commands into the device FIFO ahead of
       // other tasks' epoch-0 commands and delay the first wait by a whole epoch (the reference's
@@ -164,14 +168,13 @@ struct ReadsWork {
       for (u32 e = 0; e < epochs; ++e) {
         const u32 cur = e & 1u;
         // the next epoch's fetches ride under this epoch's compute (bench/ctc.py:47-70)
-        if (e + 1 < epochs) issue(c, task, act, e + 1, cur ^ 1u, who, sq_start);
-        wait_set(c, task, act, cur, dg);
+        if (e + 1 < epochs) issue(c, uidx, e + 1, cur ^ 1u, who, sq_start);
+        wait_set(c, uidx, cur);
         if (!user_grid_barrier(c, nusers)) return;
         if (uidx == 0 && threadIdx.x == 0) epoch_t[e + 1] = gtimer();
         compute_spin(compute_ns);
       }
     }
-    if (act) digest[task] = dg;
     // final timestamp after the last compute
     if (!user_grid_barrier(c, nusers)) return;
     if (uidx == 0 && threadIdx.x == 0) epoch_t[epochs] = gtimer();
