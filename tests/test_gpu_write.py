@@ -84,4 +84,4 @@ def test_rand_write_model_plateau(gpu_system):
     r = s.run_loop(512, warmup_ns=2_000_000, measure_ns=20_000_000, write=True)
     gbps = r["completions"] * 4096 / r["window_ns"]
     ceiling = 16 * 4096 / 29789
-    assert ceiling * 0.95 <= gbps <= ceiling * 1.01, (gbps, ceiling)
+    assert ceiling * 0.95 <= gbps <= ceiling * 1.02, (gbps, ceiling)   # window-edge completions
