@@ -28,8 +28,10 @@ def test_ctc_async_overlaps_compute(gpu_system):
 
 @pytest.mark.parametrize("ndev", [1, 2])
 def test_model_mode_rate_ceiling_and_scaling(gpu_system, ndev):
+    # 8 service warps: at 2 devices the service delivers ~1.8 M pages/s into the requesters'
+    # buffers (4 KiB copies), which 4 warps only just sustain
     s = gpu_system(num_devices=ndev, pairs=8, sq_depth=256, cq_depth=256, cache_lines=8192 * ndev, ways=32,
-                   blocks=1 << 18, emulation="model", engine_warps=16, warps=4)
+                   blocks=1 << 18, emulation="model", engine_warps=16, warps=8)
     # in-flight population well above the channel count: GPU issue/completion latencies are
     # microseconds, so the reference's 2x parallelism cannot cover them
     r = s.run_loop(512 * ndev, warmup_ns=2_000_000, measure_ns=20_000_000)
