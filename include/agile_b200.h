@@ -108,6 +108,10 @@ int agile_run_loop_rw(agile_ctx* ctx, uint32_t conc, uint64_t warmup_ns, uint64_
  * victim is claimed) and is written through to the device store before the call returns. */
 int agile_write_blocks(agile_ctx* ctx, const uint32_t* dev, const uint64_t* blk, int64_t n, const void* pages);
 
+/* SoftwareCache.evict per block (software_cache.py:268-281): outcome[i] 0 = RESET (the READY line
+ * was dropped), 1 = DEFERRED (busy, pinned or modified), 2 = not resident. */
+int agile_evict_blocks(agile_ctx* ctx, const uint32_t* dev, const uint64_t* blk, int64_t n, int8_t* outcome);
+
 /* Gather epochs (bench/sweeps.py:39-88): keys[tasks][epochs][gathers]; values = u32 element 0
  * of every gathered block; epoch_t[2] = start/end. */
 int agile_run_gather(agile_ctx* ctx, const uint64_t* keys, uint32_t tasks, uint32_t epochs, uint32_t gathers,

@@ -646,6 +646,29 @@ int agile_run_seq(agile_ctx* ctx, const uint32_t* dev, const uint64_t* blk, int6
   return rc;
 }
 
+int agile_evict_blocks(agile_ctx* ctx, const uint32_t* dev, const uint64_t* blk, int64_t n, int8_t* outcome) {
+  if (!ctx || n < 0 || (n && (!dev || !blk || !outcome))) return fail(ctx, AGILE_E_ARG, "bad evict args");
+  CK(cudaSetDevice(ctx->device));
+  for (int64_t i = 0; i < n; ++i)
+    if (dev[i] >= ctx->d.num_devices || blk[i] >= ctx->store_blocks[dev[i]])
+      return fail(ctx, AGILE_E_OUT_OF_RANGE, "block out of range");
+  if (n == 0) return 0;
+  uint32_t* d_dev; uint64_t* d_blk; int8_t* d_out;
+  CK(cudaMalloc(&d_dev, n * 4));
+  CK(cudaMalloc(&d_blk, n * 8));
+  CK(cudaMalloc(&d_out, n));
+  CK(cudaMemcpy(d_dev, dev, n * 4, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(d_blk, blk, n * 8, cudaMemcpyHostToDevice));
+  EvictWork w;
+  w.dev = d_dev; w.blk = reinterpret_cast<const u64*>(d_blk); w.n = n;
+  w.outcome = reinterpret_cast<signed char*>(d_out);
+  int rc = launch(ctx, w, 1, ctx->stream);
+  if (!rc) rc = agile_sync(ctx, ctx->stream);
+  if (!rc) CK(cudaMemcpy(outcome, d_out, n, cudaMemcpyDeviceToHost));
+  cudaFree(d_dev); cudaFree(d_blk); cudaFree(d_out);
+  return rc;
+}
+
 int agile_write_blocks(agile_ctx* ctx, const uint32_t* dev, const uint64_t* blk, int64_t n, const void* pages) {
   if (!ctx || n < 0 || (n && (!dev || !blk || !pages))) return fail(ctx, AGILE_E_ARG, "bad write args");
   CK(cudaSetDevice(ctx->device));

@@ -99,6 +99,52 @@ struct SeqWork {
   }
 };
 
+// ------------------------------------------------------------------ EvictWork
+// SoftwareCache.evict (software_cache.py:268-281 -> _evict_locked, 335-353) per block, serially
+// by one warp: a resident READY line with no pins is reset (INVALID, version + 1, evict_reset);
+// a BUSY or pinned line is DEFERRED; a MODIFIED line would need a write-back first and is
+// reported DEFERRED as well (the write path writes through, so none exists without the share
+// table).  outcome: 0 RESET, 1 DEFERRED, 2 not resident.
+struct EvictWork {
+  const u32* dev;
+  const u64* blk;
+  long long n;
+  signed char* outcome;
+  __device__ void run(const DevCtx& c, u32 uidx, u32 nusers) const {
+    if (uidx != 0 || threadIdx.x >= 32) return;
+    const u32 lane = lane_id();
+    const u32 who = user_who(0) & ~31u;
+    for (long long i = 0; i < n; ++i) {
+      const u64 key = make_key(dev[i], blk[i]);
+      u32 line = NONE;
+      u64 word = 0;
+      probe_lanes(c, lane == 0, key, line, word);
+      int oc = 2;
+      if (lane == 0 && line != NONE) {
+        const u32 set = line / c.ways;
+        oc = 1;
+        if (atom_cas_acquire(&c.set_lock[set], 0u, 1u) == 0u) {
+          const u64 w = ld_relaxed(&c.tags[line]);
+          if (!tw_live(w) || tw_key(w) != key) {
+            oc = 2;
+          } else if (tw_state(w) == ST_READY && tw_pins(w) == 0) {
+            const u64 nw = tw_make(ST_INVALID, 0, tw_ver(w) + 1, false, 0);
+            if (atom_cas_acqrel(&c.tags[line], w, nw) == w) {
+              oc = 0;
+              log_ev(c, who, M_CACHE, A_EVICT_RESET, line, key_dev(key), key_blk(key));
+              log_state(c, who, line, ST_READY, ST_INVALID, key);
+              atomicAdd(&c.stats[S_RESETS], 1ull);
+            }
+          }
+          st_release(&c.set_lock[set], 0u);
+        }
+      }
+      if (lane == 0) outcome[i] = (signed char)oc;
+      __syncwarp();
+    }
+  }
+};
+
 // ------------------------------------------------------------------ ReadsWork (CTC)
 struct ReadsWork {
   const u64* keys;        // [epochs][tasks][reads] request keys

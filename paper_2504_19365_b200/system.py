@@ -297,6 +297,15 @@ class AgileSystem:
         self._check(self._lib.agile_write_blocks(self._ctx, dev.ctypes.data, blk.ctypes.data, len(blk),
                                                  pages.ctypes.data), "write_blocks")
 
+    def evict_blocks(self, dev, blk) -> np.ndarray:
+        """SoftwareCache.evict per block: 0 RESET, 1 DEFERRED, 2 not resident."""
+        dev = np.ascontiguousarray(dev, dtype=np.uint32)
+        blk = np.ascontiguousarray(blk, dtype=np.uint64)
+        out = np.zeros(len(blk), dtype=np.int8)
+        self._check(self._lib.agile_evict_blocks(self._ctx, dev.ctypes.data, blk.ctypes.data, len(blk),
+                                                 out.ctypes.data), "evict_blocks")
+        return out
+
     def run_gather(self, keys, tasks, epochs, gathers, async_mode, compute_ns):
         import torch
         dev = torch.device("cuda", self.cuda_device)

@@ -85,3 +85,18 @@ def test_rand_write_model_plateau(gpu_system):
     gbps = r["completions"] * 4096 / r["window_ns"]
     ceiling = 16 * 4096 / 29789
     assert ceiling * 0.95 <= gbps <= ceiling * 1.02, (gbps, ceiling)   # window-edge completions
+
+
+def test_write_evict_then_device_read(gpu_system):
+    """test_gpu_api.py:131-151: write a block, evict it, read it back — the read misses and
+    returns the written bytes from the device."""
+    s = gpu_system(cache_lines=64, ways=16, blocks=1024, pairs=2, engine_warps=4, warps=2)
+    s.fill_store(0, seed=7)
+    blk = np.array([3, 77, 500], dtype=np.uint64)
+    pay = _payloads(np.random.default_rng(8), 3)
+    s.write_blocks(np.zeros(3), blk, pay)
+    assert list(s.evict_blocks(np.zeros(3), blk)) == [0, 0, 0]           # RESET
+    assert list(s.evict_blocks(np.zeros(3), blk)) == [2, 2, 2]           # no longer resident
+    out, _, pages = s.run_seq(np.zeros(3), blk, pages=True)
+    assert list(out) == [1, 1, 1]                                         # misses: device reads
+    assert np.array_equal(pages, pay)
