@@ -3,9 +3,12 @@
  * One context per GPU (one process per rank under torch.distributed).  The context owns the HBM
  * page cache (tag words + 4 KiB lines), the SQ/CQ rings and side tables, the completion service
  * and device-engine state, and one host-pinned GPU-mapped page store per emulated device.
- * Workload entry points launch one fused kernel on the caller's stream: its first CTAs become
- * the device engine (K4) and the completion service (K3), the rest run the workload against the
- * device library (K1 cache, K2 queue engine).
+ * Every workload entry point is one AGILE run on the caller's stream: an infra grid (device
+ * engine K4 + completion service K3) and a PDL-launched user grid running the workload against
+ * the device library (K1 cache, K2 queue engine), which starts only once every infra CTA is
+ * resident.  When a co-residency probe at agile_create sees a PDL dependent NOT run beside its
+ * primary (kernel-serialising tools), the context launches one fused grid instead, whose CTAs
+ * take their roles by arrival order (AGILE_LAUNCH=split|fused forces either).
  *
  * Every function returns 0 on success or a negative code; agile_last_error() has the message.
  * Codes -101.. map to the reference exception types:
@@ -55,8 +58,8 @@ enum {
 int agile_create(const char* config_text, int cuda_device, agile_ctx** out);
 int agile_destroy(agile_ctx* ctx);
 const char* agile_last_error(agile_ctx* ctx);
-/* geometry[0..9] = num_devices, pairs_per_device, sq_depth, cq_depth, lines, ways, sets,
- * engine_warps, service_warps, infra_ctas */
+/* geometry[0..10] = num_devices, pairs_per_device, sq_depth, cq_depth, lines, ways, sets,
+ * engine_warps, service_warps, infra_ctas, launch mode (0 split, 1 fused) */
 int agile_geometry(agile_ctx* ctx, uint64_t* out, int n);
 
 /* Backing store (BlockStore, ssd_model.py:61-101): pinned + GPU-mapped host memory, caller-owned
@@ -64,6 +67,11 @@ int agile_geometry(agile_ctx* ctx, uint64_t* out, int n);
  * raw little-endian block image, offset = blk * 4096, short tail zero-padded (load_image). */
 int agile_store_attach(agile_ctx* ctx, int dev, void* host_ptr, uint64_t num_blocks, const char* image_path);
 int agile_store_ptr(agile_ctx* ctx, int dev, void** host_ptr, uint64_t* num_blocks);
+/* BlockStore.load_image (ssd_model.py:84-95) into the attached store: blocks present in the raw
+ * image are overwritten (short last block zero-padded), the others keep their bytes, views from
+ * agile_store_ptr stay valid, and the device's cache lines are invalidated (IllegalState if a run
+ * of the context is still in flight). */
+int agile_store_load_image(agile_ctx* ctx, int dev, const char* path);
 /* synthetic page contents (oracle/pages.py): kind 0 = u64 word k of block b is
  * page_word(seed, dev, b, k); kind 1 = fp32 table values, each 32-bit half h of that word stored
  * as (h >> 8) * 2^-23 - 1 (page_floats) */

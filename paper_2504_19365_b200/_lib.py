@@ -28,6 +28,7 @@ SIGNATURES = {
     "agile_store_attach": (_int, [_vp, _int, _vp, _u64, _cp]),
     "agile_store_ptr": (_int, [_vp, _int, C.POINTER(_vp), C.POINTER(_u64)]),
     "agile_store_fill": (_int, [_vp, _int, _u64, _u64, _u64, _int]),
+    "agile_store_load_image": (_int, [_vp, _int, _cp]),
     "agile_store_save_image": (_int, [_vp, _int, _cp]),
     "agile_reset": (_int, [_vp, _int]),
     "agile_stats": (_int, [_vp, _vp, _int]),

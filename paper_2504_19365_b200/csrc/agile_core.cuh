@@ -25,6 +25,9 @@ struct Launch {
   u32 pad;
 };
 
+// users_started bit set by an infra grid that gave up on a user grid that never started
+constexpr u32 kInfraGaveUp = 0x80000000u;
+
 // position of the n-th (0-based) set bit of m (n < popc(m))
 __device__ __forceinline__ u32 nth_set_bit(u32 m, u32 n) {
   u32 pos = 0;
@@ -1211,10 +1214,13 @@ __device__ void service_main(const DevCtx& c, const Launch& L, u32 sw) {
       const bool users = ld_acquire(&c.run->users_done) >= L.n_user_ctas;
       const u64 out = ld_acquire(&c.pw->outstanding);
       stop = (users && out == 0) || aborted(c);
-      // the user grid never started (its launch was not allowed to overlap this grid): report
-      // instead of waiting forever
-      if (!stop && ld_relaxed(&c.run->users_started) == 0 && gtimer() - t_enter > c.watchdog_ns) {
-        set_error(c, E_LIVELOCK, 0, __LINE__ + 100000 * SPIN_FILE_ID);
+      // the user grid never started (a kernel-serialising tool, or a launch that was not allowed
+      // to overlap this grid): give up instead of waiting forever.  The CAS on users_started
+      // orders the decision against every user CTA's start (a CTA that starts later reads the
+      // give-up bit from its own atomicAdd and never waits on this grid).
+      if (!stop && gtimer() - t_enter > c.user_start_ns && ld_relaxed(&c.run->users_started) == 0 &&
+          atomicCAS(&c.run->users_started, 0u, kInfraGaveUp) == 0u) {
+        if (!c.solo_ok) set_error(c, E_LIVELOCK, 0, __LINE__ + 100000 * SPIN_FILE_ID);
         stop = 1;
       }
       if (users && atomicCAS(&c.run->stop_logged, 0u, 1u) == 0u) log_ev(c, who, M_SVC, A_STOP);
@@ -1697,8 +1703,17 @@ template <class Work>
 // it every thread would copy both structs from the parameter bank into local memory at entry.
 __global__ void __launch_bounds__(kCtaThreads, UserMinCtas<Work>::v)
     agile_user_kernel(const __grid_constant__ DevCtx c, const Launch L, const __grid_constant__ Work work) {
-  if (threadIdx.x == 0) atomicAdd(&c.run->users_started, 1u);
-  work.run(c, blockIdx.x, L.n_user_ctas);
+  __shared__ u32 s_solo;
+  if (threadIdx.x == 0) {
+    const u32 prev = atomicAdd(&c.run->users_started, 1u);
+    s_solo = (prev & kInfraGaveUp) ? 1u : 0u;
+    // the infra grid already left (this grid could not start beside it): outside profiling mode
+    // that is an error; in profiling mode the workload runs alone (an all-hit replay needs no
+    // engine or service; a miss then ends in the watchdog)
+    if (s_solo && !c.solo_ok) set_error(c, E_LIVELOCK, 1, __LINE__ + 100000 * SPIN_FILE_ID);
+  }
+  __syncthreads();
+  if (!s_solo || c.solo_ok) work.run(c, blockIdx.x, L.n_user_ctas);
   user_done(c, L.n_user_ctas);
 }
 

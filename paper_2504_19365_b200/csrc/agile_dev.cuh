@@ -17,8 +17,9 @@
 //   * completion svc   agile_service.py:90-236  -> service warps rotating over CQs, 32-entry
 //                       phase-checked windows, CQ doorbell only on full windows, SQE released
 //                       before the cache completion, drain of partial windows at stop.
-// Completion fan-out is through the per-line tag word: waiters poll it (no waiter lists, no
-// locks held while waiting), exactly the "no lock across a wait" rule of gpu_api.py:233-248.
+// Completion fan-out: async_read waiters sit on a per-line versioned waiter stack the service
+// drains (copy + barrier), array/row readers poll the per-line tag word; nobody holds a lock or a
+// pin while waiting, exactly the "no lock across a wait" rule of gpu_api.py:233-248.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -177,8 +178,9 @@ struct DevCtx {
   u32 service_warps, engine_warps, n_engine_ctas, n_service_ctas;
   u32 poll_ns, idle_max_ns;
   u32 trace;
-  u32 pad0;
+  u32 solo_ok;              // 1: a user grid that never started is not an error (profiling mode)
   u64 watchdog_ns;
+  u64 user_start_ns;        // the infra grid gives up on a user grid that has not started by then
   // cache
   u64* tags;
   unsigned short* sig;      // per-line 16-bit key signature: probe hint, the tag word decides

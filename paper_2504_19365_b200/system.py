@@ -131,10 +131,12 @@ class AgileSystem:
             raise exc(f"agile_create: {msg} (rc={rc})")
         if recorder is not None:
             self._check(self._lib.agile_trace_enable(self._ctx, trace_capacity), "trace_enable")
-        g = (C.c_uint64 * 10)()
-        self._lib.agile_geometry(self._ctx, g, 10)
+        g = (C.c_uint64 * 11)()
+        self._lib.agile_geometry(self._ctx, g, 11)
         (self.num_devices, self.pairs_per_device, self.sq_depth, self.cq_depth, self.num_lines,
-         self.ways, self.num_sets, self.engine_warps, self.service_warps, self.infra_ctas) = [int(x) for x in g]
+         self.ways, self.num_sets, self.engine_warps, self.service_warps, self.infra_ctas,
+         fused) = [int(x) for x in g]
+        self.launch_mode = "fused" if fused else "split"
         self.devices = [_Device(self, d) for d in range(self.num_devices)]
         self._views = {}
 
@@ -200,7 +202,9 @@ class AgileSystem:
         self._check(self._lib.agile_store_fill(self._ctx, dev, seed, first_blk, n, k), "store_fill")
 
     def load_image(self, dev: int, path) -> None:
-        self.attach_store(dev, self._store_blocks(dev), image_path=str(path))
+        """BlockStore.load_image (ssd_model.py:84-95) into the attached store; the device's cache
+        lines are invalidated and existing store views stay valid."""
+        self._check(self._lib.agile_store_load_image(self._ctx, dev, str(path).encode()), "load_image")
 
     def save_image(self, dev: int, path) -> None:
         self._check(self._lib.agile_store_save_image(self._ctx, dev, str(path).encode()), "save_image")
