@@ -354,7 +354,7 @@ def main():
             "roofline": roofline, "roofline_link": roofline_link,
             "hit_rate": 1.0 - miss_lookups / max(1, lookups_local),
             # per step: the infra grid + the PDL user grid of one agile_embbag run (1 in fused mode)
-            "gpu_launches": args.steps * (1 if os.environ.get("AGILE_LAUNCH") == "fused" else 2),
+            "gpu_launches": args.steps * (1 if system.launch_mode == "fused" else 2), "launch_mode": system.launch_mode,
             "clocks": clk, "setup_s": setup_s,
             "cache_warm": {"batches": warm, "seconds": warm_s}}
 

@@ -357,8 +357,14 @@ __global__ void coresidency_dependent(u32* w) {
 // 1: the dependent ran beside the primary (split launch is safe), 0: it did not, <0: CUDA error
 int probe_coresidency(agile_ctx* ctx) {
   u32* w = nullptr;
+  // load both kernels first: lazily loading the dependent's module while the primary spins waits
+  // for the device to drain, i.e. for the primary's timeout (the probe would always say "fused")
+  cudaFuncAttributes fa;
+  CK(cudaFuncGetAttributes(&fa, coresidency_primary));
+  CK(cudaFuncGetAttributes(&fa, coresidency_dependent));
   CK(cudaMalloc(&w, 8));
   CK(cudaMemset(w, 0, 8));
+  CK(cudaStreamSynchronize(ctx->stream));
   coresidency_primary<<<1, 32, 0, ctx->stream>>>(w, 200ull * 1000 * 1000);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(1);

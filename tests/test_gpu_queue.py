@@ -98,3 +98,13 @@ def test_gather_values_match_pages(gpu_system, tasks, async_mode):
     r = s.run_gather(keys, tasks, E, G, async_mode, 20000)
     exp = page_bytes(9, 0, blk.reshape(-1))[:, :4].copy().view(np.uint32).reshape(-1)
     assert np.array_equal(r["values"].reshape(-1), exp)
+
+
+def test_split_launch_selected(gpu_system):
+    """With no kernel-serialising tool attached, the co-residency probe must pick the split launch
+    (infra grid + PDL user grid, each with its own register budget)."""
+    if os.environ.get("AGILE_LAUNCH") or os.environ.get("NV_COMPUTE_PROFILER_PERFWORKS_DIR") \
+            or any(k.startswith("NV_NSIGHT") for k in os.environ):
+        pytest.skip("launch mode forced or a profiler is attached")
+    s = gpu_system()
+    assert s.launch_mode == "split"
