@@ -3,18 +3,19 @@
 
 Metric (BASELINE.json): DLRM lookups/s (and 4 KB-page IOPS) with the async-vs-sync overlap
 speedup.  A "step" is one DLRM embedding-bag batch (B=2048 x 26 tables x pooling 20, dim 128,
-fp32) gathered through the HBM page cache from the host-pinned page store:
+fp32 rows, fp64 accumulation) gathered through the HBM page cache from the host-pinned page store:
   * N=1  -> BASELINE configs[1]: tables 4x the HBM cache on one B200.
-  * N>1  -> BASELINE configs[4]: tables sharded by table over N ranks (one process per GPU,
-            torchrun), each with its own cache / queue pairs / store shard, pooled embeddings
-            exchanged with one NCCL all_to_all_single per step.  Per-GPU work is fixed
-            (weak scaling).
+  * N>1  -> BASELINE configs[4]: 1 TiB of tables sharded table-wise + row-wise over N ranks
+            (bench/dlrm.py plan_shards; one process per GPU, torchrun), each with its own cache /
+            queue pairs / store shard; K5 writes the pooled rows into the peer-major send buffer
+            and one unpadded NCCL all_to_all_single exchanges them (strong scaling: fixed tables
+            and global batch).
 Timing: W warm-up steps, then K timed steps on the launching stream with CUDA events,
 barrier + synchronize on both sides, max over ranks.  Inputs (index batches) are resident in
-HBM; every step uses a distinct batch; the working set (16 GiB cache + 64 GiB store per GPU)
-is far larger than L2.
-`--impl reference`: the CPU port of the same path (oracle/agile_oracle.c) on all host
-threads, rank 0 only.
+HBM; every step uses a distinct batch; the working set (HBM cache + page store per GPU) is far
+larger than L2.
+`--impl reference`: the CPU implementation of the same path (oracle/agile_oracle.c) on all host
+threads, rank 0 only, cache warmed to steady state, fresh batches.
 """
 
 from __future__ import annotations
@@ -45,6 +46,7 @@ def _args():
     p.add_argument("--impl", default="ours", choices=("ours", "reference"))
     p.add_argument("--cache-gib", type=float, default=16.0)
     p.add_argument("--table-mult", type=float, default=4.0)
+    p.add_argument("--total-tib", type=float, default=1.0, help="N > 1: total table bytes over all ranks (configs[4])")
     p.add_argument("--prefetch", type=int, default=0, help="in-kernel bag prefetch distance (0 = sync gather)")
     p.add_argument("--no-scatter", action="store_true")
     p.add_argument("--quick", action="store_true", help="skip e2e / sync / hit / cpu legs")
@@ -129,9 +131,16 @@ class Clocks:
 
 
 def _plan(args, world):
-    """Per-rank sizes: cache bytes and store bytes, capped by host RAM (pinned store)."""
+    """Per-rank sizes (cache bytes, table bytes held by the rank's page store).
+    N = 1 (configs[1]): a 16 GiB cache over 4x its size of tables.  N > 1 (configs[4]): 1 TiB of
+    tables in total, 1/N per rank, each rank caching 1/table_mult of its share (at most 120 GiB of
+    its 180 GB of HBM).  The pinned page store lives in host RAM: a rank's share is capped at 55 %
+    of the host's memory / local ranks (the cap is reported in config when it binds)."""
     cache_bytes = int(args.cache_gib * (1 << 30))
     table_bytes = int(cache_bytes * args.table_mult)
+    if world > 1:
+        table_bytes = int(args.total_tib * (1 << 40)) // world
+        cache_bytes = min(int(table_bytes / args.table_mult), 120 << 30)
     try:
         mem = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES")
         local = int(os.environ.get("LOCAL_WORLD_SIZE", world))
@@ -144,41 +153,82 @@ def _plan(args, world):
     return cache_bytes, table_bytes
 
 
+def _cpu_port(plan, rank, lines, scatter, threads, seconds, max_steps=400, warm_batches=None):
+    """The oracle C port (oracle/agile_oracle.c: the same paged embedding-bag through a set-
+    associative clock cache over the same row-keyed tables) on host threads.  Its cache is first
+    brought to steady state with full 2048-sample batches, as the GPU arm's is; the timed samples
+    are then fresh batches (never seen before) of 128 samples x the rank's tables x L, until
+    `seconds` of CPU time or max_steps samples.  Returns (lookups/s, description, cache)."""
+    import numpy as np
+    from paper_2504_19365_b200.bench.dlrm import make_batch
+    from oracle.cpu import CpuEmbeddingCache
+    descs, _, _ = plan.rank_layout(rank)
+    tabs = plan.rank_tables(rank)
+    rows_t = plan.rows[tabs]
+    cc = CpuEmbeddingCache(lines, 32, SEED, row_dim=D)
+    if warm_batches is None:
+        warm_batches = min(96, int(1.3 * lines / 69000) + 4)
+    t_w = time.perf_counter()
+    for k in range(warm_batches):
+        cc.embbag(make_batch(SEED + 7, k, plan.rows, B, L, ALPHA, scatter, tabs), descs["key0"], rows_t, D,
+                  threads=threads, tables=tabs)
+    warm_s = time.perf_counter() - t_w
+    bs, done, tsum, k = 128, 0, 0.0, 0
+    while tsum < seconds and k < max_steps:
+        idx = make_batch(SEED + 8, k, plan.rows, bs, L, ALPHA, scatter, tabs)
+        t0 = time.perf_counter()
+        cc.embbag(idx, descs["key0"], rows_t, D, threads=threads, tables=tabs)
+        tsum += time.perf_counter() - t0
+        done += idx.size
+        k += 1
+    st = cc.stats()
+    desc = (f"{k} fresh batches of {bs} samples x {len(tabs)} tables x {L} lookups after {warm_batches} warm-up "
+            f"batches of {B} ({warm_s:.1f} s; steady-state cache of {lines} lines, 32 ways; "
+            f"hit rate {st['hits'] / max(1, st['hits'] + st['misses']):.3f}); oracle/agile_oracle.c on {threads} threads")
+    return done / tsum, desc, cc
+
+
 def run_reference(args):
-    """CPU port of the same path on host threads (rank 0 only); bounded per-step samples."""
+    """Reference arm: the CPU implementation of the path (the oracle C port) on all host threads,
+    rank 0 only, on the GPU arm's metric and config; each step a bounded sample (128 fresh samples)
+    after the CPU cache was warmed to steady state exactly as the GPU arm warms its HBM cache."""
     rank = int(os.environ.get("RANK", 0))
     if rank != 0:
         return
     import numpy as np
-    from paper_2504_19365_b200.bench.dlrm import table_rows, layout, make_batch
+    from paper_2504_19365_b200.bench.dlrm import table_rows, plan_shards, make_batch
     from oracle.cpu import CpuEmbeddingCache
     world = args.gpus
     cache_bytes, table_bytes = _plan(args, world)
     rows = table_rows(table_bytes * world, D, T)
-    key0, pages = layout(rows, D)
+    plan = plan_shards(rows, world, D)
+    lines = cache_bytes // 4096 - (cache_bytes // 4096) % 32
     threads = os.cpu_count() or 1
-    cache = CpuEmbeddingCache(cache_bytes // 4096 - (cache_bytes // 4096) % 32, 32, SEED)
-    bs = 128   # bounded sample: 128 samples x 26 tables x 20 per step
+    scatter = not args.no_scatter
+    _, desc, cc = _cpu_port(plan, 0, lines, scatter, threads, seconds=0.0, max_steps=0)
+    descs, _, _ = plan.rank_layout(0)
+    tabs = plan.rank_tables(0)
+    bs = 128
     times = []
     for step in range(args.warmup + args.steps):
-        idx = make_batch(SEED, step, rows, B, L, ALPHA, not args.no_scatter)[:bs]
+        idx = make_batch(SEED, step, rows, bs, L, ALPHA, scatter, tabs)    # fresh every step
         t0 = time.perf_counter()
-        cache.embbag(idx, key0, rows, D, threads=threads)
+        cc.embbag(idx, descs["key0"], rows[tabs], D, threads=threads, tables=tabs)
         dt = time.perf_counter() - t0
         if step >= args.warmup:
             times.append(dt)
-    per = bs * T * L
+    per = bs * len(tabs) * L
     value = per * len(times) / sum(times)
     line = {"impl": "reference", "metric": "dlrm_lookups_per_s", "value": value, "unit": "lookups/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": "dlrm_embbag", "tables": T, "dim": D, "batch": B, "pooling": L,
-                       "cache_bytes_per_gpu": cache_bytes, "table_bytes_per_gpu": table_bytes,
-                       "zipf": ALPHA, "scatter": not args.no_scatter},
+            "scaling": "weak" if world == 1 else "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "dlrm_embbag" + ("_sharded_a2a" if world > 1 else ""), "tables": T, "dim": D,
+                       "global_batch": B, "pooling": L, "cache_bytes_per_gpu": cache_bytes,
+                       "table_bytes_per_gpu": table_bytes, "zipf": ALPHA, "scatter": scatter},
             "cpu_baseline": {"value": value, "unit": "lookups/s", "cores": threads, "kind": "port",
-                             "sample": f"{bs} samples x {T} tables x {L} lookups per step; set-assoc clock cache "
-                                       f"of {cache_bytes >> 30} GiB over {pages} synthetic pages"},
+                             "sample": f"{args.steps} timed steps of {bs} fresh samples x {len(tabs)} tables x {L} "
+                                       f"lookups (rank 0's shard); cache warm-up: {desc}"},
             "e2e": {"value": value, "unit": "lookups/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -192,8 +242,8 @@ def main():
     import torch
     import torch.distributed as dist
     from paper_2504_19365_b200 import AgileSystem, SystemConfig
-    from paper_2504_19365_b200.bench.dlrm import (table_rows, make_batch, shard_tables, build_shard,
-                                                  exchange_pooled, DlrmModel, run_pipeline, gpu_zipf_batch,
+    from paper_2504_19365_b200.bench.dlrm import (table_rows, make_batch, plan_shards, fill_rank_store,
+                                                  exchange, DlrmModel, run_pipeline, gpu_zipf_batch,
                                                   mlp_graph_ms)
 
     rank = int(os.environ.get("RANK", 0))
@@ -206,13 +256,17 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     cache_bytes, table_bytes = _plan(args, world)
     rows_all = table_rows(table_bytes * world, D, T)
-    groups, owner = shard_tables(rows_all, world)
-    shard = build_shard(rows_all, groups[rank], D)
-    Tg = len(shard.tables)
+    # N = 1: the 26 whole tables; N > 1: table-wise + row-wise pieces balanced by bytes and lookups
+    plan = plan_shards(rows_all, world, D)
+    descs, _, rank_pages = plan.rank_layout(rank)
+    my_tables = plan.rank_tables(rank)
+    my_rows = rows_all[my_tables]                 # indices of a piece's table are global rows
+    Tg = len(my_tables)
+    row_bytes = plan.row_bytes(rank)
 
     cfg = SystemConfig()
     cfg.seed = SEED
-    cfg.device.num_blocks = max(1, shard.pages)
+    cfg.device.num_blocks = max(1, rank_pages)
     cfg.device.emulation = "link"            # host-pinned page store at host-link speed
     cfg.cache.bytes = cache_bytes
     cfg.cache.ways = 32
@@ -227,30 +281,34 @@ def main():
     cfg.debug_locks = False
     t0 = time.time()
     system = AgileSystem(cfg, device=local)
-    system.fill_store(0, SEED, kind="f32")
+    fill_rank_store(system, plan, rank, SEED)      # row-keyed values: any sharding pools the same numbers
     setup_s = time.time() - t0
 
     scatter = not args.no_scatter
     nb = args.warmup + args.steps
     n_sync = max(2, args.steps // 2)
     n_e2e = args.steps
-    host_batches = [make_batch(SEED, s, rows_all, B, L, ALPHA, scatter, shard.tables)
+    host_batches = [make_batch(SEED, s, rows_all, B, L, ALPHA, scatter, my_tables)
                     for s in range(nb + n_sync + n_e2e + 1)]
     dbat = [torch.from_numpy(x).to(dev) for x in host_batches[:nb + n_sync]]
-    key0 = torch.from_numpy(shard.key0.view(np.int64)).to(dev)
-    rows = torch.from_numpy(shard.rows).to(dev)
-    out = torch.empty((B, Tg, D), dtype=torch.float32, device=dev)
+    tabs = torch.from_numpy(descs.view(np.uint8).copy()).to(dev)
+    key0 = torch.from_numpy(descs["key0"].view(np.int64).copy()).to(dev)   # whole-table view (N = 1 legs)
+    rows = torch.from_numpy(my_rows).to(dev)
+    # K5 writes each sample's row (fp32 whole tables, fp64 row-wise partials) straight into the
+    # peer-major all-to-all send buffer; at N = 1 that is the [B, 26, D] fp32 pooled tensor
+    out_bytes = torch.empty((B, row_bytes), dtype=torch.uint8, device=dev)
+    out = out_bytes.view(torch.float32).view(B, Tg, D) if world == 1 else None
     cnt = torch.zeros(2, dtype=torch.int64, device=dev)
     stream = torch.cuda.current_stream(dev)
 
     received = [None]
 
     def step(i, pd):
-        system.embbag(dbat[i], key0, rows, out, cnt, prefetch_distance=pd, stream=stream.cuda_stream)
+        system.embbag_sharded(dbat[i], tabs, out_bytes, cnt, D, prefetch_distance=pd, stream=stream.cuda_stream)
         if world > 1:
-            # pooled [B, Tg, D] is peer-major along B: one NCCL all-to-all hands every rank the
-            # pooled embeddings of its sample slice for all 26 tables
-            received[0] = exchange_pooled(out, groups, rank, world)
+            # one unpadded NCCL all_to_all_single hands every rank the rows of its sample slice;
+            # combine() adds the row-wise pieces' fp64 partials
+            received[0] = exchange(plan, out_bytes, rank, B)
 
     def barrier():
         if world > 1:
@@ -271,8 +329,8 @@ def main():
     gen = torch.Generator(device=dev).manual_seed(SEED + 1)
     t_w = time.time()
     for _ in range(warm):
-        wb = gpu_zipf_batch(gen, shard.rows, B, L, ALPHA, scatter, dev)
-        system.embbag(wb, key0, rows, out, cnt, prefetch_distance=args.prefetch, stream=stream.cuda_stream)
+        wb = gpu_zipf_batch(gen, my_rows, B, L, ALPHA, scatter, dev)
+        system.embbag_sharded(wb, tabs, out_bytes, cnt, D, prefetch_distance=args.prefetch, stream=stream.cuda_stream)
     system.sync(stream.cuda_stream)
     warm_s = time.time() - t_w
     # ---------------- warm-up steps ----------------
@@ -322,26 +380,32 @@ def main():
     avg_kern_s = statistics.mean(kern_ms) / 1e3
     bags_local = B * Tg
     alg_bytes = bags_local * L * (D * 4 + 8) + bags_local * D * 4      # rows + indices + pooled out
-    traffic = None
+    prof = {}
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_embbag_traffic.json")) as fh:
-            traffic = json.load(fh)["dram_bytes_per_launch"]
+            prof = json.load(fh)
     except Exception:
         pass
-    roofline = {"bound": "hbm", "achieved": alg_bytes / avg_kern_s / 1e9, "peak": hbm_peak, "unit": "GB/s",
-                "frac": alg_bytes / avg_kern_s / 1e9 / hbm_peak, "traffic": traffic,
-                "kernel": "agile_kernel<EmbBagWork> (fused engine+service+embbag)",
-                "bytes_per_launch": alg_bytes, "peak_kind": peak_kind,
-                "binding": "host link (see roofline_link): misses move 4 KiB pages over PCIe; hits are L2/HBM"}
+    # the step is bound by the host link: misses move 4 KiB pages host-pinned -> HBM (the engine's
+    # copies inside agile_infra_kernel), hits are served from HBM / L2 by agile_user_kernel
     miss_bytes = fills / args.steps * 4096
-    roofline_link = {"bound": "link", "achieved": miss_bytes / avg_kern_s / 1e9, "peak": link_peak, "unit": "GB/s",
-                     "frac": miss_bytes / avg_kern_s / 1e9 / link_peak,
-                     "iops": fills / args.steps / avg_kern_s, "page_fills_per_step": fills / args.steps,
-                     "peak_kind": "measured zero-copy 4 KiB gather (profiles/link_probe_r01.json)"}
+    roofline = {"bound": "link", "achieved": miss_bytes / avg_kern_s / 1e9, "peak": link_peak, "unit": "GB/s",
+                "frac": miss_bytes / avg_kern_s / 1e9 / link_peak,
+                "traffic": prof.get("link_bytes_per_launch"),
+                "kernel": f"agile_infra_kernel (engine page copies) + agile_user_kernel<EmbBagWork> ({system.launch_mode} launch)",
+                "algorithmic_bytes_per_launch": miss_bytes,
+                "iops": fills / args.steps / avg_kern_s, "page_fills_per_step": fills / args.steps,
+                "peak_kind": "measured zero-copy 4 KiB gather (profiles/link_probe_r01.json)",
+                "traffic_source": prof.get("source")}
+    roofline_hbm = {"bound": "hbm", "achieved": alg_bytes / avg_kern_s / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                    "frac": alg_bytes / avg_kern_s / 1e9 / hbm_peak, "traffic": prof.get("dram_bytes_per_launch"),
+                    "bytes_per_launch": alg_bytes, "peak_kind": peak_kind,
+                    "note": "algorithmic bytes (rows + indices + pooled out) over the whole step, hits and misses"}
 
     line = {"metric": "dlrm_lookups_per_s", "value": value, "unit": "lookups/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "higher_is_better": True, "scaling": "weak" if world == 1 else "strong", "vs_baseline": None,
+            "dtype": "f32",
             "data": "synthetic (Criteo-Kaggle-shaped cardinalities scaled to 4x cache, bounded Zipf "
                     f"{ALPHA} indices{' hashed over rows' if scatter else ''}, hash-generated fp32 rows)",
             "config": {"workload": "dlrm_embbag" + ("_sharded_a2a" if world > 1 else ""), "tables": T, "dim": D,
@@ -349,9 +413,10 @@ def main():
                        "table_bytes_per_gpu": table_bytes, "tables_this_rank": Tg,
                        "store": "host-pinned GPU-mapped page store, link emulation (no NVMe on the box)",
                        "ways": 32, "queue_pairs": 128, "sq_depth": 256, "prefetch_distance": args.prefetch,
-                       "l2": "inputs larger than L2 (16 GiB HBM cache over a 64 GiB store; distinct batch per step)",
-                       "parallelism": f"table-wise x{world}" if world > 1 else "single"},
-            "roofline": roofline, "roofline_link": roofline_link,
+                       "l2": f"inputs larger than L2 ({cache_bytes >> 30} GiB HBM cache over a {table_bytes >> 30} GiB store per GPU; distinct batch per step)",
+                       "parallelism": f"table-wise + row-wise x{world} (TWRW), NCCL all_to_all_single" if world > 1 else "single",
+                       "shard_balance": plan.balance() if world > 1 else None},
+            "roofline": roofline, "roofline_hbm": roofline_hbm,
             "hit_rate": 1.0 - miss_lookups / max(1, lookups_local),
             # per step: the infra grid + the PDL user grid of one agile_embbag run (1 in fused mode)
             "gpu_launches": args.steps * (1 if system.launch_mode == "fused" else 2), "launch_mode": system.launch_mode,
@@ -395,7 +460,7 @@ def main():
                 mlp_ms = mlp_by[best]
                 res = {}
                 for mode, co in (("sync", best), ("prefetch", args.carveout), ("async", args.carveout)):
-                    bat = [gpu_zipf_batch(gen, shard.rows, B, L, ALPHA, scatter, dev) for _ in range(args.steps)]
+                    bat = [gpu_zipf_batch(gen, my_rows, B, L, ALPHA, scatter, dev) for _ in range(args.steps)]
                     res[mode] = run_pipeline(system, bat, key0, rows, graphs[co], (out, out_b), mode,
                                              side_ctas=args.side_ctas, prefetch_distance=args.prefetch)
                 t_s = res["sync"]["ms"] / args.steps
@@ -429,12 +494,12 @@ def main():
         h1 = torch.cuda.Event(enable_timing=True)
         # one untimed pass makes every page of the batch resident (it was last touched two
         # phases ago and may have lost pages since); the timed passes are then pure hits
-        system.embbag(dbat[hb], key0, rows, out, cnt, prefetch_distance=0, stream=stream.cuda_stream)
+        system.embbag_sharded(dbat[hb], tabs, out_bytes, cnt, D, stream=stream.cuda_stream)
         cnt.zero_()
         h0.record(stream)
         reps = 5
         for _ in range(reps):
-            system.embbag(dbat[hb], key0, rows, out, cnt, prefetch_distance=0, stream=stream.cuda_stream)
+            system.embbag_sharded(dbat[hb], tabs, out_bytes, cnt, D, stream=stream.cuda_stream)
         h1.record(stream)
         system.sync(stream.cuda_stream)
         hit_s = h0.elapsed_time(h1) / reps / 1e3
@@ -449,8 +514,8 @@ def main():
             # host buffers in pinned memory, as a serving frontend would hold them
             hb_np = [torch.from_numpy(host_batches[nb + n_sync + k]).pin_memory().numpy() for k in range(args.steps)]
             outs_np = [torch.empty((B, Tg, D), dtype=torch.float32).pin_memory().numpy() for _ in range(2)]
-            keyh = torch.from_numpy(shard.key0.view(np.int64).copy()).pin_memory().numpy().view(np.uint64)
-            rowsh = torch.from_numpy(shard.rows.copy()).pin_memory().numpy()
+            keyh = torch.from_numpy(descs["key0"].view(np.int64).copy()).pin_memory().numpy().view(np.uint64)
+            rowsh = torch.from_numpy(my_rows.copy()).pin_memory().numpy()
             cnts = [np.zeros(2, dtype=np.uint64) for _ in range(2)]
             # pipelined through the C-ABI: step k's pooled output leaves (D2H) and step k+1's
             # indices arrive (H2D) while a run is on the device; every copy is inside the region
@@ -485,32 +550,16 @@ def main():
                            "path": "H2D indices -> embbag -> NCCL all_to_all -> D2H pooled (per rank)"}
         # ---- CPU baseline (rank 0, N=1 only): oracle C port on host threads, bounded sample ----
         if rank == 0 and world == 1:
-            from oracle.cpu import CpuEmbeddingCache
             threads = os.cpu_count() or 1
-            lines_ = system.num_lines
-            cc = CpuEmbeddingCache(lines_, 32, SEED)
-            bs = 128
-            done, tsum, k = 0, 0.0, 0
-            errs = []
-            while tsum < args.cpu_seconds and k < 400:
-                idx = host_batches[k % len(host_batches)][:bs]
-                t_c = time.perf_counter()
-                o = cc.embbag(idx, shard.key0, shard.rows, D, threads=threads)
-                dt = time.perf_counter() - t_c
-                if k >= 2:
-                    tsum += dt
-                    done += idx.size
-                k += 1
-            # cross-check the GPU output of the last timed-out batch against the CPU port
-            o_cpu = cc.embbag(host_batches[hb][:16], shard.key0, shard.rows, D, threads=threads)
-            system.embbag(dbat[hb], key0, rows, out, cnt, prefetch_distance=0, stream=stream.cuda_stream)
+            cpu_v, cpu_desc, cc = _cpu_port(plan, 0, system.num_lines, scatter, threads, args.cpu_seconds)
+            # cross-check the GPU output of a batch against the CPU port
+            o_cpu = cc.embbag(host_batches[hb][:16], descs["key0"], my_rows, D, threads=threads, tables=my_tables)
+            system.embbag_sharded(dbat[hb], tabs, out_bytes, cnt, D, stream=stream.cuda_stream)
             system.sync(stream.cuda_stream)
             o_gpu = out[:16].cpu().numpy()
             line["cpu_gpu_max_abs_diff"] = float(np.max(np.abs(o_cpu - o_gpu)))
-            line["cpu_baseline"] = {"value": done / tsum if tsum else None, "unit": "lookups/s", "cores": threads,
-                                    "kind": "port",
-                                    "sample": f"{k - 2} batches of {bs} samples x {T} tables x {L} (oracle/agile_oracle.c, "
-                                              f"set-assoc clock cache of {lines_} lines over the same synthetic store)"}
+            line["cpu_baseline"] = {"value": cpu_v, "unit": "lookups/s", "cores": threads, "kind": "port",
+                                    "sample": cpu_desc}
     if rank == 0:
         print(json.dumps(line), flush=True)
     system.close()

@@ -77,6 +77,13 @@ int agile_store_load_image(agile_ctx* ctx, int dev, const char* path);
  * as (h >> 8) * 2^-23 - 1 (page_floats) */
 int agile_store_fill(agile_ctx* ctx, int dev, uint64_t seed, uint64_t first_blk, uint64_t nblk, int kind);
 int agile_store_save_image(agile_ctx* ctx, int dev, const char* path);
+/* embedding rows keyed by (table, global row) (oracle/pages.py row_floats): pages
+ * [first_blk, first_blk + ceil(rows / (1024 / D))) receive rows [row0, row0 + rows) of table
+ * `table` (< 256), 1024 / D rows of D fp32 per page; u64 word k of row r is
+ * splitmix64(seed ^ table<<56 ^ r<<8 ^ k), each 32-bit half h stored as (h >> 8) * 2^-23 - 1.
+ * Any row-wise sharding of a table therefore holds the same values as the whole table. */
+int agile_store_fill_rows(agile_ctx* ctx, int dev, uint64_t seed, uint64_t first_blk, uint32_t table, uint64_t row0,
+                          uint64_t rows, uint32_t D);
 
 /* reset flags: 1 cache (tags/hands/locks), 2 queues + service/engine state, 4 stats */
 int agile_reset(agile_ctx* ctx, int flags);
@@ -126,11 +133,37 @@ int agile_run_gather(agile_ctx* ctx, const uint64_t* keys, uint32_t tasks, uint3
                      int async_mode, uint64_t compute_ns, uint32_t* values, uint64_t* epoch_t, void* stream);
 
 /* DLRM embedding-bag (K5), device pointers: idx[B][T][L] int64 rows, table_key0[T] first page
- * key of each table, table_rows[T], out[b*out_b_stride + t*out_t_stride + d] fp32 (sum pooling),
- * counters[2] += {lookups, miss-path lookups}.  prefetch_distance 0 = sync mode. */
+ * key of each table, table_rows[T], out[b*out_b_stride + t*out_t_stride + d] fp32 (sum pooling,
+ * fp64 accumulation rounded once), counters[2] += {lookups, miss-path lookups}.  Indices outside
+ * [0, table_rows[t]) raise AGILE_E_OUT_OF_RANGE.  prefetch_distance 0 = sync mode, > 0 = each
+ * warp prefetches the next block of bags it grabbed while it pools the current one. */
 int agile_embbag(agile_ctx* ctx, const int64_t* idx, const uint64_t* table_key0, const int64_t* table_rows,
                  float* out, uint64_t* counters, uint32_t B, uint32_t T, uint32_t L, uint32_t D,
                  uint32_t out_b_stride, uint32_t out_t_stride, uint32_t prefetch_distance, void* stream);
+/* Sharded / variable-length embedding-bag (K5), device pointers.  One agile_table_shard per
+ * table of the launch: a whole table (row0 = 0, rows = table_rows) or one rank's row range of a
+ * table split row-wise over ranks (BASELINE configs[4]).  Lookup l of bag (b, t) is
+ * idx[(b*T + t)*L + l] (offsets == NULL) or idx[offsets[b*T + t] + l] for l < offsets[b*T+t+1] -
+ * offsets[b*T+t] (offsets[B*T + 1], variable-length bags, torch embedding_bag's include_last_offset
+ * convention).  Indices outside [0, table_rows) raise AGILE_E_OUT_OF_RANGE; indices outside the
+ * shard's [row0, row0 + rows) are another rank's and skipped.  Sums accumulate in fp64: a shard
+ * with AGILE_TAB_PARTIAL_F64 writes its D fp64 partial sums (for the receiver to add after the
+ * exchange), otherwise the sum is rounded once to D fp32.  Table t of sample b lands at
+ * (char*)out + b*out_row_bytes + tables[t].out_offset — e.g. straight into a peer-major
+ * all-to-all send buffer.  mode 0 = pool, 1 = prefetch only (AgileApi.prefetch over the batch:
+ * every missing page submitted, the call completes when all fills landed; out may be NULL). */
+typedef struct agile_table_shard {
+  uint64_t key0;        /* page key of the shard's first page: dev << 36 | page */
+  int64_t row0;         /* first global row held by this shard */
+  int64_t rows;         /* rows held: global rows [row0, row0 + rows) */
+  int64_t table_rows;   /* rows of the whole table */
+  uint32_t out_offset;  /* byte offset of the table's pooled vector in an output row (16 B aligned) */
+  uint32_t flags;       /* AGILE_TAB_PARTIAL_F64 */
+} agile_table_shard;
+#define AGILE_TAB_PARTIAL_F64 1u
+int agile_embbag_sharded(agile_ctx* ctx, const int64_t* idx, const int64_t* offsets, const agile_table_shard* tables,
+                         void* out, uint64_t out_row_bytes, uint64_t* counters, uint32_t B, uint32_t T, uint32_t L,
+                         uint32_t D, uint32_t prefetch_distance, uint32_t user_ctas, int mode, void* stream);
 /* Same, with the launch bounded to user_ctas user CTAs (0 = every resident slot): a gather issued
  * on a side stream beside compute (the DLRM MLPs) leaves the remaining SMs to that compute. */
 int agile_embbag_ctas(agile_ctx* ctx, const int64_t* idx, const uint64_t* table_key0, const int64_t* table_rows,

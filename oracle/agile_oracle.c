@@ -8,7 +8,9 @@
  *     bytes are the synthetic store contents of oracle/pages.py (page_floats: every 32-bit half h
  *     of splitmix64(seed ^ dev<<56 ^ blk<<9 ^ k) stored as (h >> 8) * 2^-23 - 1);
  *   - the embedding-bag built on read_range (software_cache.py:212-219, the gather stand-in of
- *     bench/sweeps.py): pooled[b,t,:] = sum_l row(idx[b,t,l]), fp32, l ascending.
+ *     bench/sweeps.py): pooled[b,t,:] = sum_l row(idx[b,t,l]), accumulated in fp64 (l ascending)
+ *     and rounded once to fp32 — the GPU kernel's definition (exact sum, correctly rounded,
+ *     whenever the fp64 sum is exact).
  * Threads split the bags; a per-set spinlock serialises each set (the reference's policy lock,
  * software_cache.py:163, narrowed to one set).
  */
@@ -28,6 +30,7 @@ typedef struct {
   atomic_flag* lock;
   float* data;        /* lines * 1024 floats */
   uint64_t seed;
+  uint32_t row_dim;   /* 0: page-keyed contents (page_floats); D: row-keyed tables (row_floats) */
   atomic_ullong hits, misses, evictions;
 } ocache;
 
@@ -78,8 +81,29 @@ static void fetch_block(const ocache* c, uint64_t dev, uint64_t blk, float* dst)
   }
 }
 
-/* access (dev, blk) under its set lock; returns the line index (lock held on return) */
-static uint64_t access_locked(ocache* c, uint64_t dev, uint64_t blk, uint32_t* set_out) {
+/* row-keyed table page (oracle/pages.py row_floats): rows first_row.. of `table`, D fp32 each */
+static void fetch_rows(const ocache* c, uint32_t table, uint64_t first_row, uint64_t table_rows, float* dst) {
+  const uint32_t D = c->row_dim, rpp = BLOCK / (4 * D);
+  for (uint32_t s = 0; s < rpp; ++s) {
+    const uint64_t r = first_row + s;
+    for (uint32_t k = 0; k < D / 2; ++k) {
+      uint64_t x = 0;
+      if (r < table_rows) x = splitmix64(c->seed ^ ((uint64_t)table << 56) ^ (r << 8) ^ k);
+      float lo = (float)((uint32_t)x >> 8) * (1.0f / 8388608.0f) - 1.0f;
+      float hi = (float)((uint32_t)(x >> 32) >> 8) * (1.0f / 8388608.0f) - 1.0f;
+      if (r >= table_rows) lo = hi = 0.0f;
+      dst[s * D + 2 * k] = lo;
+      dst[s * D + 2 * k + 1] = hi;
+    }
+  }
+}
+
+void oracle_cache_rowkeyed(void* h, uint32_t D) { ((ocache*)h)->row_dim = D; }
+
+/* access (dev, blk) under its set lock; returns the line index (lock held on return).  A miss
+ * fills the line with the block's contents: page-keyed, or rows of (table, page_in_table). */
+static uint64_t access_locked(ocache* c, uint64_t dev, uint64_t blk, uint32_t table, uint64_t page_in_table,
+                              uint64_t table_rows, uint32_t* set_out) {
   const uint32_t s = set_of(dev, blk, c->sets);
   *set_out = s;
   while (atomic_flag_test_and_set_explicit(&c->lock[s], memory_order_acquire)) { }
@@ -104,7 +128,10 @@ static uint64_t access_locked(ocache* c, uint64_t dev, uint64_t blk, uint32_t* s
   if (c->tag[victim]) atomic_fetch_add_explicit(&c->evictions, 1, memory_order_relaxed);
   c->tag[victim] = key;
   c->ref[victim] = 1;
-  fetch_block(c, dev, blk, c->data + victim * 1024);
+  if (c->row_dim)
+    fetch_rows(c, table, page_in_table * (BLOCK / (4 * c->row_dim)), table_rows, c->data + victim * 1024);
+  else
+    fetch_block(c, dev, blk, c->data + victim * 1024);
   return victim;
 }
 
@@ -113,9 +140,11 @@ typedef struct {
   const int64_t* idx;
   const uint64_t* key0;
   const int64_t* rows;
+  const int64_t* table_id;   /* global table id of every table of the launch (row-keyed mode) */
   float* out;
   uint32_t B, T, L, D;
   uint64_t bag0, bag1;
+  int bad;   /* an index outside [0, rows) was seen (OutOfRange) */
 } job;
 
 static void* run_bags(void* arg) {
@@ -125,38 +154,43 @@ static void* run_bags(void* arg) {
   for (uint64_t bag = j->bag0; bag < j->bag1; ++bag) {
     const uint64_t t = bag % j->T;
     float* o = j->out + bag * j->D;
-    memset(o, 0, sizeof(float) * j->D);
+    double acc[BLOCK / 4];
+    memset(acc, 0, sizeof(double) * j->D);
     const uint64_t dev = j->key0[t] >> 36;
     const uint64_t page0 = j->key0[t] & ((1ull << 36) - 1);
     for (uint32_t l = 0; l < j->L; ++l) {
       int64_t r = j->idx[bag * j->L + l];
-      if (r < 0 || r >= j->rows[t]) r = 0;
+      if (r < 0 || r >= j->rows[t]) { j->bad = 1; continue; }
       uint32_t s;
-      const uint64_t line = access_locked(c, dev, page0 + (uint64_t)r / rpp, &s);
+      const uint64_t line = access_locked(c, dev, page0 + (uint64_t)r / rpp, (uint32_t)j->table_id[t],
+                                          (uint64_t)r / rpp, (uint64_t)j->rows[t], &s);
       const float* row = c->data + line * 1024 + (uint64_t)(r % rpp) * j->D;
-      for (uint32_t d = 0; d < j->D; ++d) o[d] += row[d];
+      for (uint32_t d = 0; d < j->D; ++d) acc[d] += (double)row[d];
       atomic_flag_clear_explicit(&c->lock[s], memory_order_release);
     }
+    for (uint32_t d = 0; d < j->D; ++d) o[d] = (float)acc[d];
   }
   return NULL;
 }
 
-/* pooled[B][T][D]; idx[B][T][L]; returns 0 */
-int oracle_embbag(void* h, const int64_t* idx, const uint64_t* key0, const int64_t* rows, float* out,
-                  uint32_t B, uint32_t T, uint32_t L, uint32_t D, int nthreads) {
+/* pooled[B][T][D]; idx[B][T][L]; returns 0, or -2 when an index is out of range */
+int oracle_embbag(void* h, const int64_t* idx, const uint64_t* key0, const int64_t* rows, const int64_t* table_id,
+                  float* out, uint32_t B, uint32_t T, uint32_t L, uint32_t D, int nthreads) {
   ocache* c = h;
-  if (!c || D == 0 || (BLOCK / 4) % D) return -1;
+  if (!c || D == 0 || (BLOCK / 4) % D || (c->row_dim && (c->row_dim != D || !table_id))) return -1;
   if (nthreads < 1) nthreads = 1;
   const uint64_t nb = (uint64_t)B * T;
   pthread_t th[256];
   job jobs[256];
   if (nthreads > 256) nthreads = 256;
   for (int i = 0; i < nthreads; ++i) {
-    jobs[i] = (job){c, idx, key0, rows, out, B, T, L, D, nb * i / nthreads, nb * (i + 1) / nthreads};
+    jobs[i] = (job){c, idx, key0, rows, table_id, out, B, T, L, D, nb * i / nthreads, nb * (i + 1) / nthreads, 0};
     if (nthreads == 1) run_bags(&jobs[i]);
     else pthread_create(&th[i], NULL, run_bags, &jobs[i]);
   }
   if (nthreads > 1)
     for (int i = 0; i < nthreads; ++i) pthread_join(th[i], NULL);
+  for (int i = 0; i < nthreads; ++i)
+    if (jobs[i].bad) return -2;
   return 0;
 }

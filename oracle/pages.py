@@ -43,6 +43,17 @@ def page_floats(seed: int, dev: int, blks) -> np.ndarray:
     return ((u >> np.uint32(8)).astype(np.float32) * np.float32(2.0 ** -23) - np.float32(1.0)).astype(np.float32)
 
 
+def row_floats(seed: int, table: int, rows, D: int) -> np.ndarray:
+    """float32 [len(rows), D]: embedding rows keyed by (table, global row) — u64 word k of row r
+    is splitmix64(seed ^ table<<56 ^ r<<8 ^ k), each 32-bit half h stored as (h >> 8) * 2^-23 - 1
+    (agile_b200.cu fill_rows_kernel).  A row-wise shard of a table holds these same values."""
+    r = np.asarray(rows, dtype=np.uint64).reshape(-1, 1)
+    k = np.arange(D // 2, dtype=np.uint64).reshape(1, -1)
+    x = np.uint64(seed) ^ (np.uint64(table) << np.uint64(56)) ^ (r << np.uint64(8)) ^ k
+    u = splitmix64(x).view(np.uint32).reshape(len(r), D)
+    return ((u >> np.uint32(8)).astype(np.float32) * np.float32(2.0 ** -23) - np.float32(1.0)).astype(np.float32)
+
+
 def load_image(path, num_blocks: int) -> np.ndarray:
     """BlockStore.load_image (ssd_model.py:84-95): blocks past the file are zero."""
     out = np.zeros((num_blocks, BLOCK), dtype=np.uint8)

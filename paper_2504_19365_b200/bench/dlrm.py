@@ -5,9 +5,9 @@ ancestor is the synthetic gather of bench/sweeps.py:1-9, which "stands in for em
   8 rows per 4 KiB page, laid out contiguously in the emulated device's page store.
 * Indices: bounded Zipf(alpha) ranks per table, optionally scattered over rows by a bijective
   multiplicative hash (hashed categorical ids), deterministic per (seed, batch).
-* Table-wise sharding over G ranks, balanced by bytes (largest first); pooled outputs of a
-  rank's tables are [B, T_g, D], i.e. already in the peer-major layout all_to_all_single
-  splits along B.
+* Table-wise + row-wise sharding over G ranks (plan_shards), balanced by bytes and lookups;
+  K5 writes every rank's pooled rows straight into the peer-major all-to-all send buffer, one
+  unpadded all_to_all_single exchanges them, combine() adds the row-wise partials.
 """
 
 from __future__ import annotations
@@ -88,30 +88,188 @@ def gpu_zipf_batch(gen, rows_t, B: int, L: int, alpha: float, scatter: bool, dev
     return torch.stack(cols, dim=1).contiguous()
 
 
-def shard_tables(rows: np.ndarray, G: int):
-    """Table-wise assignment balanced by bytes (largest first onto the lightest rank)."""
-    load = [0] * G
-    owner = np.zeros(len(rows), dtype=np.int64)
-    for t in np.argsort(-rows, kind="stable"):
-        g = int(np.argmin(load))
-        owner[t] = g
-        load[g] += int(rows[t])
-    return [np.nonzero(owner == g)[0] for g in range(G)], owner
+# ----------------------------------------------------------------------------- sharding (configs[4])
+
+# one agile_table_shard (include/agile_b200.h) per table piece of a launch
+TAB_DTYPE = np.dtype([("key0", "<u8"), ("row0", "<i8"), ("rows", "<i8"), ("table_rows", "<i8"),
+                      ("out_offset", "<u4"), ("flags", "<u4")])
+assert TAB_DTYPE.itemsize == 40
+PARTIAL_F64 = 1
 
 
 @dataclass
-class DlrmShard:
-    """One rank's share: its tables, their rows and page keys in the rank's own store."""
-    tables: np.ndarray
+class Piece:
+    """Rows [row0, row0 + rows) of global table `table`; `partial`: the table is split by rows over
+    several ranks, so this rank sends its fp64 partial sums and the sample's owner adds them."""
+    table: int
+    row0: int
+    rows: int
+    partial: bool
+
+
+@dataclass
+class ShardPlan:
+    """Table-wise + row-wise sharding of the DLRM tables over `world` ranks (TWRW).
+
+    Small tables stay whole and are spread by lookup count; large tables are cut into page-aligned
+    row ranges so every rank holds about 1/world of the table bytes and of the lookups.  Row-wise
+    pieces pool fp64 partial sums; because the kernel accumulates in fp64 (exact for the synthetic
+    rows), the receiver's fp64 sum of the partials rounds to the same fp32 as a single device."""
+    world: int
+    dim: int
     rows: np.ndarray
-    key0: np.ndarray
-    pages: int
+    pieces: list   # per rank: [Piece], whole tables first, then partials
+
+    @property
+    def rpp(self) -> int:
+        return 4096 // (4 * self.dim)
+
+    def rank_tables(self, rank: int) -> np.ndarray:
+        return np.array([p.table for p in self.pieces[rank]], dtype=np.int64)
+
+    def row_bytes(self, rank: int) -> int:
+        """bytes of one sample's output row on `rank`: D fp32 per whole table, D fp64 per piece"""
+        return sum(self.dim * (8 if p.partial else 4) for p in self.pieces[rank])
+
+    def n_whole(self, rank: int) -> int:
+        return sum(1 for p in self.pieces[rank] if not p.partial)
+
+    def rank_layout(self, rank: int, dev: int = 0, first_page: int = 0):
+        """(descs [P] TAB_DTYPE, first page of every piece [P], total pages) of the rank's store."""
+        ps = self.pieces[rank]
+        descs = np.zeros(len(ps), dtype=TAB_DTYPE)
+        first = np.zeros(len(ps), dtype=np.int64)
+        page, off = first_page, 0
+        for j, p in enumerate(ps):
+            first[j] = page
+            descs[j] = ((dev << 36) | page, p.row0, p.rows, int(self.rows[p.table]), off,
+                        PARTIAL_F64 if p.partial else 0)
+            page += (p.rows + self.rpp - 1) // self.rpp
+            off += self.dim * (8 if p.partial else 4)
+        return descs, first, page
+
+    def balance(self, lookups_by_table=None) -> dict:
+        """max/mean over ranks of table bytes and of lookups (expected: proportional to the rows of
+        a piece, or counted: lookups_by_table[t] = callable(row0, rows) -> lookups in the range)."""
+        by = np.array([sum(p.rows for p in ps) for ps in self.pieces], dtype=np.float64)
+        if lookups_by_table is None:
+            lk = np.array([sum(p.rows / self.rows[p.table] for p in ps) for ps in self.pieces])
+        else:
+            lk = np.array([sum(lookups_by_table[p.table](p.row0, p.rows) for p in ps) for ps in self.pieces],
+                          dtype=np.float64)
+        return {"bytes": float(by.max() / by.mean()), "lookups": float(lk.max() / lk.mean()),
+                "pieces": [len(ps) for ps in self.pieces]}
 
 
-def build_shard(all_rows: np.ndarray, tables: np.ndarray, dim: int) -> DlrmShard:
-    rows = all_rows[tables]
-    key0, pages = layout(rows, dim)
-    return DlrmShard(tables=tables, rows=rows, key0=key0, pages=pages)
+def plan_shards(rows: np.ndarray, world: int, dim: int = 128, eps: float = 0.03,
+                small_frac: float = 0.05) -> ShardPlan:
+    """Greedy TWRW plan.  Tables are taken largest first.  A table whose pages exceed small_frac of
+    a rank's byte target is cut into page-aligned row ranges, each put on the rank with the lowest
+    normalised load max(lookups / target, bytes / target) and sized to fill it up to (1 + eps) of
+    both targets.  Smaller tables stay whole, on the rank with the fewest lookups (ties: bytes)."""
+    rows = np.asarray(rows, dtype=np.int64)
+    T = len(rows)
+    rpp = 4096 // (4 * dim)
+    pages = (rows + rpp - 1) // rpp
+    tl, tb = T / world, pages.sum() / world
+    ll = np.zeros(world)
+    lb = np.zeros(world)
+    raw = [[] for _ in range(world)]
+    for t in np.argsort(-rows, kind="stable"):
+        n = int(rows[t])
+        if world == 1 or pages[t] <= small_frac * tb:
+            g = int(np.lexsort((lb, ll))[0])
+            raw[g].append((int(t), 0, n))
+            ll[g] += 1
+            lb[g] += pages[t]
+            continue
+        r0 = 0
+        while r0 < n:
+            g = int(np.argmin(np.maximum(ll / tl, lb / tb)))
+            rem = n - r0
+            fit = min(((1 + eps) * tl - ll[g]) * n, ((1 + eps) * tb - lb[g]) * rpp)
+            take = rem if fit >= rem else min(rem, max(rpp, int(fit) // rpp * rpp))
+            raw[g].append((int(t), r0, take))
+            ll[g] += take / n
+            lb[g] += (take + rpp - 1) // rpp
+            r0 += take
+    split = {t for ps in raw for (t, r0, k) in ps if k < rows[t]}
+    pieces = []
+    for ps in raw:
+        whole = [Piece(t, r0, k, False) for (t, r0, k) in sorted(ps) if t not in split]
+        part = [Piece(t, r0, k, True) for (t, r0, k) in sorted(ps) if t in split]
+        pieces.append(whole + part)
+    return ShardPlan(world=world, dim=dim, rows=rows, pieces=pieces)
+
+
+def fill_rank_store(system, plan: ShardPlan, rank: int, seed: int, dev: int = 0) -> None:
+    """Write the rank's pieces into its page store, row-keyed (oracle/pages.py row_floats)."""
+    descs, first, _ = plan.rank_layout(rank, dev)
+    for j, p in enumerate(plan.pieces[rank]):
+        system.fill_rows(dev, seed, int(first[j]), p.table, p.row0, p.rows, plan.dim)
+
+
+def combine(plan: ShardPlan, recv, n_local: int):
+    """Received bytes (all_to_all_single output: peer q's [n_local, row_bytes(q)] blocks in rank
+    order) -> pooled [n_local, T, D] fp32 in global table order: whole tables copied, row-wise
+    pieces summed in fp64 (exact) and rounded once."""
+    import torch
+    D, T = plan.dim, len(plan.rows)
+    out = torch.empty((n_local, T, D), dtype=torch.float32, device=recv.device)
+    split = sorted({p.table for ps in plan.pieces for p in ps if p.partial})
+    slot = {t: i for i, t in enumerate(split)}
+    acc = torch.zeros((n_local, len(split), D), dtype=torch.float64, device=recv.device) if split else None
+    off = 0
+    for q, ps in enumerate(plan.pieces):
+        rb = plan.row_bytes(q)
+        blk = recv[off:off + n_local * rb].view(n_local, rb)
+        off += n_local * rb
+        nw = plan.n_whole(q)
+        if nw:
+            tw = torch.as_tensor([p.table for p in ps[:nw]], dtype=torch.long, device=recv.device)
+            out[:, tw] = blk[:, :nw * D * 4].contiguous().view(torch.float32).view(n_local, nw, D)
+        if len(ps) > nw:
+            sl = torch.as_tensor([slot[p.table] for p in ps[nw:]], dtype=torch.long, device=recv.device)
+            acc.index_add_(1, sl, blk[:, nw * D * 4:].contiguous().view(torch.float64).view(n_local, len(ps) - nw, D))
+    if split:
+        out[:, torch.as_tensor(split, dtype=torch.long, device=recv.device)] = acc.to(torch.float32)
+    return out
+
+
+def exchange(plan: ShardPlan, send, rank: int, batch: int):
+    """One all_to_all_single of the kernel's output rows: `send` is the rank's [batch, row_bytes]
+    uint8 buffer, peer-major along the batch (samples [p*batch/G, (p+1)*batch/G) go to rank p),
+    unpadded: rank q's rows are row_bytes(q) wide (input/output split sizes per peer)."""
+    import torch
+    import torch.distributed as dist
+    G = plan.world
+    nl = batch // G
+    rb = plan.row_bytes(rank)
+    out_splits = [nl * plan.row_bytes(q) for q in range(G)]
+    recv = torch.empty(sum(out_splits), dtype=torch.uint8, device=send.device)
+    dist.all_to_all_single(recv, send.view(-1), out_splits, [nl * rb] * G)
+    return combine(plan, recv, nl)
+
+
+def pool_rank_reference(plan: ShardPlan, rank: int, idx: np.ndarray, seed: int) -> np.ndarray:
+    """CPU restatement of the rank's K5 output rows ([B, row_bytes] uint8) from row-keyed tables:
+    whole tables fp32(fp64 sum), row pieces the fp64 partial over the rows they hold.  Test
+    infrastructure for the exchange (the gloo test) — the GPU path writes these bytes itself."""
+    from oracle.pages import row_floats
+    B = idx.shape[0]
+    D = plan.dim
+    cols = []
+    for j, p in enumerate(plan.pieces[rank]):
+        ix = idx[:, j, :]
+        m = (ix >= p.row0) & (ix < p.row0 + p.rows)
+        acc = np.zeros((B, D), dtype=np.float64)
+        if m.any():
+            uniq, inv = np.unique(ix[m], return_inverse=True)
+            vals = row_floats(seed, p.table, uniq, D).astype(np.float64)
+            bi = np.nonzero(m)[0]
+            np.add.at(acc, bi, vals[inv])
+        cols.append(acc.view(np.uint8) if p.partial else acc.astype(np.float32).view(np.uint8))
+    return np.ascontiguousarray(np.concatenate(cols, axis=1)) if cols else np.zeros((B, 0), np.uint8)
 
 
 # ----------------------------------------------------------------------------- DLRM model + pipeline
@@ -317,22 +475,3 @@ def run_dlrm(cfg, trace: bool = False):
             res = run_pipeline(system, bat, k0, r, mlps, outs, mode)
             result.rows.append((mode, nb, int(res["ms"] * 1e6), round(res["lookups_per_s"], 3), res["miss_lookups"]))
     return result
-
-
-def exchange_pooled(pooled_local, groups, rank: int, world: int):
-    """Table-wise model parallel -> data parallel: rank r holds pooled[B, T_r, D] for its tables;
-    after one all_to_all_single every rank holds pooled[B/world, T, D] for its sample slice, tables
-    in global order.  pooled_local's B dimension is already peer-major (slice p goes to rank p)."""
-    import torch
-    import torch.distributed as dist
-    B, Tr, D = pooled_local.shape
-    tmax = max(len(g) for g in groups)
-    send = torch.zeros((world, B // world, tmax, D), dtype=pooled_local.dtype, device=pooled_local.device)
-    send[:, :, :Tr] = pooled_local.view(world, B // world, Tr, D)
-    recv = torch.empty_like(send)
-    dist.all_to_all_single(recv, send)
-    T = sum(len(g) for g in groups)
-    out = torch.empty((B // world, T, D), dtype=pooled_local.dtype, device=pooled_local.device)
-    for q in range(world):
-        out[:, torch.as_tensor(groups[q], dtype=torch.long, device=out.device)] = recv[q, :, :len(groups[q])]
-    return out

@@ -323,6 +323,35 @@ __global__ void fill_store_kernel(uint8_t* base, uint64_t seed, uint32_t dev, ui
   }
 }
 
+// Embedding rows keyed by (table, global row) rather than by page (oracle/pages.py row_floats):
+// u64 word k of row r of table t is splitmix64(seed ^ t<<56 ^ r<<8 ^ k); each 32-bit half h is
+// stored as the fp32 (h >> 8) * 2^-23 - 1.  A shard holding rows [row0, row0 + rows) of the table
+// gets the same values wherever its pages sit, so any sharding of the tables over ranks pools the
+// same numbers.  Page p (from first) holds rows row0 + p*rpp .. ; slots past the shard are zero.
+__global__ void fill_rows_kernel(uint8_t* base, uint64_t seed, uint32_t table, uint64_t first, uint64_t row0,
+                                 uint64_t rows, uint32_t D) {
+  const uint32_t rpp = 4096u / (4u * D), wpr = D / 2;   // rows per page, u64 words per row
+  const uint64_t npages = (rows + rpp - 1) / rpp;
+  const uint64_t nwords = npages * 512;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nwords; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t pg = i / 512, w = i % 512;
+    const uint64_t slot = w / wpr, k = w % wpr;
+    const uint64_t rr = pg * rpp + slot;
+    uint64_t x = 0;
+    if (rr < rows) {
+      x = seed ^ ((uint64_t)table << 56) ^ ((row0 + rr) << 8) ^ k;
+      x += 0x9E3779B97F4A7C15ull;
+      x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+      x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+      x ^= x >> 31;
+      const float lo = (float)((uint32_t)x >> 8) * (1.0f / 8388608.0f) - 1.0f;
+      const float hi = (float)((uint32_t)(x >> 32) >> 8) * (1.0f / 8388608.0f) - 1.0f;
+      x = (uint64_t)__float_as_uint(lo) | ((uint64_t)__float_as_uint(hi) << 32);
+    }
+    AGILE_FILL_STORE(reinterpret_cast<unsigned long long*>(base + (first + pg) * 4096) + w, (unsigned long long)x);
+  }
+}
+
 // Drop every line of device `dev` (between runs: nothing is in flight).  READY lines go INVALID
 // with a version bump (readers validating the old identity see the change); a BUSY or pinned line
 // would mean a run is still active and is counted instead.
@@ -655,6 +684,21 @@ int agile_store_fill(agile_ctx* ctx, int dev, uint64_t seed, uint64_t first_blk,
   return 0;
 }
 
+int agile_store_fill_rows(agile_ctx* ctx, int dev, uint64_t seed, uint64_t first_blk, uint32_t table, uint64_t row0,
+                          uint64_t rows, uint32_t D) {
+  if (!ctx || dev < 0 || dev >= (int)ctx->d.num_devices) return AGILE_E_ARG;
+  if (D == 0 || D > 128 || D % 4 || (1024u % D) != 0 || table > 255 || row0 + rows >= (1ull << 48))
+    return fail(ctx, AGILE_E_ARG, "bad fill_rows geometry");
+  const uint64_t rpp = 1024 / D, npages = (rows + rpp - 1) / rpp;
+  if (first_blk + npages > ctx->store_blocks[dev]) return fail(ctx, AGILE_E_OUT_OF_RANGE, "fill beyond store");
+  if (!npages) return 0;
+  CK(cudaSetDevice(ctx->device));
+  fill_rows_kernel<<<ctx->sms * 8, 256>>>(ctx->d.store_w[dev], seed, table, first_blk, row0, rows, D);
+  CK(cudaGetLastError());
+  CK(cudaDeviceSynchronize());
+  return 0;
+}
+
 int agile_store_save_image(agile_ctx* ctx, int dev, const char* path) {
   if (!ctx || dev < 0 || dev >= (int)ctx->d.num_devices || !path) return AGILE_E_ARG;
   CK(cudaDeviceSynchronize());
@@ -907,6 +951,33 @@ int agile_run_gather(agile_ctx* ctx, const uint64_t* keys, uint32_t tasks, uint3
 
 static uint32_t embbag_users(agile_ctx* ctx) { return resident_ctas<EmbBagWork>(ctx); }
 
+// common launch of K5: geometry checks, then one AGILE run (user_ctas != 0: a bounded side run)
+static int embbag_launch(agile_ctx* ctx, EmbBagWork& w, const int64_t* idx, const int64_t* offsets, uint8_t* out,
+                         uint64_t* counters, uint32_t B, uint32_t T, uint32_t L, uint32_t D, uint32_t pd,
+                         uint32_t user_ctas, int prefetch_only, void* stream) {
+  if (T == 0) return fail(ctx, AGILE_E_ARG, "no tables");
+  if (!offsets && L > 4096) return fail(ctx, AGILE_E_ARG, "pooling factor L must be <= 4096");
+  if (D == 0 || D > 128 || D % 4 || (1024u % D) != 0) return fail(ctx, AGILE_E_ARG, "D must divide 1024, be a multiple of 4 and <= 128");
+  if ((uint64_t)B * T >= (1ull << 31) || (!offsets && (uint64_t)B * T * L >= (1ull << 40)))
+    return fail(ctx, AGILE_E_ARG, "too many bags");
+  CK(cudaSetDevice(ctx->device));
+  w.idx = reinterpret_cast<const long long*>(idx);
+  w.offsets = reinterpret_cast<const long long*>(offsets);
+  w.out = out;
+  w.lookups_miss = reinterpret_cast<u64*>(counters);
+  w.B = B; w.T = T; w.L = offsets ? 0 : L; w.D = D;
+  w.pd = pd;
+  uint32_t rpp = kBlockBytes / (D * 4), sh = 0;
+  while ((1u << sh) < rpp) ++sh;
+  w.rows_per_page_shift = sh;
+  w.prefetch_only = prefetch_only ? 1u : 0u;
+  const uint32_t full = embbag_users(ctx);
+  const uint32_t users = user_ctas ? std::min(user_ctas, full) : full;
+  w.nwarps_total = users * kCtaWarps;
+  if ((uint64_t)B * T == 0) return 0;
+  return launch(ctx, w, users, reinterpret_cast<cudaStream_t>(stream), user_ctas != 0);
+}
+
 int agile_embbag_grid(agile_ctx* ctx, uint32_t* user_ctas, uint32_t* infra_ctas) {
   if (!ctx) return AGILE_E_ARG;
   if (user_ctas) *user_ctas = embbag_users(ctx);
@@ -926,52 +997,36 @@ int agile_embbag_ctas(agile_ctx* ctx, const int64_t* idx, const uint64_t* table_
                       uint32_t out_b_stride, uint32_t out_t_stride, uint32_t prefetch_distance, uint32_t user_ctas,
                       void* stream) {
   if (!ctx || !idx || !table_key0 || !table_rows || !out || !counters) return fail(ctx, AGILE_E_ARG, "null embbag arg");
-  if (L == 0 || L > 32) return fail(ctx, AGILE_E_ARG, "pooling factor L must be in [1, 32]");
-  if (D == 0 || D > 128 || D % 4 || (1024u % D) != 0) return fail(ctx, AGILE_E_ARG, "D must divide 1024, be a multiple of 4 and <= 128");
-  if ((uint64_t)B * T >= (1ull << 31)) return fail(ctx, AGILE_E_ARG, "too many bags");
-  CK(cudaSetDevice(ctx->device));
-  EmbBagWork w;
-  w.idx = reinterpret_cast<const long long*>(idx);
+  EmbBagWork w{};
   w.table_key0 = reinterpret_cast<const u64*>(table_key0);
   w.table_rows = reinterpret_cast<const long long*>(table_rows);
-  w.out = out;
-  w.lookups_miss = reinterpret_cast<u64*>(counters);
-  w.B = B; w.T = T; w.L = L; w.D = D;
-  w.pd = prefetch_distance;
-  uint32_t rpp = kBlockBytes / (D * 4), sh = 0;
-  while ((1u << sh) < rpp) ++sh;
-  w.rows_per_page_shift = sh;
-  w.out_b_stride = out_b_stride ? out_b_stride : T * D;
-  w.out_t_stride = out_t_stride ? out_t_stride : D;
-  const uint32_t full = embbag_users(ctx);
-  const uint32_t users = user_ctas ? std::min(user_ctas, full) : full;
-  w.nwarps_total = users * kCtaWarps;
-  w.prefetch_only = 0;
-  return launch(ctx, w, users, reinterpret_cast<cudaStream_t>(stream), user_ctas != 0);
+  w.out_row_bytes = (u64)(out_b_stride ? out_b_stride : T * D) * 4;
+  w.out_t_bytes = (out_t_stride ? out_t_stride : D) * 4;
+  return embbag_launch(ctx, w, idx, nullptr, reinterpret_cast<uint8_t*>(out), counters, B, T, L, D, prefetch_distance,
+                       user_ctas, 0, stream);
+}
+
+int agile_embbag_sharded(agile_ctx* ctx, const int64_t* idx, const int64_t* offsets, const agile_table_shard* tables,
+                         void* out, uint64_t out_row_bytes, uint64_t* counters, uint32_t B, uint32_t T, uint32_t L,
+                         uint32_t D, uint32_t prefetch_distance, uint32_t user_ctas, int mode, void* stream) {
+  if (!ctx || !idx || !tables || !counters || (mode == 0 && !out)) return fail(ctx, AGILE_E_ARG, "null embbag arg");
+  if (mode != 0 && mode != 1) return fail(ctx, AGILE_E_ARG, "mode must be 0 (pool) or 1 (prefetch only)");
+  if (mode == 0 && (out_row_bytes % 16)) return fail(ctx, AGILE_E_ARG, "out_row_bytes must be a multiple of 16");
+  EmbBagWork w{};
+  w.tabs = reinterpret_cast<const TabDesc*>(tables);
+  w.out_row_bytes = out_row_bytes;
+  return embbag_launch(ctx, w, idx, offsets, reinterpret_cast<uint8_t*>(out), counters, B, T, L, D,
+                       prefetch_distance, user_ctas, mode, stream);
 }
 
 int agile_embbag_prefetch(agile_ctx* ctx, const int64_t* idx, const uint64_t* table_key0, const int64_t* table_rows,
                           uint64_t* counters, uint32_t B, uint32_t T, uint32_t L, uint32_t D, uint32_t user_ctas,
                           void* stream) {
   if (!ctx || !idx || !table_key0 || !table_rows || !counters) return fail(ctx, AGILE_E_ARG, "null prefetch arg");
-  if (L == 0 || L > 32) return fail(ctx, AGILE_E_ARG, "pooling factor L must be in [1, 32]");
-  if (D == 0 || D > 128 || D % 4 || (1024u % D) != 0) return fail(ctx, AGILE_E_ARG, "bad D");
-  CK(cudaSetDevice(ctx->device));
   EmbBagWork w{};
-  w.idx = reinterpret_cast<const long long*>(idx);
   w.table_key0 = reinterpret_cast<const u64*>(table_key0);
   w.table_rows = reinterpret_cast<const long long*>(table_rows);
-  w.out = nullptr;
-  w.lookups_miss = reinterpret_cast<u64*>(counters);
-  w.B = B; w.T = T; w.L = L; w.D = D;
-  uint32_t rpp = kBlockBytes / (D * 4), sh = 0;
-  while ((1u << sh) < rpp) ++sh;
-  w.rows_per_page_shift = sh;
-  w.prefetch_only = 1;
-  const uint32_t full = embbag_users(ctx);
-  const uint32_t users = user_ctas ? std::min(user_ctas, full) : full;
-  w.nwarps_total = users * kCtaWarps;
-  return launch(ctx, w, users, reinterpret_cast<cudaStream_t>(stream), user_ctas != 0);
+  return embbag_launch(ctx, w, idx, nullptr, nullptr, counters, B, T, L, D, 0, user_ctas, 1, stream);
 }
 
 // ------------------------------------------------------------------ graph drivers (K6 / K7)

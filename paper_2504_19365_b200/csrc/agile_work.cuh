@@ -52,21 +52,15 @@ __device__ __forceinline__ void compute_spin(u64 ns) {
 __device__ __forceinline__ u32 user_who(u32 uidx) { return WHO_USER | (uidx * kCtaThreads + threadIdx.x); }
 
 // Read-side ordering of the cached-row readers (embedding-bag hot path).  Every tag word is read
-// with a strong gpu-scope load and every row with an L2 (.cg / cp.async.cg) load, so L2 — the
-// single point of coherence — serves both; the writer side publishes page bytes before the READY
-// tag through release/acquire (engine fence -> CQE release -> service acquire -> tag release).
-// Two read-side orders remain:
-//   READY seen -> row read:  the row load is control-dependent on the tag value (issued only after
-//                            the confirming load returned; sm_100 issues loads in order),
-//   row read -> tag re-read: the re-read is issued after the row values were consumed.
-// So no MEMBAR is needed on the hit path; AGILE_HIT_FENCE=1 restores a fence.acq_rel.gpu (MEMBAR +
-// L1 invalidate) at both points, the formal PTX-model pattern, for A/B runs.
-#ifndef AGILE_HIT_FENCE
-#define AGILE_HIT_FENCE 0
-#endif
-__device__ __forceinline__ void hit_fence() {
-  if (AGILE_HIT_FENCE) fence_acq_rel();
-}
+// with a strong gpu-scope load and every row with an L2 (.cg) load, so L2 — the single point of
+// coherence — serves both; the writer side publishes page bytes before the READY tag through
+// release/acquire (engine fence -> CQE release -> service acquire -> tag release), and a claim
+// bumps the tag's version before the line's bytes are overwritten.  The reader needs:
+//   READY seen -> row read:  the confirming tag load is an acquire (ld.acquire.gpu);
+//   row read -> tag re-read: the re-read's address carries a data dependency on the row values
+//                            (dep_zero over a warp reduction), so it cannot be issued before
+//                            every row load of the warp returned.
+// No fence.acq_rel (MEMBAR + L1 invalidate) is issued on the hit path.
 
 // ------------------------------------------------------------------ SeqWork
 struct SeqWork {
@@ -402,69 +396,127 @@ struct GatherWork {
 };
 
 // ------------------------------------------------------------------ EmbBagWork (K5)
-// pooled[b, t, :] = sum_l table_t[idx[b, t, l], :] over 4 KiB pages of 8 rows x 128 fp32.
-// One warp per bag: lanes 0..L-1 map their index to (page, row slot), the warp probes all L
-// pages with the batched ballot probe, misses are claimed/submitted warp-aggregated, then every
-// lane loads one float4 of each row (16 B/lane, 512 B coalesced per row) and sums in registers.
-// Hits are validated seqlock-style against the tag word after a fence (no pin atomics on the
-// hot path).  Async mode prefetches the warp's bag `pd` positions ahead before processing.
+// pooled[b, t, :] = sum_l table_t[idx(b, t, l), :] over 4 KiB pages of 4096 / (4 D) rows of D fp32.
+//
+// Tables are described per launch by TabDesc (= agile_table_shard of the C-ABI): the page key of
+// the shard's first page, the global row range [row0, row0 + rows) the shard holds (row-wise
+// sharding over ranks; a whole table has row0 = 0, rows = table_rows), the whole table's row
+// count (indices outside [0, table_rows) raise OutOfRange, gpu_api.py:328-332 / ssd_model.py:24),
+// the byte offset of the table's pooled vector in an output row, and whether the shard writes its
+// fp64 partial sum (row shards, summed by the receiver after the exchange) or the final fp32.
+//
+// Accumulation is fp64, rounded once to fp32: whenever the fp64 sum is exact (always for the
+// synthetic tables, whose values lie on a 2^-23 grid in [-1, 1), for any pooling factor below
+// 2^29) the result is the correctly rounded exact sum, independent of summation order — so a
+// table split by rows over ranks, or a bag split into 32-lookup chunks, gives bit-identical
+// pooled vectors.
+//
+// One warp per bag; a bag's lookups are taken 32 per chunk (lane = lookup; fixed L or
+// variable-length bags through offsets).  A chunk's pages are resolved with the batched
+// signature probe (READY confirmed by an acquire load), misses claimed/submitted warp-aggregated
+// and waited without holding anything; then every lane loads one 16 B slice of each row (512 B
+// coalesced per row at D = 128) and accumulates.  Hits are validated seqlock-style once per
+// chunk: the tag re-read carries a data dependency on every row value the warp loaded, so it is
+// issued only after those loads returned; a changed identity redoes the chunk.
+struct TabDesc {
+  u64 key0;
+  long long row0, rows, total;
+  u32 out_off;
+  u32 flags;
+};
+static_assert(sizeof(TabDesc) == 40, "TabDesc must match agile_table_shard");
+constexpr u32 TAB_PARTIAL_F64 = 1u;
+
+// 0, computed from v: an address offset that cannot be formed before v's load returned
+__device__ __forceinline__ u64 dep_zero(u32 v) {
+  u32 z;
+  asm volatile("and.b32 %0, %1, 0;" : "=r"(z) : "r"(v));
+  return (u64)z;
+}
+
 struct EmbBagWork {
-  const long long* idx;        // [B][T][L]
+  const long long* idx;        // bag (b, t): idx[(b*T + t)*L + l], or idx[offsets[b*T + t] + l]
+  const long long* offsets;    // [B*T + 1] (variable-length bags) or null
+  const TabDesc* tabs;         // [T] or null: then table_key0 / table_rows, whole tables
   const u64* table_key0;       // [T] key of the table's first page (dev << 36 | page)
   const long long* table_rows; // [T]
-  float* out;                  // [B][T][D]
+  uint8_t* out;                // table t of sample b at out + b*out_row_bytes + out_off(t)
+  u64 out_row_bytes;
+  u32 out_t_bytes;             // legacy layout: out_off(t) = t * out_t_bytes
   u64* lookups_miss;           // [2] lookups, miss-path lookups
   u32 B, T, L, D;
-  u32 pd;                      // prefetch distance in bags (0 = sync)
+  u32 pd;                      // > 0: prefetch the next grabbed block of bags (async mode)
   u32 rows_per_page_shift;     // log2(4096 / (D*4))
-  u32 out_b_stride, out_t_stride;   // in floats
   u32 nwarps_total;
   u32 prefetch_only;           // 1: pull every page of the batch toward the cache, no pooling
 
-  // stage A of a bag: the lane's raw row index (read-only input: non-coherent loads survive the
-  // L1 invalidations of acquire loads and fences)
-  __device__ __forceinline__ long long bag_raw(u32 bag, bool lane_act) const {
-    return lane_act ? __ldg(idx + (u64)bag * L + lane_id()) : 0ll;
-  }
-  // stage B: page key and byte offset of the lane's row
-  __device__ __forceinline__ bool bag_key_of(u32 bag, bool lane_act, long long r, u64& key, u32& off) const {
-    if (!lane_act) return false;
-    const u32 t = bag % T;
-    const long long rows = __ldg(table_rows + t);
-    if (r < 0 || r >= rows) r = 0;   // invalid index -> row 0 (callers validate on host)
-    const u64 page = (u64)r >> rows_per_page_shift;
-    const u32 slot = (u32)r & ((1u << rows_per_page_shift) - 1u);
-    key = __ldg(reinterpret_cast<const unsigned long long*>(table_key0) + t) + page;
-    off = slot * D * 4;
-    return true;
-  }
-
-  __device__ __forceinline__ bool bag_keys(u32 bag, bool lane_act, u64& key, u32& off) const {
-    const u32 b = bag / T, t = bag % T;
-    if (!lane_act) return false;
-    long long r = idx[((u64)b * T + t) * L + lane_id()];
-    const long long rows = table_rows[t];
-    if (r < 0 || r >= rows) r = 0;   // invalid index -> row 0 (callers validate on host)
-    const u64 page = (u64)r >> rows_per_page_shift;
-    const u32 slot = (u32)r & ((1u << rows_per_page_shift) - 1u);
-    key = table_key0[t] + page;
-    off = slot * D * 4;
-    return true;
-  }
-
-  static constexpr u32 kMaxPd = 8;
-  // next bag for this warp from the launch-wide counter (dynamic balance: a warp held up by a
-  // slow miss does not hold back a static share of the batch)
-  static constexpr u32 kGrab = 4;   // bags taken per counter atomic
-  __device__ __forceinline__ u32 grab(const DevCtx& c, u32& pool, u32& left) const {
-    if (!left) {
-      u32 b = 0;
-      if (lane_id() == 0) b = (u32)atomicAdd(&c.run->work_next, (u64)kGrab);
-      pool = __shfl_sync(FULL, b, 0);
-      left = kGrab;
+  __device__ __forceinline__ TabDesc tab(u32 t) const {
+    TabDesc d;
+    if (tabs) {
+      const TabDesc* p = tabs + t;
+      d.key0 = __ldg(reinterpret_cast<const unsigned long long*>(&p->key0));
+      d.row0 = __ldg(&p->row0);
+      d.rows = __ldg(&p->rows);
+      d.total = __ldg(&p->total);
+      d.out_off = __ldg(&p->out_off);
+      d.flags = __ldg(&p->flags);
+    } else {
+      d.key0 = __ldg(reinterpret_cast<const unsigned long long*>(table_key0) + t);
+      d.row0 = 0;
+      d.rows = d.total = __ldg(table_rows + t);
+      d.out_off = t * out_t_bytes;
+      d.flags = 0;
     }
-    --left;
-    return pool++;
+    return d;
+  }
+  __device__ __forceinline__ void bag_span(u32 bag, u64& start, u32& n) const {
+    if (offsets) {
+      const long long s0 = __ldg(offsets + bag), s1 = __ldg(offsets + bag + 1);
+      start = (u64)s0;
+      n = s1 > s0 ? (u32)(s1 - s0) : 0u;
+    } else {
+      start = (u64)bag * L;
+      n = L;
+    }
+  }
+  // the lane's lookup -> (page key, byte offset in the page); false when the lane has no lookup
+  // in this shard.  Out-of-range indices raise OutOfRange (the run aborts, the host sees -103).
+  __device__ __forceinline__ bool lookup_key(const DevCtx& c, const TabDesc& td, bool lact, long long r, u32 t,
+                                             u64& key, u32& off) const {
+    if (!lact) return false;
+    if (r < 0 || r >= td.total) {
+      set_error(c, E_OUT_OF_RANGE, t, (u64)r);
+      return false;
+    }
+    if (r < td.row0 || r >= td.row0 + td.rows) return false;   // another rank's rows
+    const u64 lr = (u64)(r - td.row0);
+    key = td.key0 + (lr >> rows_per_page_shift);
+    off = ((u32)lr & ((1u << rows_per_page_shift) - 1u)) * D * 4;
+    return true;
+  }
+
+  // bags are grabbed kGrab at a time from the launch-wide counter (dynamic balance: a warp held
+  // up by a slow miss does not hold back a static share of the batch)
+  static constexpr u32 kGrab = 4;
+  __device__ __forceinline__ u32 grab_block(const DevCtx& c) const {
+    u32 b = 0;
+    if (lane_id() == 0) b = (u32)atomicAdd(&c.run->work_next, (u64)kGrab);
+    return __shfl_sync(FULL, b, 0);
+  }
+  // async mode: submit the missing pages of a block's bags (first chunk of each), no waiting
+  __device__ __noinline__ void prefetch_block(const DevCtx& c, u32 first, u32 nbags, u32 who, u32 sq) const {
+    for (u32 k = 0; k < kGrab && first + k < nbags; ++k) {
+      const u32 bag = first + k;
+      const u32 t = bag % T;
+      const TabDesc td = tab(t);
+      u64 start; u32 n;
+      bag_span(bag, start, n);
+      const bool lact = lane_id() < n;
+      const long long r = lact ? __ldg(idx + start + lane_id()) : 0ll;
+      u64 key = 0; u32 off = 0;
+      const bool a = lookup_key(c, td, lact, r, t, key, off);
+      prefetch_warp(c, a, key, who, sq + k, true);
+    }
   }
 
   // user-grid register budget: 4 CTAs x 8 warps per SM (64 registers per thread).  (A variant
@@ -475,26 +527,60 @@ struct EmbBagWork {
 #endif
   static constexpr int kMinCtas = AGILE_EMB_MIN_CTAS;
 
-  __device__ void run(const DevCtx& c, u32 uidx, u32 nusers) const { run_direct(c, uidx, nusers); }
-
-  __device__ void run_direct(const DevCtx& c, u32 uidx, u32 nusers) const {
-    const u32 lane = lane_id();
+  __device__ void run(const DevCtx& c, u32 uidx, u32 nusers) const {
     const u32 gw = uidx * kCtaWarps + (threadIdx.x >> 5);
-    const u32 nbags = B * T;
     const u32 who = user_who(uidx);
-    const bool lact = lane < L;
-    const u32 depth = pd > kMaxPd ? kMaxPd : pd;
-    u32 misses_local = 0, lookups_local = 0;
-    u32 gpool = 0, gleft = 0;
-    if (prefetch_only) {
-      // batch-level async (AGILE prefetch, gpu_api.py:345-361): submit every missing page of the
-      // batch and return; the service keeps the launch alive until all fills completed.  The
-      // batch's lookups are taken as one flat stream, 32 per warp pass (lane = lookup, coalesced
-      // index loads), so every lane probes — a bag-per-warp walk would idle 32 - L lanes.
+    if (prefetch_only) { run_prefetch(c, gw, who); return; }
+    const u32 nbags = B * T;
+    u32 misses = 0, lookups = 0;
+    u32 cur = grab_block(c);
+    if (pd && cur < nbags) prefetch_block(c, cur, nbags, who, gw);
+    u32 pass = 0;
+    while (cur < nbags) {
+      const u32 nxt = grab_block(c);
+      if (pd && nxt < nbags) prefetch_block(c, nxt, nbags, who, gw + (++pass));
+      for (u32 k = 0; k < kGrab && cur + k < nbags; ++k)
+        if (!pool_bag(c, cur + k, who, gw, misses, lookups)) { cur = nbags; break; }
+      if (aborted(c)) break;
+      cur = nxt;
+    }
+    if (lane_id() == 0) {
+      atomicAdd(&lookups_miss[0], (u64)lookups);
+      atomicAdd(&lookups_miss[1], (u64)misses);
+    }
+  }
+
+  // batch-level async (AGILE prefetch, gpu_api.py:139-162): submit every missing page of the
+  // batch and return; the service keeps the launch alive until all fills completed.  Fixed-L
+  // batches are taken as one flat stream of lookups, 32 per warp pass (lane = lookup, coalesced
+  // index loads), so every lane probes; variable-length bags go bag by bag.
+  __device__ __noinline__ void run_prefetch(const DevCtx& c, u32 gw, u32 who) const {
+    const u32 lane = lane_id();
+    const u32 nbags = B * T;
+    u32 lookups = 0, pass = 0;
+    if (offsets) {
+      while (true) {
+        const u32 first = grab_block(c);
+        if (first >= nbags) break;
+        for (u32 k = 0; k < kGrab && first + k < nbags; ++k) {
+          const u32 bag = first + k, t = bag % T;
+          const TabDesc td = tab(t);
+          u64 start; u32 n;
+          bag_span(bag, start, n);
+          for (u32 c0 = 0; c0 < n; c0 += 32) {
+            const bool lact = c0 + lane < n;
+            u64 key = 0; u32 off = 0;
+            const bool a = lookup_key(c, td, lact, lact ? __ldg(idx + start + c0 + lane) : 0ll, t, key, off);
+            prefetch_warp(c, a, key, who, gw + (++pass), false);
+          }
+          lookups += n;
+        }
+        if (aborted(c)) break;
+      }
+    } else {
       const u64 nlk = (u64)nbags * L;
       u64 base = 0;
       u32 left = 0;
-      u32 pass = 0;
       while (true) {
         if (!left) {
           u64 b = 0;
@@ -510,163 +596,181 @@ struct EmbBagWork {
         u64 key = 0; u32 off = 0;
         bool a = false;
         if (act) {
-          const u32 bag = (u32)(g / L);
-          a = bag_key_of(bag, true, __ldg(idx + g), key, off);
+          const u32 t = (u32)(g / L) % T;
+          a = lookup_key(c, tab(t), true, __ldg(idx + g), t, key, off);
         }
         prefetch_warp(c, a, key, who, gw + (++pass), false);
-        lookups_local += __popc(__ballot_sync(FULL, act));
+        lookups += __popc(__ballot_sync(FULL, act));
         if ((pass & 15u) == 0 && aborted(c)) break;
       }
-      if (lane == 0) atomicAdd(&lookups_miss[0], (u64)lookups_local);
-      return;
     }
-    // ring of grabbed-and-prefetched bags (async mode): the warp always has `depth` future bags'
-    // misses in flight while it sums the oldest one
-    u32 ring[kMaxPd];
-    u32 head = 0, count = 0;
-    for (u32 k = 0; k < depth; ++k) {
-      const u32 nb = grab(c, gpool, gleft);
-      if (nb >= nbags) break;
-      u64 key = 0; u32 off = 0;
-      const bool a = bag_keys(nb, lact, key, off);
-      prefetch_warp(c, a, key, who, gw + k, true);
-      ring[(head + count) % kMaxPd] = nb;
-      ++count;
-    }
-    u32 pass = 0, abort_chk = 0;
-    while (true) {
-      u32 bag;
-      if (depth) {
-        if (!count) break;
-        bag = ring[head];
-        head = (head + 1) % kMaxPd;
-        --count;
-        const u32 nb = grab(c, gpool, gleft);
-        if (nb < nbags) {
-          u64 key = 0; u32 off = 0;
-          const bool a = bag_keys(nb, lact, key, off);
-          prefetch_warp(c, a, key, who, gw + (++pass), true);
-          ring[(head + count) % kMaxPd] = nb;
-          ++count;
+    if (lane == 0) atomicAdd(&lookups_miss[0], (u64)lookups);
+  }
+
+  // Miss path of a chunk: lanes in `need` claim or attach to the fill of their page and wait for
+  // READY; nothing is held meanwhile (a line reassigned under us goes again).  Out of line: the
+  // hot (all-hit) path keeps its registers, the call saves them only when a miss happens.
+  struct Resolved { u64 word; u32 line; u32 ok; };
+  __device__ __noinline__ Resolved resolve_misses(const DevCtx& c, u32 need, u64 key, u32 who, u32 gw, u32 line,
+                                                  u64 word) const {
+    const u32 lane = lane_id();
+    Resolved res;
+    res.ok = 0;
+    Spin sp;
+    while (need) {
+      const bool nm = (need >> lane) & 1u;
+      const Req r = access_warp(c, nm, key, false, who, gw, false);
+      const bool got = nm && (r.kind == R_HIT || r.kind == R_FILLING || r.kind == R_MISS);
+      if (got) line = r.line;
+      u32 wp = __ballot_sync(FULL, got);
+      u32 done = 0;
+      Spin s2;
+      while (wp) {
+        bool rd = false, gone = false;
+        if ((wp >> lane) & 1u) {
+          const u64 w = ld_acquire(&c.tags[line]);
+          if (!tw_live(w) || tw_key(w) != key) gone = true;
+          else if (tw_state(w) == ST_READY || tw_state(w) == ST_MODIFIED) { word = w; rd = true; }
         }
+        done |= __ballot_sync(FULL, rd);
+        wp &= ~__ballot_sync(FULL, rd || gone);
+        if (wp && !s2.again(c, 1024, __LINE__ + 100000 * SPIN_FILE_ID)) break;
+      }
+      need &= ~done;
+      if (aborted(c)) return res;
+      if (need && !done && !sp.again(c, 1024, __LINE__ + 100000 * SPIN_FILE_ID)) return res;
+    }
+    res.line = line;
+    res.word = word;
+    res.ok = aborted(c) ? 0u : 1u;
+    return res;
+  }
+
+  // pool one bag (fp64, 4 dims per lane) and store it; false when the run aborts.  A chunk whose
+  // validation fails restarts the bag (rare: a page was evicted while the warp read it); after 4
+  // failures the bag is pooled row by row, each row validated on its own.
+  __device__ bool pool_bag(const DevCtx& c, u32 bag, u32 who, u32 gw, u32& misses, u32& lookups) const {
+    const u32 lane = lane_id();
+    const u32 b = bag / T, t = bag - b * T;
+    const TabDesc td = tab(t);
+    u64 start; u32 n;
+    bag_span(bag, start, n);
+    const bool dims = lane * 4 < D;
+    double a0, a1, a2, a3;
+    u32 fails = 0;
+    Spin rsp;
+  restart:
+    a0 = a1 = a2 = a3 = 0.0;
+    for (u32 c0 = 0; c0 < n; c0 += 32) {
+      const bool lact = c0 + lane < n;
+      const long long r = lact ? __ldg(idx + start + c0 + lane) : 0ll;
+      u64 key = 0; u32 off = 0;
+      const bool a = lookup_key(c, td, lact, r, t, key, off);
+      const u32 am = __ballot_sync(FULL, a);
+      if (fails == 0) lookups += __popc(am);
+      if (fails >= 4) {
+        const Acc4 r4 = pool_rows_one_by_one(c, am, key, off, who, gw, make_acc4(a0, a1, a2, a3));
+        if (!r4.ok) return false;
+        a0 = r4.v[0]; a1 = r4.v[1]; a2 = r4.v[2]; a3 = r4.v[3];
+        continue;
+      }
+      u32 line = NONE; u64 word = 0;
+      probe_lanes<true>(c, a, key, line, word);
+      const bool ready = a && line != NONE && (tw_state(word) == ST_READY || tw_state(word) == ST_MODIFIED);
+      if (ready && !tw_ref(word)) atomicOr(&c.tags[line], REF_BIT);   // on_hit
+      const u32 need = __ballot_sync(FULL, a && !ready);
+      if (need) {
+        if (fails == 0) misses += __popc(need);
+        const Resolved rs = resolve_misses(c, need, key, who, gw, line, word);
+        if (!rs.ok) return false;
+        line = rs.line;
+        word = rs.word;
+      }
+      // sum the chunk's rows in lookup order, lane owns dims [4*lane, 4*lane+4): 8 row loads
+      // (16 B/lane, 512 B coalesced each at D = 128) in flight per step
+      const u64 rowaddr = a ? (u64)(uintptr_t)(line_ptr(c, line) + off) : 0ull;
+      u32 dep = 0;
+      for (u32 m = am; m; ) {
+        float4 v[8];
+#pragma unroll
+        for (u32 j = 0; j < 8; ++j) {
+          const int src = m ? __ffs(m) - 1 : 0;
+          const u64 ra = __shfl_sync(FULL, rowaddr, src);
+          v[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (m && dims) v[j] = __ldcg(reinterpret_cast<const float4*>(ra) + lane);
+          m &= m - 1;
+        }
+#pragma unroll
+        for (u32 j = 0; j < 8; ++j) {
+          a0 += (double)v[j].x; a1 += (double)v[j].y; a2 += (double)v[j].z; a3 += (double)v[j].w;
+          dep |= __float_as_uint(v[j].x) | __float_as_uint(v[j].w);
+        }
+      }
+      // seqlock validation, once per chunk: the tag re-read's address depends on every row value
+      // of the warp (redux over the lanes), so it is issued after all of them were loaded
+      const u64 z = dep_zero(__reduce_or_sync(FULL, dep));
+      bool bad = false;
+      if (a) bad = ((ld_relaxed(&c.tags[line] + z) ^ word) & IDENT_MASK) != 0;
+      if (__any_sync(FULL, bad)) {
+        ++fails;
+        if (!rsp.again(c, 256, __LINE__ + 100000 * SPIN_FILE_ID)) return false;
+        goto restart;
+      }
+    }
+    uint8_t* o = out + (u64)b * out_row_bytes + td.out_off;
+    if (dims) {
+      if (td.flags & TAB_PARTIAL_F64) {
+        reinterpret_cast<double2*>(o)[2 * lane] = make_double2(a0, a1);
+        reinterpret_cast<double2*>(o)[2 * lane + 1] = make_double2(a2, a3);
       } else {
-        bag = grab(c, gpool, gleft);
-        if (bag >= nbags) break;
+        reinterpret_cast<float4*>(o)[lane] = make_float4((float)a0, (float)a1, (float)a2, (float)a3);
       }
-      if ((++abort_chk & 15u) == 0 && aborted(c)) break;
-      u64 key = 0; u32 off = 0;
-      const bool a = bag_key_of(bag, lact, bag_raw(bag, lact), key, off);
-      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-      bool first = true;
-      u32 fails = 0;
-      Spin rsp;
+    }
+    return true;
+  }
+
+  struct Acc4 { double v[4]; u32 ok; };
+  static __device__ __forceinline__ Acc4 make_acc4(double x, double y, double z, double w) {
+    Acc4 r; r.v[0] = x; r.v[1] = y; r.v[2] = z; r.v[3] = w; r.ok = 1; return r;
+  }
+  __device__ __noinline__ Acc4 pool_rows_one_by_one(const DevCtx& c, u32 am, u64 key, u32 off, u32 who, u32 gw,
+                                                    Acc4 acc) const {
+    const u32 lane = lane_id();
+    double a0 = acc.v[0], a1 = acc.v[1], a2 = acc.v[2], a3 = acc.v[3];
+    acc.ok = 0;
+    for (u32 m = am; m; m &= m - 1) {
+      const u32 l = __ffs(m) - 1;
+      const u64 kl = __shfl_sync(FULL, key, l);
+      const u32 ol = __shfl_sync(FULL, off, l);
+      Spin s3;
       while (true) {
-        // 1. resolve every lookup to a READY line: batched ballot probe, then the miss path
-        //    (claim or find the in-flight fill, wait for it) for the rest
-        u32 line; u64 word;
-        probe_lanes<false>(c, a, key, line, word);
-        bool ready = a && line != NONE && (tw_state(word) == ST_READY || tw_state(word) == ST_MODIFIED);
-        if (ready && !tw_ref(word)) atomicOr(&c.tags[line], REF_BIT);   // on_hit
-        u32 need = __ballot_sync(FULL, a && !ready);
-        if (need && first) misses_local += __popc(need);
-        const bool waited = need != 0;
-        Spin sp;
-        while (need) {
-          const bool nm = (need >> lane) & 1u;
-          const Req r = access_warp(c, nm, key, false, who, gw, false);
-          bool got = nm && (r.kind == R_HIT || r.kind == R_FILLING || r.kind == R_MISS);
-          if (got) { line = r.line; word = r.word; }
-          // wait for the fill; nothing is held meanwhile (a line reassigned under us goes again)
-          u32 wp = __ballot_sync(FULL, got);
-          u32 done = 0;
-          Spin s2;
-          while (wp) {
-            bool rd = false, gone = false;
-            if ((wp >> lane) & 1u) {
-              const u64 w = ld_relaxed(&c.tags[line]);
-              if (!tw_live(w) || tw_key(w) != key) gone = true;
-              else if (tw_state(w) == ST_READY || tw_state(w) == ST_MODIFIED) { word = w; rd = true; }
-            }
-            done |= __ballot_sync(FULL, rd);
-            wp &= ~__ballot_sync(FULL, rd || gone);
-            if (wp && !s2.again(c, 1024, __LINE__ + 100000 * SPIN_FILE_ID)) break;
+        if (aborted(c)) return acc;
+        const Req r = access_warp(c, lane == l, kl, false, who, gw, false);
+        const int kind = __shfl_sync(FULL, r.kind, l);
+        if (kind == R_HIT || kind == R_FILLING || kind == R_MISS) {
+          const u32 ln = __shfl_sync(FULL, r.line, l);
+          u64 w = 0;
+          Spin s4;
+          while (true) {
+            w = ld_acquire(&c.tags[ln]);
+            if (!tw_live(w) || tw_key(w) != kl) break;
+            if (tw_state(w) == ST_READY || tw_state(w) == ST_MODIFIED) break;
+            if (!s4.again(c, 1024, __LINE__ + 100000 * SPIN_FILE_ID)) return acc;
           }
-          need &= ~done;
-          if (aborted(c)) break;
-          if (need && !done && !sp.again(c, 1024, __LINE__ + 100000 * SPIN_FILE_ID)) break;
-        }
-        if (aborted(c)) break;
-        first = false;
-        // hits were confirmed by an acquire load of their READY tag word (probe_lanes); lines
-        // that became READY while we polled them (relaxed) need the fence
-        if (waited) hit_fence();
-        // 2. sum the L rows, lane owns dims [4*lane, 4*lane+4): 8 row loads (16 B/lane, 512 B
-        //    coalesced each) in flight per chunk, rows added in l order (bit-exact with the oracle)
-        acc = make_float4(0.f, 0.f, 0.f, 0.f);
-        const u64 rowaddr = a ? (u64)(uintptr_t)(line_ptr(c, line) + off) : 0ull;
-        for (u32 l0 = 0; l0 < L; l0 += 8) {
-          float4 v[8];
-#pragma unroll
-          for (u32 j = 0; j < 8; ++j) {
-            const u64 ra = __shfl_sync(FULL, rowaddr, (l0 + j) & 31);
-            v[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (l0 + j < L && lane * 4 < D) v[j] = __ldcg(reinterpret_cast<const float4*>(ra) + lane);
-          }
-#pragma unroll
-          for (u32 j = 0; j < 8; ++j) { acc.x += v[j].x; acc.y += v[j].y; acc.z += v[j].z; acc.w += v[j].w; }
-        }
-        // 3. seqlock validation, once per bag: no page changed identity while we read it;
-        //    otherwise (rare) the whole bag is recomputed
-        hit_fence();
-        bool bad = false;
-        if (a) bad = ((ld_relaxed(&c.tags[line]) ^ word) & IDENT_MASK) != 0;
-        if (!__any_sync(FULL, bad)) break;
-        if (++fails >= 4) {
-          // heavy eviction pressure: rows one at a time, each validated on its own (a single page
-          // only has to survive one row read), still summed in l order
-          acc = make_float4(0.f, 0.f, 0.f, 0.f);
-          for (u32 l = 0; l < L && !aborted(c); ++l) {
-            const u64 kl = __shfl_sync(FULL, key, l);
-            const u32 ol = __shfl_sync(FULL, off, l);
-            Spin s3;
-            while (true) {
-              const Req r = access_warp(c, lane == l, kl, false, who, gw, false);
-              const int kind = __shfl_sync(FULL, r.kind, l);
-              if (kind == R_HIT || kind == R_FILLING || kind == R_MISS) {
-                const u32 ln = __shfl_sync(FULL, r.line, l);
-                u64 w = 0;
-                Spin s4;
-                while (true) {
-                  w = ld_acquire(&c.tags[ln]);
-                  if (!tw_live(w) || tw_key(w) != kl) break;
-                  if (tw_state(w) == ST_READY || tw_state(w) == ST_MODIFIED) break;
-                  if (!s4.again(c, 1024, __LINE__ + 100000 * SPIN_FILE_ID)) break;
-                }
-                if (tw_live(w) && tw_key(w) == kl && tw_state(w) >= ST_READY) {
-                  float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-                  if (lane * 4 < D) v = __ldcg(reinterpret_cast<const float4*>(line_ptr(c, ln) + ol) + lane);
-                  fence_acq_rel();
-                  if (((ld_relaxed(&c.tags[ln]) ^ w) & IDENT_MASK) == 0) {
-                    acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
-                    break;
-                  }
-                }
-              }
-              if (!s3.again(c, 1024, __LINE__ + 100000 * SPIN_FILE_ID)) break;
+          if (tw_live(w) && tw_key(w) == kl && tw_state(w) >= ST_READY) {
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (lane * 4 < D) v = __ldcg(reinterpret_cast<const float4*>(line_ptr(c, ln) + ol) + lane);
+            const u64 z = dep_zero(__reduce_or_sync(FULL, __float_as_uint(v.x) | __float_as_uint(v.w)));
+            if (((ld_relaxed(&c.tags[ln] + z) ^ w) & IDENT_MASK) == 0) {
+              a0 += (double)v.x; a1 += (double)v.y; a2 += (double)v.z; a3 += (double)v.w;
+              break;
             }
           }
-          break;
         }
-        if (!rsp.again(c, 256, __LINE__ + 100000 * SPIN_FILE_ID)) break;
+        if (!s3.again(c, 1024, __LINE__ + 100000 * SPIN_FILE_ID)) return acc;
       }
-      lookups_local += L;
-      const u32 b = bag / T, t = bag % T;
-      if (lane * 4 < D) reinterpret_cast<float4*>(out + (u64)b * out_b_stride + (u64)t * out_t_stride)[lane] = acc;
     }
-    if (lane == 0) {
-      atomicAdd(&lookups_miss[0], (u64)lookups_local);
-      atomicAdd(&lookups_miss[1], (u64)misses_local);
-    }
+    return make_acc4(a0, a1, a2, a3);
   }
 };
 

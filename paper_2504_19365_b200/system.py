@@ -201,6 +201,12 @@ class AgileSystem:
         k = {"words": 0, "f32": 1}[kind]
         self._check(self._lib.agile_store_fill(self._ctx, dev, seed, first_blk, n, k), "store_fill")
 
+    def fill_rows(self, dev: int, seed: int, first_blk: int, table: int, row0: int, rows: int, D: int) -> None:
+        """Row-keyed embedding table pages (oracle/pages.py row_floats): rows [row0, row0 + rows)
+        of `table` from page first_blk on, 4096 / (4 D) rows per page."""
+        self._check(self._lib.agile_store_fill_rows(self._ctx, dev, seed, first_blk, table, row0, rows, D),
+                    "store_fill_rows")
+
     def load_image(self, dev: int, path) -> None:
         """BlockStore.load_image (ssd_model.py:84-95) into the attached store; the device's cache
         lines are invalidated and existing store views stay valid."""
@@ -328,6 +334,8 @@ class AgileSystem:
         """Device-tensor embedding-bag (sum pooling) through the page cache; async launch.
         user_ctas bounds the user CTAs of the launch (0 = every resident slot)."""
         import torch
+        if not idx.is_contiguous() or not out.is_contiguous():
+            raise ValueError("embbag: idx and out must be contiguous")
         B, T, L = idx.shape
         D = out.shape[-1]
         st = stream if stream is not None else torch.cuda.current_stream(idx.device).cuda_stream
@@ -335,6 +343,31 @@ class AgileSystem:
                                                 table_rows.data_ptr(), out.data_ptr(), counters.data_ptr(), B, T, L,
                                                 D, out_b_stride, out_t_stride, prefetch_distance, user_ctas, st),
                     "embbag")
+
+    def embbag_sharded(self, idx, tables, out, counters, D, offsets=None, prefetch_distance=0, user_ctas=0,
+                       prefetch_only=False, stream=None, B=None, L=None):
+        """Sharded / variable-length embedding-bag (agile_embbag_sharded): `tables` is a device
+        tensor holding one agile_table_shard (40 B, bench.dlrm.TAB_DTYPE) per table of the launch;
+        `out` is a device buffer whose rows (one per sample) receive each table's pooled vector at
+        its out_offset — fp32, or fp64 partial sums for row-wise pieces.  idx [B, T, L] int64, or
+        with offsets [B*T + 1] a flat index array (pass B)."""
+        import torch
+        for name, t in (("idx", idx), ("tables", tables), ("out", out), ("offsets", offsets)):
+            if t is not None and not t.is_contiguous():
+                raise ValueError(f"embbag_sharded: {name} must be contiguous")
+        T = tables.numel() * tables.element_size() // 40
+        if offsets is None:
+            B, _, L = idx.shape
+            off_ptr = 0
+        else:
+            L = 0
+            off_ptr = offsets.data_ptr()
+        row_bytes = 0 if out is None else out.numel() * out.element_size() // max(1, B)
+        st = stream if stream is not None else torch.cuda.current_stream(idx.device).cuda_stream
+        self._check(self._lib.agile_embbag_sharded(self._ctx, idx.data_ptr(), off_ptr, tables.data_ptr(),
+                                                   0 if out is None else out.data_ptr(), row_bytes,
+                                                   counters.data_ptr(), B, T, L, D, prefetch_distance, user_ctas,
+                                                   1 if prefetch_only else 0, st), "embbag_sharded")
 
     def embbag_prefetch(self, idx, table_key0, table_rows, D, counters, user_ctas=0, stream=None):
         """Pull every page of the batch into the cache (async launch on `stream`)."""

@@ -1,6 +1,8 @@
-"""CPU, world_size 2 over gloo: the sharded DLRM exchange (table-wise -> data-parallel, one
-all_to_all) delivers every rank exactly the global pooled embeddings of its sample slice.  Each
-rank pools its own tables with the CPU oracle (stand-in for its GPU's kernel)."""
+"""CPU, world_size 2 over gloo: the sharded DLRM exchange (TWRW plan -> data-parallel, one
+unpadded all_to_all_single of the kernel's output rows) delivers every rank exactly the global
+pooled embeddings of its sample slice.  Each rank's send buffer is the CPU restatement of K5's
+output bytes (pool_rank_reference: fp32 whole tables, fp64 row-wise partials at the kernel's
+offsets) — the layout the GPU test checks the kernel against."""
 
 import os
 import socket
@@ -10,8 +12,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from oracle.embbag import embbag_reference
-from paper_2504_19365_b200.bench.dlrm import exchange_pooled, layout, make_batch, shard_tables, table_rows
+from oracle.embbag import embbag_rows_reference
+from paper_2504_19365_b200.bench.dlrm import exchange, make_batch, plan_shards, pool_rank_reference, table_rows
 
 SEED, B, L, D = 11, 16, 5, 32
 
@@ -28,19 +30,11 @@ def _worker(rank, world, port, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     rows = table_rows(64 << 20, D, 26)
-    groups, _ = shard_tables(rows, world)
-    mine = groups[rank]
-    idx = make_batch(SEED, 0, rows, B, L, 1.05, True, mine)
-    key0, _ = layout(rows[mine], D)
-    pooled = torch.from_numpy(embbag_reference(SEED, 0, key0, idx, D))
-    got = exchange_pooled(pooled, groups, rank, world)
-    # the global reference for this rank's samples, tables in global order
+    plan = plan_shards(rows, world, D)
     full_idx = make_batch(SEED, 0, rows, B, L, 1.05, True)
-    out = np.zeros((B, 26, D), dtype=np.float32)
-    for g in range(world):
-        k0, _ = layout(rows[groups[g]], D)
-        out[:, groups[g]] = embbag_reference(SEED, 0, k0, full_idx[:, groups[g]], D)
-    exp = out[rank * (B // world):(rank + 1) * (B // world)]
+    send = torch.from_numpy(pool_rank_reference(plan, rank, full_idx[:, plan.rank_tables(rank)], SEED))
+    got = exchange(plan, send, rank, B)
+    exp = embbag_rows_reference(SEED, full_idx, D)[rank * (B // world):(rank + 1) * (B // world)]
     q.put((rank, bool(np.array_equal(got.numpy(), exp))))
     dist.destroy_process_group()
 

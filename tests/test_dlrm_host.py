@@ -2,8 +2,8 @@
 
 import numpy as np
 
-from paper_2504_19365_b200.bench.dlrm import (build_shard, layout, make_batch, shard_tables, table_rows,
-                                              zipf_rows)
+from paper_2504_19365_b200.bench.dlrm import (TAB_DTYPE, combine, layout, make_batch, plan_shards,
+                                              pool_rank_reference, table_rows, zipf_rows)
 
 
 def test_table_rows_criteo_shape_and_budget():
@@ -33,18 +33,60 @@ def test_zipf_rows_bounded_and_skewed():
 def test_make_batch_rank_slices_equal_global():
     rows = table_rows(1 << 30)
     full = make_batch(3, 5, rows, 64, 20, 1.05, True)
-    groups, _ = shard_tables(rows, 4)
-    for g in groups:
-        assert np.array_equal(make_batch(3, 5, rows, 64, 20, 1.05, True, g), full[:, g])
+    plan = plan_shards(rows, 4)
+    for r in range(4):
+        t = plan.rank_tables(r)
+        assert np.array_equal(make_batch(3, 5, rows, 64, 20, 1.05, True, t), full[:, t])
     assert (full < rows[None, :, None]).all()
 
 
-def test_shard_tables_balanced():
-    rows = table_rows(8 << 30)
+def _check_cover(plan, rows):
+    """every row of every table is held by exactly one piece; pieces are page-aligned"""
+    for t in range(len(rows)):
+        ps = sorted((p.row0, p.rows) for q in plan.pieces for p in q if p.table == t)
+        assert ps[0][0] == 0 and sum(n for _, n in ps) == rows[t]
+        for (a, n), (b, _) in zip(ps, ps[1:]):
+            assert a + n == b and a % plan.rpp == 0 and n % plan.rpp == 0
+        assert all(p.partial == (len(ps) > 1) for q in plan.pieces for p in q if p.table == t)
+
+
+def test_plan_covers_and_balances_1tb():
+    """configs[4]: 1 TB of Criteo-shaped tables over 2/4/8 ranks.  Table-wise alone would give one
+    rank 19 of 26 tables at G = 8 (2.4x the mean bytes); TWRW keeps both bytes and lookups within
+    1.15x of the mean."""
+    rows = table_rows(1 << 40)
+    for G in (1, 2, 4, 8):
+        plan = plan_shards(rows, G)
+        _check_cover(plan, rows)
+        bal = plan.balance()
+        assert bal["bytes"] <= 1.15 and bal["lookups"] <= 1.15, (G, bal)
+        descs, first, pages = plan.rank_layout(G - 1)
+        assert descs.dtype == TAB_DTYPE and pages == sum((p.rows + 7) // 8 for p in plan.pieces[G - 1])
+        assert all(d["out_offset"] % 16 == 0 for d in descs)
+
+
+def test_plan_lookup_balance_counted():
+    """lookups counted from generated batches (hashed Zipf 1.05), not assumed proportional to rows"""
+    rows = table_rows(1 << 40)
+    full = make_batch(1, 0, rows, 2048, 20, 1.05, True)
+    counters = {t: (lambda c: (lambda r0, n: float(((c >= r0) & (c < r0 + n)).sum())))(full[:, t].reshape(-1))
+                for t in range(26)}
     for G in (2, 4, 8):
-        groups, owner = shard_tables(rows, G)
-        assert sorted(np.concatenate(groups).tolist()) == list(range(26))
-        load = [rows[g].sum() for g in groups]
-        assert max(load) <= rows.max() + sum(load) / G
-        sh = build_shard(rows, groups[0], 128)
-        assert sh.pages == layout(rows[groups[0]], 128)[1]
+        assert plan_shards(rows, G).balance(counters)["lookups"] <= 1.15
+
+
+def test_combine_replays_single_device_result():
+    """CPU replay of the exchange: rank outputs in the kernel's byte layout, recv = rank-ordered
+    blocks, combine() = the global fp64-exact pooled embeddings."""
+    from oracle.embbag import embbag_rows_reference
+    import torch
+    rows = table_rows(32 << 20, 64, 26)
+    for G in (2, 4):
+        plan = plan_shards(rows, G, 64)
+        full = make_batch(5, 1, rows, 16, 6, 1.05, True)
+        sends = [torch.from_numpy(pool_rank_reference(plan, r, full[:, plan.rank_tables(r)], 9)) for r in range(G)]
+        ref = embbag_rows_reference(9, full, 64)
+        nl = 16 // G
+        for p in range(G):
+            recv = torch.cat([sends[q][p * nl:(p + 1) * nl].reshape(-1) for q in range(G)])
+            assert np.array_equal(combine(plan, recv, nl).numpy(), ref[p * nl:(p + 1) * nl])
