@@ -200,10 +200,30 @@ int agile_bfs(agile_ctx* ctx, const int64_t* row_ptr, uint32_t V, uint32_t sourc
               int32_t* level, uint32_t prefetch_distance, uint64_t* stats, void* stream);
 /* SpMV over a paged CSR (K7; configs[3]): y = alpha * A x + beta for E edges; col int32 and val
  * fp32 paged one page per 1024 edges (val_key0 = UINT64_MAX: unit weights, the PageRank A^T
- * case).  Deterministic summation order.  counters (device u64[2]) += {edges, page misses}. */
+ * case).  Deterministic summation order; exact fp64 products summed in fp64, y rounded once to
+ * fp32.  counters (device u64[2]) += {edges, page misses}. */
 int agile_spmv(agile_ctx* ctx, const int64_t* row_ptr, uint32_t V, uint64_t E, uint64_t col_key0, uint64_t val_key0,
                const float* x, float* y, float alpha, float beta, uint32_t prefetch_distance, uint64_t* counters,
                void* stream);
+/* SpMV over the rows of a 1D vertex partition (configs[3] over N GPUs): rows [0, n_rows) of the
+ * rank's CSR; row_ptr[0] may be > 0 — edge positions [0, row_ptr[0]) belong to the previous
+ * partition and are skipped, so a rank whose col/val pages start at the unpartitioned CSR's page
+ * holding its first edge (positions = global - a page-aligned base) cuts its edges into the same
+ * 1024-edge chunks as one GPU would, and every row sum is formed in the same order.  x has x_len
+ * entries (the global vertex vector, col ids index it).  Products are exact in fp64 and summed in
+ * fp64, y rounded once to fp32; y[r] = alpha * sum + beta, rows without edges get beta. */
+int agile_spmv_rows(agile_ctx* ctx, const int64_t* row_ptr, uint32_t n_rows, uint64_t e_end, uint32_t x_len,
+                    uint64_t col_key0, uint64_t val_key0, const float* x, float* y, float alpha, float beta,
+                    uint32_t prefetch_distance, uint64_t* counters, void* stream);
+/* One top-down BFS level over the frontier vertices a rank owns (1D vertex partition, configs[2]
+ * over N GPUs): row_ptr[v - v0] for owned v (positions into the rank's paged col_idx from
+ * col_key0), frontier[n] ascending global vertex ids, visited / next_bits (global bitmaps,
+ * (V+31)/32 words; next_bits zeroed by the caller) and level[V] (global) updated for every
+ * vertex discovered here; the caller ORs next_bits over ranks (all-gather) to form the next
+ * frontier.  counters (device u64[2]) += {edges expanded, page misses}.  Async launch. */
+int agile_bfs_level(agile_ctx* ctx, const int64_t* row_ptr, uint32_t v0, const int32_t* frontier, uint32_t n,
+                    uint32_t* visited, uint32_t* next_bits, int32_t* level, int32_t cur, uint64_t col_key0,
+                    uint32_t prefetch_distance, uint64_t* counters, void* stream);
 /* number of user CTAs the embbag launch uses (for roofline accounting) */
 int agile_embbag_grid(agile_ctx* ctx, uint32_t* user_ctas, uint32_t* infra_ctas);
 

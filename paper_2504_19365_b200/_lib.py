@@ -54,6 +54,9 @@ SIGNATURES = {
     "agile_embbag_sharded": (_int, [_vp, _vp, _vp, _vp, _vp, _u64, _vp, _u32, _u32, _u32, _u32, _u32, _u32, _int,
                                     _vp]),
     "agile_store_fill_rows": (_int, [_vp, _int, _u64, _u64, _u32, _u64, _u64, _u32]),
+    "agile_spmv_rows": (_int, [_vp, _vp, _u32, _u64, _u32, _u64, _u64, _vp, _vp, C.c_float, C.c_float, _u32, _vp,
+                               _vp]),
+    "agile_bfs_level": (_int, [_vp, _vp, _u32, _vp, _u32, _vp, _vp, _vp, C.c_int32, _u64, _u32, _vp, _vp]),
 }
 
 _lib = None

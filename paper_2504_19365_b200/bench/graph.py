@@ -208,3 +208,161 @@ def run_graph(cfg, kind: str):
                 _, s2 = run_spmv(system, row_ptr, V, E, 0, val_key0, x, 1, pd)
                 res.rows.append(("spmv", cfg.graph_scale, V, E, pd, round(s2["ms"], 3), round(s2["gflops"], 6)))
     return res
+
+
+# ----------------------------------------------------------------------------- multi-GPU (§8(e))
+# 1D vertex partition: rank r owns vertices [v0, v1) = an equal share of V, i.e. their CSR rows and
+# the col_idx (and SpMV value) pages of those rows in its own page store, read through its own
+# cache and queue pairs.  The rank's store starts at the unpartitioned CSR's page holding its first
+# edge (local position = global position - base, base page-aligned), so its edges fall into the
+# same 1024-edge chunks a single GPU uses: every SpMV row sum is formed in the same order and the
+# sharded results are bit-identical to one GPU's.  Exchanges (torch.distributed, NCCL on GPUs):
+#   BFS:      per level, all-gather of every rank's next-frontier bitmap (V/8 bytes), OR-reduced;
+#   PageRank: per iteration, all-gather of the owned slices of x = r / outdeg (4 V / N bytes each).
+
+from dataclasses import dataclass as _dataclass
+
+
+@_dataclass
+class GraphPart:
+    rank: int
+    world: int
+    v0: int
+    v1: int
+    base: int      # page-aligned global edge position of the rank's first stored entry
+    e_end: int     # local end position (global row_ptr[v1] - base)
+
+    @property
+    def pages(self) -> int:
+        return pages_for(self.e_end)
+
+
+def partition_1d(row_ptr_host: np.ndarray, world: int):
+    V = len(row_ptr_host) - 1
+    assert V % (32 * world) == 0, "V must split into word-aligned equal vertex ranges"
+    parts = []
+    for r in range(world):
+        v0, v1 = r * V // world, (r + 1) * V // world
+        e0, e1 = int(row_ptr_host[v0]), int(row_ptr_host[v1])
+        base = e0 - e0 % ENTRIES_PER_PAGE
+        parts.append(GraphPart(r, world, v0, v1, base, e1 - base))
+    return parts
+
+
+def load_part(system, part: GraphPart, row_ptr, col, vals=None):
+    """Write the rank's col (and value) pages into its store; returns (local row_ptr, col_key0,
+    val_key0) — row_ptr local = global[v0 : v1 + 1] - base."""
+    rp = (row_ptr[part.v0:part.v1 + 1] - part.base).contiguous()
+    e1 = part.base + part.e_end
+    nxt = write_paged(system, 0, 0, col[part.base:e1])
+    vk = None
+    if vals is not None:
+        write_paged(system, 0, nxt, vals[part.base:e1])
+        vk = nxt
+    return rp, 0, vk
+
+
+def bits_to_ids(words, offset: int = 0):
+    """Ascending vertex ids of the set bits of an int32 bitmap (bit k of word w = vertex 32 w + k)."""
+    import torch
+    w = words.to(torch.int64) & 0xFFFFFFFF
+    nz = torch.nonzero(w).flatten()
+    if nz.numel() == 0:
+        return torch.empty(0, dtype=torch.int32, device=words.device)
+    ar = torch.arange(32, device=words.device)
+    bits = ((w[nz].unsqueeze(1) >> ar) & 1).bool()
+    ids = (nz.unsqueeze(1) * 32 + ar)[bits]
+    return (ids + offset).to(torch.int32)
+
+
+class BfsRank:
+    """One rank of the partitioned BFS: expands the frontier vertices it owns (agile_bfs_level);
+    visited / level are kept globally on every rank and merged after each level's exchange."""
+
+    def __init__(self, system, part: GraphPart, row_ptr_local, V: int, source: int, prefetch_distance: int = 0,
+                 col_key0: int = 0):
+        import torch
+        dev = row_ptr_local.device
+        self.s, self.part, self.rp, self.V, self.pd, self.ck = system, part, row_ptr_local, V, prefetch_distance, col_key0
+        self.nw = (V + 31) // 32
+        self.visited = torch.zeros(self.nw, dtype=torch.int32, device=dev)
+        self.visited[source // 32] = torch.tensor(1 << (source % 32), dtype=torch.int64).to(torch.int32)
+        self.level = torch.full((V,), -1, dtype=torch.int32, device=dev)
+        self.level[source] = 0
+        own = part.v0 <= source < part.v1
+        self.frontier = torch.tensor([source] if own else [], dtype=torch.int32, device=dev)
+        self.cur = 0
+        self.counters = torch.zeros(2, dtype=torch.int64, device=dev)
+
+    def expand(self):
+        import torch
+        nb = torch.zeros(self.nw, dtype=torch.int32, device=self.rp.device)
+        if self.frontier.numel():
+            self.s.bfs_level(self.rp, self.part.v0, self.frontier, self.visited, nb, self.level, self.cur, self.ck,
+                             self.pd, self.counters)
+        return nb
+
+    def merge(self, nb_global) -> int:
+        new = nb_global & ~self.visited
+        self.visited |= nb_global
+        ids = bits_to_ids(new)
+        if ids.numel():
+            self.level[ids.long()] = self.cur + 1
+        w0, w1 = self.part.v0 // 32, (self.part.v1 + 31) // 32
+        self.frontier = bits_to_ids(nb_global[w0:w1], self.part.v0)
+        self.cur += 1
+        return int(bits_to_ids(nb_global).numel())
+
+
+def _or_reduce(stack):
+    import functools
+    import torch
+    return functools.reduce(torch.bitwise_or, list(stack))
+
+
+def bfs_partitioned(ranks, allgather=None):
+    """Level-synchronous BFS over partition ranks.  `ranks`: this process's rank objects — one
+    (multi-process: allgather = torch.distributed all-gather of a tensor into [world, ...]) or all
+    of them (single process: the all-gather is the list itself).  Returns levels run."""
+    levels = 0
+    while True:
+        nbs = [r.expand() for r in ranks]
+        gathered = allgather(nbs[0]) if allgather is not None else nbs
+        nb = _or_reduce(gathered)
+        levels += 1
+        n = [r.merge(nb) for r in ranks][0]
+        if n == 0:
+            return levels
+
+
+class PagerankRank:
+    """One rank of the partitioned PageRank: r over its owned vertices, SpMV over its rows."""
+
+    def __init__(self, system, part: GraphPart, row_ptr_local, V: int, outdeg, d: float = 0.85,
+                 prefetch_distance: int = 0, col_key0: int = 0):
+        import torch
+        dev = row_ptr_local.device
+        self.s, self.part, self.rp, self.V, self.d, self.pd, self.ck = system, part, row_ptr_local, V, d, prefetch_distance, col_key0
+        n = part.v1 - part.v0
+        self.r = torch.full((n,), 1.0 / V, dtype=torch.float32, device=dev)
+        self.y = torch.empty_like(self.r)
+        od = outdeg[part.v0:part.v1]
+        self.inv = torch.where(od > 0, 1.0 / od.clamp(min=1).float(), torch.zeros_like(self.r))
+        self.counters = torch.zeros(2, dtype=torch.int64, device=dev)
+
+    def x_local(self):
+        return self.r * self.inv
+
+    def step(self, x_global):
+        self.s.spmv_rows(self.rp, self.part.v1 - self.part.v0, self.part.e_end, self.V, self.ck, None, x_global,
+                         self.y, self.d, (1 - self.d) / self.V, self.pd, self.counters)
+        self.r, self.y = self.y, self.r
+
+
+def pagerank_partitioned(ranks, iters: int, allgather=None):
+    import torch
+    for _ in range(iters):
+        xs = [r.x_local() for r in ranks]
+        x = torch.cat(list(allgather(xs[0]))) if allgather is not None else torch.cat(xs)
+        for r in ranks:
+            r.step(x)

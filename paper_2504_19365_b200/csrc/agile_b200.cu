@@ -1049,9 +1049,10 @@ T* scratch(agile_ctx* ctx, const char* name, size_t count) {
 }
 
 // deg[i] = out-degree of frontier vertex i (deg[n] = 0), for the exclusive scan into eoff
-__global__ void frontier_degree_kernel(const long long* row_ptr, const int* f, uint32_t n, long long* deg) {
+__global__ void frontier_degree_kernel(const long long* row_ptr, const int* f, uint32_t n, long long* deg,
+                                       uint32_t v0) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i <= n; i += (uint64_t)gridDim.x * blockDim.x)
-    deg[i] = i < n ? row_ptr[f[i] + 1] - row_ptr[f[i]] : 0;
+    deg[i] = i < n ? row_ptr[f[i] - (int)v0 + 1] - row_ptr[f[i] - (int)v0] : 0;
 }
 
 __global__ void popc_kernel(const uint32_t* bits, uint32_t nw, uint32_t* cnt) {
@@ -1080,20 +1081,20 @@ __global__ void fill_f32_kernel(float* y, uint64_t n, float v) {
 
 // rows crossing chunk boundaries: the chunk where the row starts walks the following chunks'
 // partials in chunk order (deterministic), then writes y
-__global__ void spmv_fixup_kernel(const long long* row_ptr, const uint32_t* last_row, const float* part_first,
-                                  const float* part_last, uint64_t nch, uint64_t E, float alpha, float beta, float* y) {
+__global__ void spmv_fixup_kernel(const long long* row_ptr, const uint32_t* last_row, const double* part_first,
+                                  const double* part_last, uint64_t nch, uint64_t E, float alpha, float beta, float* y) {
   for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < nch; c += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t r = last_row[c];
     if (r == 0xffffffffu) continue;
     const long long rend = row_ptr[r + 1];
-    float s = part_last[c];
+    double s = part_last[c];
     for (uint64_t c2 = c + 1; c2 < nch; ++c2) {
       s += part_first[c2];
       const uint64_t ce = (c2 + 1) * SpmvWork::kChunk;
       const long long e1 = (long long)(ce < E ? ce : E);
       if (rend <= e1) break;
     }
-    y[r] = alpha * s + beta;
+    y[r] = (float)((double)alpha * s + (double)beta);
   }
 }
 
@@ -1144,12 +1145,13 @@ int agile_bfs(agile_ctx* ctx, const int64_t* row_ptr, uint32_t V, uint32_t sourc
   uint32_t n = 1, levels = 0;
   int cur = 0;
   while (n) {
-    frontier_degree_kernel<<<grid_for((uint64_t)n + 1), 256, 0, st>>>(reinterpret_cast<const long long*>(row_ptr), fa, n, deg);
+    frontier_degree_kernel<<<grid_for((uint64_t)n + 1), 256, 0, st>>>(reinterpret_cast<const long long*>(row_ptr), fa, n, deg, 0u);
     size_t tb = tb1;
     CK(cub::DeviceScan::ExclusiveSum(tmp, tb, deg, eoff, (int64_t)n + 1, st));
     CK(cudaMemsetAsync(next_bits, 0, (size_t)nw * 4, st));
     BfsWork w;
     w.row_ptr = reinterpret_cast<const long long*>(row_ptr);
+    w.v0 = 0;
     w.frontier = fa;
     w.eoff = eoff;
     w.n = n;
@@ -1196,21 +1198,29 @@ int agile_bfs(agile_ctx* ctx, const int64_t* row_ptr, uint32_t V, uint32_t sourc
 int agile_spmv(agile_ctx* ctx, const int64_t* row_ptr, uint32_t V, uint64_t E, uint64_t col_key0, uint64_t val_key0,
                const float* x, float* y, float alpha, float beta, uint32_t prefetch_distance, uint64_t* counters,
                void* stream) {
-  if (!ctx || !row_ptr || !x || !y || !counters || !V) return fail(ctx, AGILE_E_ARG, "null spmv arg");
+  return agile_spmv_rows(ctx, row_ptr, V, E, V, col_key0, val_key0, x, y, alpha, beta, prefetch_distance, counters,
+                         stream);
+}
+
+int agile_spmv_rows(agile_ctx* ctx, const int64_t* row_ptr, uint32_t n_rows, uint64_t e_end, uint32_t x_len,
+                    uint64_t col_key0, uint64_t val_key0, const float* x, float* y, float alpha, float beta,
+                    uint32_t prefetch_distance, uint64_t* counters, void* stream) {
+  if (!ctx || !row_ptr || !x || !y || !counters || !n_rows || !x_len) return fail(ctx, AGILE_E_ARG, "null spmv arg");
   CK(cudaSetDevice(ctx->device));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  const uint64_t nch = (E + SpmvWork::kChunk - 1) / SpmvWork::kChunk;
-  float* pf = scratch<float>(ctx, "spmv.first", nch);
-  float* pl = scratch<float>(ctx, "spmv.last", nch);
+  const uint64_t nch = (e_end + SpmvWork::kChunk - 1) / SpmvWork::kChunk;
+  double* pf = scratch<double>(ctx, "spmv.first", nch);
+  double* pl = scratch<double>(ctx, "spmv.last", nch);
   uint32_t* lr = scratch<uint32_t>(ctx, "spmv.lastrow", nch);
   if (!pf || !pl || !lr) return fail(ctx, AGILE_E_CUDA, "spmv scratch allocation failed");
-  fill_f32_kernel<<<grid_for(V), 256, 0, st>>>(y, V, beta);   // rows without edges: alpha * 0 + beta
+  fill_f32_kernel<<<grid_for(n_rows), 256, 0, st>>>(y, n_rows, beta);   // rows without edges: alpha * 0 + beta
   if (!nch) return 0;
   CK(cudaMemsetAsync(lr, 0xff, nch * 4, st));
   SpmvWork w;
   w.row_ptr = reinterpret_cast<const long long*>(row_ptr);
-  w.V = V;
-  w.E = E;
+  w.V = n_rows;
+  w.nx = x_len;
+  w.E = e_end;
   w.x = x;
   w.y = y;
   w.alpha = alpha;
@@ -1227,10 +1237,46 @@ int agile_spmv(agile_ctx* ctx, const int64_t* row_ptr, uint32_t V, uint64_t E, u
   const uint32_t users = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(full, (nch + kCtaWarps - 1) / kCtaWarps));
   int rc = launch(ctx, w, users, st);
   if (rc) return rc;
-  spmv_fixup_kernel<<<grid_for(nch), 256, 0, st>>>(reinterpret_cast<const long long*>(row_ptr), lr, pf, pl, nch, E,
-                                                     alpha, beta, y);
+  spmv_fixup_kernel<<<grid_for(nch), 256, 0, st>>>(reinterpret_cast<const long long*>(row_ptr), lr, pf, pl, nch,
+                                                     e_end, alpha, beta, y);
   CK(cudaGetLastError());
   return 0;
+}
+
+int agile_bfs_level(agile_ctx* ctx, const int64_t* row_ptr, uint32_t v0, const int32_t* frontier, uint32_t n,
+                    uint32_t* visited, uint32_t* next_bits, int32_t* level, int32_t cur, uint64_t col_key0,
+                    uint32_t prefetch_distance, uint64_t* counters, void* stream) {
+  if (!ctx || !row_ptr || !visited || !next_bits || !level || !counters || (n && !frontier))
+    return fail(ctx, AGILE_E_ARG, "null bfs_level arg");
+  if (!n) return 0;
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  long long* deg = scratch<long long>(ctx, "bfsl.deg", (size_t)n + 1);
+  long long* eoff = scratch<long long>(ctx, "bfsl.eoff", (size_t)n + 1);
+  size_t tb = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tb, deg, eoff, (int64_t)n + 1);
+  void* tmp = scratch<uint8_t>(ctx, "bfsl.cubtmp", tb);
+  if (!deg || !eoff || !tmp) return fail(ctx, AGILE_E_CUDA, "bfs_level scratch allocation failed");
+  frontier_degree_kernel<<<grid_for((uint64_t)n + 1), 256, 0, st>>>(reinterpret_cast<const long long*>(row_ptr),
+                                                                     frontier, n, deg, v0);
+  CK(cub::DeviceScan::ExclusiveSum(tmp, tb, deg, eoff, (int64_t)n + 1, st));
+  BfsWork w;
+  w.row_ptr = reinterpret_cast<const long long*>(row_ptr);
+  w.v0 = v0;
+  w.frontier = frontier;
+  w.eoff = eoff;
+  w.n = n;
+  w.visited = visited;
+  w.next_bits = next_bits;
+  w.level = level;
+  w.cur = cur;
+  w.col_key0 = col_key0;
+  w.pd = prefetch_distance;
+  w.counters = reinterpret_cast<u64*>(counters);
+  const uint32_t full = resident_ctas<BfsWork>(ctx);
+  const uint64_t est = (uint64_t)n * 64 / BfsWork::kChunk + 1;
+  const uint32_t users = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(full, (est + kCtaWarps - 1) / kCtaWarps));
+  return launch(ctx, w, users, st);
 }
 
 int agile_embbag_host_submit(agile_ctx* ctx, const int64_t* idx, const uint64_t* table_key0,

@@ -658,6 +658,7 @@ struct EmbBagWork {
     const bool dims = lane * 4 < D;
     double a0, a1, a2, a3;
     u32 fails = 0;
+    u32 counted = 0;   // chunks below this position were counted (a restart does not count twice)
     Spin rsp;
   restart:
     a0 = a1 = a2 = a3 = 0.0;
@@ -667,7 +668,11 @@ struct EmbBagWork {
       u64 key = 0; u32 off = 0;
       const bool a = lookup_key(c, td, lact, r, t, key, off);
       const u32 am = __ballot_sync(FULL, a);
-      if (fails == 0) lookups += __popc(am);
+      const bool first_visit = c0 >= counted;
+      if (first_visit) {
+        lookups += __popc(am);
+        counted = c0 + 32;
+      }
       if (fails >= 4) {
         const Acc4 r4 = pool_rows_one_by_one(c, am, key, off, who, gw, make_acc4(a0, a1, a2, a3));
         if (!r4.ok) return false;
@@ -680,7 +685,7 @@ struct EmbBagWork {
       if (ready && !tw_ref(word)) atomicOr(&c.tags[line], REF_BIT);   // on_hit
       const u32 need = __ballot_sync(FULL, a && !ready);
       if (need) {
-        if (fails == 0) misses += __popc(need);
+        if (first_visit) misses += __popc(need);
         const Resolved rs = resolve_misses(c, need, key, who, gw, line, word);
         if (!rs.ok) return false;
         line = rs.line;
@@ -913,7 +918,8 @@ __device__ __forceinline__ u32 window_slot(long long ev, long long x) {
 // (pd > 0): a warp grabs pd chunks ahead and prefetches their pages before expanding the oldest
 // (the AGILE prefetch pattern, gpu_api.py:345-361); pd = 0 is the synchronous baseline.
 struct BfsWork {
-  const long long* row_ptr;   // [V+1] (HBM)
+  const long long* row_ptr;   // [rows+1] (HBM), row of vertex v at row_ptr[v - v0]
+  u32 v0;                     // first vertex of the partition (1D vertex partition; 0 = whole graph)
   const int* frontier;        // [n] ascending
   const long long* eoff;      // [n+1], eoff[n] = m
   u32 n;
@@ -930,7 +936,7 @@ struct BfsWork {
   __device__ __forceinline__ void load_window(u64 i, long long& ev, long long& rp) const {
     const u64 wi = i + lane_id();
     ev = wi <= n ? __ldcg(eoff + wi) : LLONG_MAX;
-    rp = wi < n ? __ldg(row_ptr + __ldg(frontier + wi)) : 0;
+    rp = wi < n ? __ldg(row_ptr + (__ldg(frontier + wi) - (int)v0)) : 0;
   }
 
   __device__ void prefetch_chunk(const DevCtx& c, u64 ch, u64 m, u32 who, u32 sq) const {
@@ -1053,15 +1059,16 @@ struct BfsWork {
 // (deterministic run to run).  Async mode (pd > 0) prefetches the pages of the chunks a warp
 // grabbed ahead.
 struct SpmvWork {
-  const long long* row_ptr;   // [V+1]
-  u32 V;
-  u64 E;
+  const long long* row_ptr;   // [V+1]; row_ptr[0] > 0: edges before it belong to another partition
+  u32 V;                      // rows
+  u32 nx;                     // length of x (columns)
+  u64 E;                      // edge positions [0, E) = row_ptr[V]
   const float* x;
   float* y;
   float alpha, beta;
   u64 col_key0, val_key0;
-  float* part_first;          // [nchunks] partial of the chunk's first row if it began earlier
-  float* part_last;           // [nchunks] partial of the chunk's last row if it continues
+  double* part_first;         // [nchunks] partial of the chunk's first row if it began earlier
+  double* part_last;          // [nchunks] partial of the chunk's last row if it continues
   u32* last_row;              // [nchunks]
   u32 pd;
   u64* counters;              // [0] edges, [1] page misses
@@ -1073,6 +1080,7 @@ struct SpmvWork {
     const u32 gw = uidx * kCtaWarps + (threadIdx.x >> 5);
     const u32 who = user_who(uidx);
     const u64 nch = (E + kChunk - 1) / kChunk;
+    const u64 e_lo = (u64)__ldg(row_ptr);
     const bool weighted = val_key0 != ~0ull;
     const u32 depth = pd > kMaxPd ? kMaxPd : pd;
     PageRegs pr;
@@ -1114,7 +1122,10 @@ struct SpmvWork {
         ch = grab();
         if (ch >= nch) break;
       }
-      const u64 e0 = ch * kChunk, e1 = min(E, e0 + kChunk);
+      const u64 e1 = min(E, ch * kChunk + kChunk);
+      const u64 e0 = max(ch * kChunk, e_lo);   // a partition's first chunk may start mid-page
+      const u64 ep = ch * kChunk;              // page base of the chunk
+      if (e0 >= e1) continue;
       edges += e1 - e0;
       const u64 r0 = warp_search_le(row_ptr, 0, V, (long long)e0);
       Spin sp;
@@ -1130,33 +1141,35 @@ struct SpmvWork {
         u64 r = r0;
         long long ev = (r + lane <= V) ? __ldcg(row_ptr + r + lane) : LLONG_MAX;
         u64 carry_row = ~0ull;
-        float carry = 0.f;
+        double carry = 0.0;
         for (u32 p0 = 0; p0 < kChunk / 32; p0 += 4) {
           u32 col[4];
           float val[4], xv[4];
 #pragma unroll
           for (u32 j = 0; j < 4; ++j) {
-            const u64 e = e0 + (p0 + j) * 32 + lane;
+            const u64 e = ep + (p0 + j) * 32 + lane;
             col[j] = 0; val[j] = 1.f;
-            if (e < e1) {
+            if (e >= e0 && e < e1) {
               col[j] = __ldcg(reinterpret_cast<const unsigned int*>(colp) + ((p0 + j) * 32 + lane));
               if (weighted) val[j] = __ldcg(reinterpret_cast<const float*>(valp) + ((p0 + j) * 32 + lane));
             }
           }
 #pragma unroll
           for (u32 j = 0; j < 4; ++j) {
-            const u64 e = e0 + (p0 + j) * 32 + lane;
+            const u64 e = ep + (p0 + j) * 32 + lane;
             // col is speculative until the page is validated below: an index read from a line
             // that changed identity mid-read must not address outside x (the pass is redone)
-            xv[j] = (e < e1 && col[j] < V) ? __ldg(x + col[j]) : 0.f;
+            xv[j] = (e >= e0 && e < e1 && col[j] < nx) ? __ldg(x + col[j]) : 0.f;
           }
 #pragma unroll
           for (u32 j = 0; j < 4; ++j) {
-            const u64 pe0 = e0 + (p0 + j) * 32;
+            const u64 pe0 = ep + (p0 + j) * 32;
             if (pe0 >= e1) break;
+            if (pe0 + 32 <= e0) continue;
             const long long my = (long long)(pe0 + lane);
-            bool unloc = (u64)my < e1 && (u64)my < pe0 + 32;
-            const float v0 = unloc ? val[j] * xv[j] : 0.f;
+            bool unloc = (u64)my >= e0 && (u64)my < e1;
+            // fp64: the product of two fp32 is exact, the sum is rounded once to fp32 at the end
+            const double v0 = unloc ? (double)val[j] * (double)xv[j] : 0.0;
             // sub-rounds: the lanes whose edge the 31-row window covers (normally all of them)
             while (__any_sync(FULL, unloc)) {
               const long long x0 = __shfl_sync(FULL, my, __ffs(__ballot_sync(FULL, unloc)) - 1);
@@ -1176,14 +1189,14 @@ struct SpmvWork {
               const u32 k = window_slot(ev, my);
               const u64 row = inw ? r + k : ~0ull - lane;   // inactive lanes: distinct sentinels
               const long long rend = __shfl_sync(FULL, ev, k + 1 > 31 ? 31 : k + 1);
-              float v = inw ? v0 : 0.f;
+              double v = inw ? v0 : 0.0;
               const u32 ib = __ballot_sync(FULL, inw);
               const int fl = __ffs(ib) - 1, ll = 31 - __clz(ib);
               if ((int)lane == fl && row == carry_row) v += carry;
-              float sum = v;
+              double sum = v;
 #pragma unroll
               for (u32 d = 1; d < 32; d <<= 1) {   // segmented inclusive scan, fixed order
-                const float t = __shfl_up_sync(FULL, sum, d);
+                const double t = __shfl_up_sync(FULL, sum, d);
                 const u64 rr = __shfl_up_sync(FULL, row, d);
                 if (lane >= d && rr == row) sum += t;
               }
@@ -1205,7 +1218,7 @@ struct SpmvWork {
                   part_last[ch] = sum;                      // continues into later chunks
                   last_row[ch] = (u32)row;
                 } else {
-                  y[row] = alpha * sum + beta;              // wholly inside this chunk
+                  y[row] = (float)((double)alpha * sum + (double)beta);   // wholly inside this chunk
                 }
               }
               unloc = unloc && !inw;

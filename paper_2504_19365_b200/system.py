@@ -429,6 +429,30 @@ class AgileSystem:
                                          counters.data_ptr(), st), "spmv")
         return counters
 
+    def spmv_rows(self, row_ptr, n_rows, e_end, x_len, col_key0, val_key0, x, y, alpha=1.0, beta=0.0,
+                  prefetch_distance=0, counters=None, stream=None):
+        """SpMV over the rows of a 1D vertex partition (agile_spmv_rows): row_ptr[0] may be > 0
+        (positions before it belong to the previous partition); x has x_len entries."""
+        import torch
+        st = stream if stream is not None else torch.cuda.current_stream(row_ptr.device).cuda_stream
+        if counters is None:
+            counters = torch.zeros(2, dtype=torch.int64, device=row_ptr.device)
+        vk = (1 << 64) - 1 if val_key0 is None else val_key0
+        self._check(self._lib.agile_spmv_rows(self._ctx, row_ptr.data_ptr(), n_rows, e_end, x_len, col_key0, vk,
+                                              x.data_ptr(), y.data_ptr(), float(alpha), float(beta),
+                                              prefetch_distance, counters.data_ptr(), st), "spmv_rows")
+        return counters
+
+    def bfs_level(self, row_ptr, v0, frontier, visited, next_bits, level, cur, col_key0, prefetch_distance=0,
+                  counters=None, stream=None):
+        """One BFS level over the owned frontier of a 1D vertex partition (agile_bfs_level)."""
+        import torch
+        st = stream if stream is not None else torch.cuda.current_stream(row_ptr.device).cuda_stream
+        n = frontier.numel()
+        self._check(self._lib.agile_bfs_level(self._ctx, row_ptr.data_ptr(), v0, frontier.data_ptr() if n else 0, n,
+                                              visited.data_ptr(), next_bits.data_ptr(), level.data_ptr(), cur,
+                                              col_key0, prefetch_distance, counters.data_ptr(), st), "bfs_level")
+
     def embbag_grid(self):
         u, i = C.c_uint32(), C.c_uint32()
         self._check(self._lib.agile_embbag_grid(self._ctx, C.byref(u), C.byref(i)), "embbag_grid")
