@@ -62,6 +62,12 @@ const char* agile_last_error(agile_ctx* ctx);
  * engine_warps, service_warps, infra_ctas, launch mode (0 split, 1 fused) */
 int agile_geometry(agile_ctx* ctx, uint64_t* out, int n);
 
+/* Launch mode of later runs: 0 split (infra grid + PDL user grid), 1 fused (one grid, roles by
+ * arrival ticket), 2 split with solo users (profiling: when a kernel-serialising tool keeps the
+ * user grid from starting beside the infra grid, the infra grid leaves after 100 ms and the user
+ * grid runs alone — an all-hit replay needs neither engine nor service). */
+int agile_set_launch_mode(agile_ctx* ctx, int mode);
+
 /* Backing store (BlockStore, ssd_model.py:61-101): pinned + GPU-mapped host memory, caller-owned
  * when host_ptr != NULL (registered), else context-owned and zeroed.  image_path (optional) is a
  * raw little-endian block image, offset = blk * 4096, short tail zero-padded (load_image). */
@@ -126,6 +132,14 @@ int agile_write_blocks(agile_ctx* ctx, const uint32_t* dev, const uint64_t* blk,
 /* SoftwareCache.evict per block (software_cache.py:268-281): outcome[i] 0 = RESET (the READY line
  * was dropped), 1 = DEFERRED (busy, pinned or modified), 2 = not resident. */
 int agile_evict_blocks(agile_ctx* ctx, const uint32_t* dev, const uint64_t* blk, int64_t n, int8_t* outcome);
+
+/* AgileApi.array_get (gpu_api.py:250-278), n elements at once, host arrays: element idx[i] of
+ * device dev[i] viewed as a little-endian array of elem_size-byte elements (elem_size must divide
+ * 4096, else AGILE_E_ARG = ValueError; a block past the store raises AGILE_E_OUT_OF_RANGE).  Each
+ * element is read through the cache (hit, attach to a fill in flight, or miss + fill) and its raw
+ * bytes land at out + i * elem_size. */
+int agile_array_get(agile_ctx* ctx, const uint32_t* dev, const uint64_t* idx, int64_t n, uint32_t elem_size,
+                    void* out);
 
 /* Gather epochs (bench/sweeps.py:39-88): keys[tasks][epochs][gathers]; values = u32 element 0
  * of every gathered block; epoch_t[2] = start/end. */

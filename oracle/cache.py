@@ -72,3 +72,31 @@ def reference_clock(cache_size: int, accesses):
     (tests/test_software_cache.py:164-185): eviction sequence of a fully associative clock."""
     _, v = clock_sequence([(0, b) for b in accesses], cache_size, cache_size)
     return [k[1] for _, k in v]
+
+
+def modulo_sequence(accesses, lines: int, ways: int | None = None):
+    """ModuloPolicy (software_cache.py:129-143) per set: a miss of (dev, blk) evicts way
+    (dev * 7919 + blk) mod W of the key's set (set_of above; with one set, W = lines, this is the
+    reference's direct-mapped placement over the whole cache).  Serialized mode: the home way is
+    always available, so busy_eviction_choice never matters.  Same return shape as
+    clock_sequence."""
+    ways = lines if not ways else ways
+    assert lines % ways == 0
+    sets = lines // ways
+    slot = [None] * lines
+    where = {}
+    outcomes, victims = [], []
+    for i, key in enumerate(accesses):
+        key = (int(key[0]), int(key[1]))
+        if key in where:
+            outcomes.append("hit")
+            continue
+        outcomes.append("miss")
+        chosen = set_of(key[0], key[1], sets) * ways + (key[0] * 7919 + key[1]) % ways
+        old = slot[chosen]
+        if old is not None:
+            victims.append((i, old))
+            del where[old]
+        slot[chosen] = key
+        where[key] = chosen
+    return outcomes, victims

@@ -467,7 +467,7 @@ int agile_create(const char* config_text, int cuda_device, agile_ctx** out) {
   if ((uint64_t)d.num_devices * d.pairs_per_device > 65535) return fail(ctx, AGILE_E_CONFIG, "too many queue pairs");
   if (lines % ways) return fail(ctx, AGILE_E_CONFIG, "cache.lines must be a multiple of cache.ways");
   if (lines >= (1ull << 32) - 1) return fail(ctx, AGILE_E_CONFIG, "cache too large");
-  if (policy != "clock") return fail(ctx, AGILE_E_CONFIG, "cache.policy: only 'clock' (set-associative clock) on the B200 path");
+  if (policy != "clock" && policy != "modulo") return fail(ctx, AGILE_E_CONFIG, "unknown cache policy '" + policy + "'");
   if (busy != "wait" && busy != "find_another") return fail(ctx, AGILE_E_CONFIG, "cache.busy_choice must be wait|find_another");
   if (cfg.b("share_table.enabled", false)) return fail(ctx, AGILE_E_CONFIG, "share_table.enabled=true is not supported on the B200 path (SURVEY 8(f))");
   if (cfg.u("device.parallelism", 16) > 32 * kMaxChanPerLane) return fail(ctx, AGILE_E_CONFIG, "device.parallelism must be <= 256");
@@ -492,6 +492,8 @@ int agile_create(const char* config_text, int cuda_device, agile_ctx** out) {
   d.watchdog_ns = std::max<uint64_t>(budget, 1000000) * 4000ull;   // events -> ~ns budget (>= 4 s)
   if (d.watchdog_ns > 60ull * 1000000000ull) d.watchdog_ns = 60ull * 1000000000ull;
   d.user_start_ns = d.watchdog_ns;
+  d.policy = policy == "modulo" ? POL_MODULO : POL_CLOCK;   // system.py:23-31 _make_policy
+  d.find_another = busy == "find_another" ? 1u : 0u;
   d.solo_ok = 0;
   if (const char* so = getenv("AGILE_SOLO_USERS")) {
     // profiling mode: a split launch whose user grid cannot start beside the infra grid (ncu
@@ -855,6 +857,41 @@ int agile_evict_blocks(agile_ctx* ctx, const uint32_t* dev, const uint64_t* blk,
   int rc = launch(ctx, w, 1, ctx->stream);
   if (!rc) rc = agile_sync(ctx, ctx->stream);
   if (!rc) CK(cudaMemcpy(outcome, d_out, n, cudaMemcpyDeviceToHost));
+  return rc;
+}
+
+int agile_set_launch_mode(agile_ctx* ctx, int mode) {
+  if (!ctx || mode < 0 || mode > 2) return fail(ctx, AGILE_E_ARG, "launch mode must be 0 (split), 1 (fused) or 2 (split, solo users)");
+  ctx->fused = mode == 1;
+  ctx->d.solo_ok = mode == 2 ? 1u : 0u;
+  ctx->d.user_start_ns = mode == 2 ? 100ull * 1000 * 1000 : ctx->d.watchdog_ns;
+  return 0;
+}
+
+int agile_array_get(agile_ctx* ctx, const uint32_t* dev, const uint64_t* idx, int64_t n, uint32_t elem_size,
+                    void* out) {
+  if (!ctx || n < 0 || (n && (!dev || !idx || !out))) return fail(ctx, AGILE_E_ARG, "bad array_get args");
+  if (elem_size == 0 || kBlockBytes % elem_size) return fail(ctx, AGILE_E_ARG, "element size must divide the block size");
+  CK(cudaSetDevice(ctx->device));
+  for (int64_t i = 0; i < n; ++i) {   // AgileApi._check_block (gpu_api.py:122-126)
+    if (dev[i] >= ctx->d.num_devices) return fail(ctx, AGILE_E_OUT_OF_RANGE, "no such device");
+    if (idx[i] > (UINT64_MAX >> 13) || idx[i] * elem_size / kBlockBytes >= ctx->store_blocks[dev[i]])
+      return fail(ctx, AGILE_E_OUT_OF_RANGE, "element out of range");
+  }
+  if (n == 0) return 0;
+  DevTmp tmp;
+  uint32_t* d_dev; uint64_t* d_idx; uint8_t* d_out;
+  CK(tmp.alloc(&d_dev, n * 4));
+  CK(tmp.alloc(&d_idx, n * 8));
+  CK(tmp.alloc(&d_out, (size_t)n * elem_size));
+  CK(cudaMemcpy(d_dev, dev, n * 4, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(d_idx, idx, n * 8, cudaMemcpyHostToDevice));
+  ArrayGetWork w;
+  w.dev = d_dev; w.idx = reinterpret_cast<const u64*>(d_idx); w.n = (u64)n; w.elem_size = elem_size; w.out = d_out;
+  const uint32_t users = (uint32_t)std::min<uint64_t>((n + kCtaThreads - 1) / kCtaThreads, resident_ctas<ArrayGetWork>(ctx));
+  int rc = launch(ctx, w, std::max<uint32_t>(1, users), ctx->stream);
+  if (!rc) rc = agile_sync(ctx, ctx->stream);
+  if (!rc) CK(cudaMemcpy(out, d_out, (size_t)n * elem_size, cudaMemcpyDeviceToHost));
   return rc;
 }
 

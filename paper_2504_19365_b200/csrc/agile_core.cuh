@@ -83,20 +83,76 @@ __device__ __forceinline__ u32 sig_match8(uint4 v, u32 pat) {
   return m;
 }
 
-// kAcquire = false: the confirming tag load is relaxed; the caller issues a fence before it reads
-// the line's bytes (one fence then covers every key of the warp).
+// Probe result of one lane (line = NONE: not resident)
+struct ProbeRes { u64 word; u32 line; };
+
+// Generic batched probe (W > 32, W not a multiple of 8): lanes are split into groups of W (one
+// lane per way) and each group resolves one key per round with a ballot; W > 32 or W not a power
+// of two go one key at a time.  Out of line: the hot paths (W a multiple of 8, <= 32) never carry
+// its registers.
+__device__ __noinline__ ProbeRes probe_lanes_generic(const DevCtx& c, bool active, u64 key) {
+  ProbeRes res;
+  res.line = NONE;
+  res.word = 0;
+  const u32 W = c.ways;
+  const u32 lane = lane_id();
+  const u32 act = __ballot_sync(FULL, active);
+  if (!act) return res;
+  if (W > 32 || (W & (W - 1))) {
+    u32 todo = act;
+    while (todo) {
+      const int src = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const u64 k = __shfl_sync(FULL, key, src);
+      u32 l; u64 w;
+      const bool f = probe_key_warp(c, k, l, w);
+      if (lane == (u32)src && f) { res.line = l; res.word = w; }
+    }
+    return res;
+  }
+  const u32 G = 32 / W;                // keys per round
+  const u32 g = lane / W, way = lane % W;
+  const u32 nact = __popc(act);
+  const u32 my_rank = __popc(act & lanemask_lt());
+  const u32 rounds = (nact + G - 1) / G;
+  const u32 gmask = (W == 32) ? FULL : ((1u << W) - 1);
+  for (u32 r0 = 0; r0 < rounds; ++r0) {
+    const u32 rank = r0 * G + g;
+    const bool valid = rank < nact;
+    const u32 src = valid ? nth_set_bit(act, rank) : 0u;
+    const u64 k = __shfl_sync(FULL, key, src);
+    u64 tw = 0, sb = 0;
+    if (valid) {
+      sb = (u64)set_of(c, k) * W;
+      const u64 t = ld_relaxed(&c.tags[sb + way]);
+      tw = (tw_live(t) && tw_key(t) == k) ? t : 0;
+    }
+    const u32 b = __ballot_sync(FULL, tw != 0);
+    const bool mine = active && (my_rank / G) == r0;
+    const u32 mg = my_rank % G;
+    const u32 bits = (b >> (mg * W)) & gmask;
+    const int hw = bits ? __ffs(bits) - 1 : 0;
+    const u64 wv = __shfl_sync(FULL, tw, mg * W + hw);
+    const u64 base = __shfl_sync(FULL, sb, mg * W + hw);
+    if (mine && bits) { res.line = (u32)(base + hw); res.word = wv; }
+  }
+  return res;
+}
+
+// Lane-per-key probe.  For W a multiple of 8 and <= 32 (every production geometry) each active
+// lane scans its own set's W 16-bit signatures (2W bytes, all loads in flight at once), then
+// confirms candidate ways against the tag word.  kAcquire: the confirming load is an acquire
+// (a READY word read here makes the line's bytes visible to the caller); false: relaxed, the
+// caller orders its reads itself.  A signature lags its tag word only between a claim's CAS and
+// the signature store; a probe that misses in that window takes the miss path, which re-probes
+// the full tags under the set lock, so in-flight de-duplication is unaffected.  Warp-collective
+// (the generic path needs every lane).
 template <bool kAcquire = true>
 __device__ __forceinline__ void probe_lanes(const DevCtx& c, bool active, u64 key, u32& line, u64& word) {
   line = NONE;
   word = 0;
   const u32 W = c.ways;
   if (W <= 32 && (W & 7u) == 0) {
-    // lane-per-key signature probe: each active lane scans its own set's W signatures (2W bytes,
-    // all loads in flight at once), then confirms candidate ways against the tag word with an
-    // acquire load (a READY word read here makes the line's bytes visible to the caller).  A
-    // signature lags its tag word only between a claim's CAS and the signature store; a probe
-    // that misses in that window takes the miss path, which re-probes the full tags under the
-    // set lock, so in-flight de-duplication is unaffected.
     if (active) {
       const u64 base = (u64)set_of(c, key) * W;
       const uint4* sp = reinterpret_cast<const uint4*>(c.sig + base);
@@ -117,60 +173,9 @@ __device__ __forceinline__ void probe_lanes(const DevCtx& c, bool active, u64 ke
     }
     return;
   }
-  const u32 lane = lane_id();
-  const u32 act = __ballot_sync(FULL, active);
-  if (!act) return;
-  if (W > 32 || (W & (W - 1))) {
-    // generic path: one key at a time
-    u32 todo = act;
-    while (todo) {
-      const int src = __ffs(todo) - 1;
-      todo &= todo - 1;
-      const u64 k = __shfl_sync(FULL, key, src);
-      u32 l; u64 w;
-      const bool f = probe_key_warp(c, k, l, w);
-      if (lane == (u32)src && f) { line = l; word = w; }
-    }
-    return;
-  }
-  const u32 G = 32 / W;                // keys per round
-  const u32 g = lane / W, way = lane % W;
-  const u32 nact = __popc(act);
-  const u32 my_rank = __popc(act & lanemask_lt());
-  const u32 rounds = (nact + G - 1) / G;
-  const u32 gmask = (W == 32) ? FULL : ((1u << W) - 1);
-  for (u32 r0 = 0; r0 < rounds; r0 += 8) {
-    u64 tw[8];
-    u64 sb[8];
-#pragma unroll
-    for (u32 j = 0; j < 8; ++j) {
-      const u32 rank = (r0 + j) * G + g;
-      tw[j] = 0;
-      sb[j] = 0;
-      // source lane of this rank (rank-th set bit of act)
-      u32 src = 0;
-      const bool valid = rank < nact;
-      if (valid) src = nth_set_bit(act, rank);
-      const u64 k = __shfl_sync(FULL, key, valid ? src : 0);
-      if (valid && r0 + j < rounds) {
-        sb[j] = (u64)set_of(c, k) * W;
-        const u64 t = ld_relaxed(&c.tags[sb[j] + way]);
-        tw[j] = (tw_live(t) && tw_key(t) == k) ? t : 0;
-      }
-    }
-#pragma unroll
-    for (u32 j = 0; j < 8; ++j) {
-      const u32 b = __ballot_sync(FULL, tw[j] != 0);
-      // the lane owning rank (r0+j)*G + g' reads group g' bits
-      const bool mine = active && (my_rank / G) == (r0 + j);
-      const u32 mg = my_rank % G;
-      const u32 bits = (b >> (mg * W)) & gmask;
-      const int hw = bits ? __ffs(bits) - 1 : 0;
-      const u64 wv = __shfl_sync(FULL, tw[j], mg * W + hw);
-      const u64 base = __shfl_sync(FULL, sb[j], mg * W + hw);
-      if (mine && bits) { line = (u32)(base + hw); word = wv; }
-    }
-  }
+  const ProbeRes r = probe_lanes_generic(c, active, key);
+  line = r.line;
+  word = r.word;
 }
 
 // Clock victim choice over one set held under its lock (ClockPolicy.map semantics,
@@ -202,6 +207,22 @@ __device__ __forceinline__ int clock_pick_vec(u32 W, u32 hand, u32 avail, u32 re
   return v;
 }
 
+// ModuloPolicy.map (software_cache.py:129-143) inside the key's set: try t maps to way
+// (dev * 7919 + blk + t) mod W (with one set of W = lines ways this is the reference's direct-mapped
+// modulo placement over the whole cache).  `avail` = ways that are not BUSY and not pinned.
+// busy_eviction_choice (software_cache.py:366-371): "wait" takes the home way or nothing (the
+// caller retries: the reference parks on that line's ready_wait); "find_another" walks t = 1, 2,
+// .. to the first available way (none in W tries: every way busy -> any_free_wait).  No reference
+// bits, no hand.
+__device__ __forceinline__ int modulo_pick(const DevCtx& c, u64 key, u32 W, u32 avail) {
+  const u32 h = (u32)(((u64)key_dev(key) * 7919ull + key_blk(key)) % W);
+  if (!c.find_another) return ((avail >> h) & 1u) ? (int)h : -1;
+  const u32 fullw = (W == 32) ? FULL : ((1u << W) - 1);
+  const u32 r = h ? (((avail >> h) | (avail << (W - h))) & fullw) : (avail & fullw);
+  if (!r) return -1;
+  return (int)((h + (u32)(__ffs(r) - 1)) % W);
+}
+
 // Serial exact sweep for W > 32 (fully associative parity mode), run by one lane.
 __device__ __forceinline__ int clock_pick_serial(const DevCtx& c, u64 base, u32 W, u32 hand, u32& new_hand,
                                                  u64* cleared_list, u32& ncleared, u32 max_cleared) {
@@ -220,6 +241,18 @@ __device__ __forceinline__ int clock_pick_serial(const DevCtx& c, u64 base, u32 
     return (int)idx;
   }
   new_hand = hand;
+  return -1;
+}
+
+// ModuloPolicy for W > 32, run by one lane (see modulo_pick)
+__device__ __forceinline__ int modulo_pick_serial(const DevCtx& c, u64 base, u32 W, u64 key) {
+  const u64 h = ((u64)key_dev(key) * 7919ull + key_blk(key)) % W;
+  for (u32 t = 0; t < W; ++t) {
+    const u32 idx = (u32)((h + t) % W);
+    const u64 w = ld_relaxed(&c.tags[base + idx]);
+    if (tw_state(w) != ST_BUSY && tw_pins(w) == 0) return (int)idx;
+    if (!c.find_another) return -1;
+  }
   return -1;
 }
 
@@ -299,13 +332,16 @@ __device__ int claim_key_warp(const DevCtx& c, u64 key, u32 pin_n, u32 who, u32&
       if (lane < W) tw = ld_relaxed(&c.tags[base + lane]);
       const u32 avail = __ballot_sync(FULL, lane < W && tw_state(tw) != ST_BUSY && tw_pins(tw) == 0);
       const u32 ref1 = __ballot_sync(FULL, lane < W && tw_ref(tw));
-      v = clock_pick_vec(W, hand, avail, ref1, cleared, new_hand);
+      if (c.policy == POL_MODULO) { v = modulo_pick(c, key, W, avail); new_hand = hand; }
+      else v = clock_pick_vec(W, hand, avail, ref1, cleared, new_hand);
       if (v >= 0) old = __shfl_sync(FULL, tw, v);
     } else {
       int vv = -1;
       u32 nh = hand;
       u32 ncl = 0;
-      if (lane == 0) vv = clock_pick_serial(c, base, W, hand, nh, nullptr, ncl, 0);
+      if (lane == 0)
+        vv = c.policy == POL_MODULO ? modulo_pick_serial(c, base, W, key)
+                                    : clock_pick_serial(c, base, W, hand, nh, nullptr, ncl, 0);
       v = __shfl_sync(FULL, vv, 0);
       new_hand = __shfl_sync(FULL, nh, 0);
       if (v >= 0) old = ld_relaxed(&c.tags[base + v]);
@@ -414,7 +450,8 @@ __device__ int claim_lanes(const DevCtx& c, bool want, u64 key, u32 pin_n, u32 w
         settled = true;
       } else {
         u32 cleared = 0, nh = hand;
-        const int v = clock_pick_vec(W, hand, avail, ref1, cleared, nh);
+        const int v = c.policy == POL_MODULO ? modulo_pick(c, key, W, avail)
+                                             : clock_pick_vec(W, hand, avail, ref1, cleared, nh);
         if (v < 0) {
           kind = R_RETRY;   // every way busy/pinned: wait (any_free_wait, software_cache.py:364-365)
           settled = true;

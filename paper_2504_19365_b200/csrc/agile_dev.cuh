@@ -54,6 +54,9 @@ constexpr int ST_SHIFT = 62;
 constexpr u64 ST_MASK = 3ull << ST_SHIFT;
 constexpr u64 IDENT_MASK = ST_MASK | VER_MASK | KEY_MASK;   // everything a reader validates
 
+// victim-selection plug-ins (CachePolicy, software_cache.py:67-143)
+enum : u32 { POL_CLOCK = 0, POL_MODULO = 1 };
+
 // CacheState (software_cache.py:30-34)
 enum : u32 { ST_INVALID = 0, ST_BUSY = 1, ST_READY = 2, ST_MODIFIED = 3 };
 
@@ -179,6 +182,8 @@ struct DevCtx {
   u32 poll_ns, idle_max_ns;
   u32 trace;
   u32 solo_ok;              // 1: a user grid that never started is not an error (profiling mode)
+  u32 policy;               // victim policy inside a set: POL_CLOCK | POL_MODULO (CachePolicy seam)
+  u32 find_another;         // busy_eviction_choice: 0 wait, 1 find_another (software_cache.py:366-371)
   u64 watchdog_ns;
   u64 user_start_ns;        // the infra grid gives up on a user grid that has not started by then
   // cache

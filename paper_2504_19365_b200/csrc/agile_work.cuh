@@ -308,6 +308,73 @@ struct WriteWork {
   }
 };
 
+// ------------------------------------------------------------------ ArrayGetWork
+// AgileApi.array_get (gpu_api.py:250-278): the device viewed as a little-endian array of
+// elem_size-byte elements; element idx lives in block idx * elem_size / 4096 at byte offset
+// idx * elem_size % 4096 (elem_size divides 4096, so an element never straddles blocks).  One
+// GPU thread per element: read_range (software_cache.py:212-219) = access (hit, attach to the
+// fill in flight, or claim + submit a miss), wait READY, copy the element's bytes, release.  The
+// lane pins only its own line and only once its access succeeded (no hold-and-wait).
+struct ArrayGetWork {
+  const u32* dev;
+  const u64* idx;
+  u64 n;
+  u32 elem_size;
+  uint8_t* out;            // [n][elem_size]
+  __device__ void run(const DevCtx& c, u32 uidx, u32 nusers) const {
+    const u32 lane = lane_id();
+    const u32 who = user_who(uidx);
+    const u32 sq = uidx * kCtaWarps + (threadIdx.x >> 5);
+    for (u64 i0 = (u64)uidx * kCtaThreads; i0 < n; i0 += (u64)nusers * kCtaThreads) {
+      const u64 i = i0 + threadIdx.x;
+      bool pend = i < n;
+      u64 key = 0;
+      u32 off = 0;
+      if (pend) {
+        const u64 byte_off = idx[i] * elem_size;
+        key = make_key(dev[i], byte_off >> kBlockShift);
+        off = (u32)(byte_off & (kBlockBytes - 1));
+      }
+      Spin sp;
+      while (__any_sync(FULL, pend)) {
+        const Req r = access_warp(c, pend, key, true, who, sq, false);
+        const bool pinned = pend && (r.kind == R_HIT || r.kind == R_FILLING || r.kind == R_MISS);
+        u32 wp = __ballot_sync(FULL, pinned);
+        Spin s2;
+        while (wp) {
+          bool rd = false;
+          if ((wp >> lane) & 1u) {
+            const u64 w = ld_acquire(&c.tags[r.line]);
+            rd = tw_state(w) == ST_READY || tw_state(w) == ST_MODIFIED;
+          }
+          wp &= ~__ballot_sync(FULL, rd);
+          if (wp && !s2.again(c, 512, __LINE__ + 100000 * SPIN_FILE_ID)) break;
+        }
+        if (pinned) {
+          const uint8_t* src = line_ptr(c, r.line) + off;
+          uint8_t* dst = out + i * elem_size;
+          if ((elem_size & 15u) == 0) {
+            for (u32 k = 0; k < elem_size; k += 16)
+              *reinterpret_cast<uint4*>(dst + k) = __ldcg(reinterpret_cast<const uint4*>(src + k));
+          } else if ((elem_size & 7u) == 0) {
+            for (u32 k = 0; k < elem_size; k += 8)
+              *reinterpret_cast<u64*>(dst + k) = __ldcg(reinterpret_cast<const u64*>(src + k));
+          } else if ((elem_size & 3u) == 0) {
+            for (u32 k = 0; k < elem_size; k += 4)
+              *reinterpret_cast<u32*>(dst + k) = __ldcg(reinterpret_cast<const u32*>(src + k));
+          } else {
+            for (u32 k = 0; k < elem_size; ++k) dst[k] = src[k];
+          }
+          unpin_line(c, r.line, 1);
+        }
+        pend = pend && r.kind == R_RETRY;
+        if (aborted(c)) return;
+        if (__any_sync(FULL, pend) && !sp.again(c, 1024, __LINE__ + 100000 * SPIN_FILE_ID)) return;
+      }
+    }
+  }
+};
+
 // ------------------------------------------------------------------ GatherWork (queue/cache sweeps)
 // One warp = 32 tasks in lockstep (run_workload(..., warp_size=32)). Per epoch each task
 // prefetches its gather set (warp-coalesced) and then array_gets element 0 of every block.
@@ -525,6 +592,13 @@ struct EmbBagWork {
 #ifndef AGILE_EMB_MIN_CTAS
 #define AGILE_EMB_MIN_CTAS 4
 #endif
+#ifndef AGILE_K5_RIF
+#define AGILE_K5_RIF 8   // row loads in flight per lane in pool_block
+#endif
+  static constexpr u32 kRif = AGILE_K5_RIF;
+#ifndef AGILE_K5_BAG
+#define AGILE_K5_BAG 1   // 1: the bag-at-a-time pooling (pool_bag); 0: block passes (pool_block)
+#endif
   static constexpr int kMinCtas = AGILE_EMB_MIN_CTAS;
 
   __device__ void run(const DevCtx& c, u32 uidx, u32 nusers) const {
@@ -539,8 +613,12 @@ struct EmbBagWork {
     while (cur < nbags) {
       const u32 nxt = grab_block(c);
       if (pd && nxt < nbags) prefetch_block(c, nxt, nbags, who, gw + (++pass));
+#if AGILE_K5_BAG
       for (u32 k = 0; k < kGrab && cur + k < nbags; ++k)
         if (!pool_bag(c, cur + k, who, gw, misses, lookups)) { cur = nbags; break; }
+#else
+      if (!pool_block(c, cur, min(kGrab, nbags - cur), who, gw, misses, lookups)) break;
+#endif
       if (aborted(c)) break;
       cur = nxt;
     }
@@ -732,6 +810,228 @@ struct EmbBagWork {
       }
     }
     return true;
+  }
+
+  // Pool a block of nb consecutive bags as ONE flat run of lookups (the block's indices are
+  // contiguous in idx, fixed L or offsets alike), 32 lookups per pass with every lane busy: a
+  // pass resolves its 32 pages with one signature probe round and one confirming tag round,
+  // then sums its rows in lookup order, 8 row loads (16 B/lane, 512 B coalesced per row) in
+  // flight per step, flushing a bag's pooled vector the moment its last lookup was added.  The
+  // next pass's indices are loaded while this pass works.  Validation (seqlock) once per pass:
+  // the tag re-read's address depends on every row value of the pass, so it is issued after all
+  // of them returned.  A failed validation (a page changed identity mid-read: rare) redoes the
+  // block from its first lookup — already flushed bags are simply rewritten — and after 4
+  // failures the block is pooled row by row, each row validated on its own.
+  __device__ bool pool_block(const DevCtx& c, u32 first, u32 nb, u32 who, u32 gw, u32& misses, u32& lookups) const {
+    const u32 lane = lane_id();
+    u64 s0, s1;
+    long long bend = 0;   // lane k < nb: flat end position of bag first + k
+    if (offsets) {
+      const long long o = lane <= nb ? __ldg(offsets + first + lane) : 0ll;
+      s0 = (u64)__shfl_sync(FULL, o, 0);
+      s1 = (u64)__shfl_sync(FULL, o, nb);
+      bend = __shfl_down_sync(FULL, o, 1);
+      // an empty bag has no lookup to flush it: it pools to zero here
+      const bool empty = lane < nb && bend <= o;
+      u32 em = __ballot_sync(FULL, empty);
+      while (em) {
+        const u32 k = __ffs(em) - 1;
+        em &= em - 1;
+        const u32 bag = first + k, b = bag / T;
+        const TabDesc td = tab(bag - b * T);
+        store_pooled((u64)b * out_row_bytes + td.out_off, td.flags, 0.0, 0.0, 0.0, 0.0);
+      }
+    } else {
+      s0 = (u64)first * L;
+      s1 = s0 + (u64)nb * L;
+    }
+    const bool dims = lane * 4 < D;
+    double a0, a1, a2, a3;
+    u32 fails = 0;
+    u64 counted = s0;   // passes below this position were counted (a redo does not count twice)
+    Spin rsp;
+  restart:
+    a0 = a1 = a2 = a3 = 0.0;
+    long long r_nx = s0 + lane < s1 ? __ldg(idx + s0 + lane) : 0ll;
+    for (u64 q0 = s0; q0 < s1; q0 += 32) {
+      const u64 p = q0 + lane;
+      const bool lact = p < s1;
+      const long long r = r_nx;
+      if (q0 + 32 < s1) r_nx = p + 32 < s1 ? __ldg(idx + p + 32) : 0ll;   // next pass, in flight now
+      // the bag of position p and whether p is its last lookup
+      u32 k;
+      bool last;
+      block_pos(first, nb, s0, s1, bend, p, k, last);
+      const u32 bag = first + (lact ? k : 0u), b = bag / T, t = bag - b * T;
+      const TabDesc td = tab(t);
+      const u64 obase = (u64)b * out_row_bytes + td.out_off;
+      u64 key = 0; u32 off = 0;
+      const bool a = lookup_key(c, td, lact, r, t, key, off);
+      const u32 am = __ballot_sync(FULL, a);
+      const u32 endm = __ballot_sync(FULL, last);
+      const u32 npos = __popc(__ballot_sync(FULL, lact));   // positions form a prefix of the lanes
+      const bool first_visit = q0 >= counted;
+      if (first_visit) {
+        lookups += __popc(am);
+        counted = q0 + 32;
+      }
+      u32 line = NONE; u64 word = 0;
+      {
+        probe_lanes<true>(c, a, key, line, word);
+        const bool ready = a && line != NONE && (tw_state(word) == ST_READY || tw_state(word) == ST_MODIFIED);
+        if (ready && !tw_ref(word)) atomicOr(&c.tags[line], REF_BIT);   // on_hit
+        const u32 need = __ballot_sync(FULL, a && !ready);
+        if (need) {
+          if (first_visit) misses += __popc(need);
+          const Resolved rs = resolve_misses(c, need, key, who, gw, line, word);
+          if (!rs.ok) return false;
+          line = rs.line;
+          word = rs.word;
+        }
+      }
+      const u64 rowaddr = a ? (u64)(uintptr_t)(line_ptr(c, line) + off) : 0ull;
+      u32 dep = 0;
+      // rows in lookup order as a rolling pipeline: the load of row s + kRif is issued before row
+      // s is added, so kRif row loads are in flight per lane while the adds run
+      float4 v[kRif];
+#pragma unroll
+      for (u32 j = 0; j < kRif; ++j) {
+        const u64 ra = __shfl_sync(FULL, rowaddr, j);
+        v[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (((am >> j) & 1u) && dims) v[j] = __ldcg(reinterpret_cast<const float4*>(ra) + lane);
+      }
+#pragma unroll
+      for (u32 s = 0; s < 32; ++s) {
+        if (s >= npos) break;
+        const float4 x = v[s % kRif];
+        if (s + kRif < 32) {
+          const u32 sn = s + kRif;
+          const u64 ra = __shfl_sync(FULL, rowaddr, sn);
+          v[s % kRif] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (((am >> sn) & 1u) && dims) v[s % kRif] = __ldcg(reinterpret_cast<const float4*>(ra) + lane);
+        }
+        a0 += (double)x.x; a1 += (double)x.y; a2 += (double)x.z; a3 += (double)x.w;
+        dep |= __float_as_uint(x.x) | __float_as_uint(x.w);
+        if ((endm >> s) & 1u) {   // bag complete: store its pooled vector
+          store_pooled(__shfl_sync(FULL, obase, s), __shfl_sync(FULL, td.flags, s), a0, a1, a2, a3);
+          a0 = a1 = a2 = a3 = 0.0;
+        }
+      }
+      // seqlock validation, once per pass: the tag re-read's address depends on every row value
+      // of the pass (redux over the lanes), so it is issued after all of them were loaded
+      const u64 z = dep_zero(__reduce_or_sync(FULL, dep));
+      bool bad = false;
+      if (a) bad = ((ld_relaxed(&c.tags[line] + z) ^ word) & IDENT_MASK) != 0;
+      if (__any_sync(FULL, bad)) {
+        if (++fails >= 4) return pool_block_slow(c, first, nb, s0, s1, bend, counted, who, gw, lookups);
+        if (!rsp.again(c, 256, __LINE__ + 100000 * SPIN_FILE_ID)) return false;
+        goto restart;
+      }
+    }
+    return true;
+  }
+
+  // the bag position info of flat position p of a block (see pool_block)
+  __device__ __forceinline__ void block_pos(u32 first, u32 nb, u64 s0, u64 s1, long long bend, u64 p, u32& k,
+                                            bool& last) const {
+    const bool lact = p < s1;
+    if (offsets) {
+      k = 0;
+      for (u32 j = 0; j < nb; ++j) k += (u64)__shfl_sync(FULL, bend, j) <= p ? 1u : 0u;
+      last = lact && (u64)__shfl_sync(FULL, bend, k < 31 ? k : 31) == p + 1;
+    } else {
+      const u32 rel = (u32)(p - s0);   // < kGrab * L
+      k = rel / L;
+      last = lact && rel - k * L == L - 1;
+    }
+  }
+
+  // Slow path of pool_block: every row read and validated on its own (row_one), bags flushed in
+  // lookup order as in the fast path.  Out of line.
+  __device__ __noinline__ bool pool_block_slow(const DevCtx& c, u32 first, u32 nb, u64 s0, u64 s1, long long bend,
+                                               u64 counted, u32 who, u32 gw, u32& lookups) const {
+    const u32 lane = lane_id();
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    for (u64 q0 = s0; q0 < s1; q0 += 32) {
+      const u64 p = q0 + lane;
+      const bool lact = p < s1;
+      u32 k;
+      bool last;
+      block_pos(first, nb, s0, s1, bend, p, k, last);
+      const long long r = lact ? __ldg(idx + p) : 0ll;
+      const u32 bag = first + (lact ? k : 0u), b = bag / T, t = bag - b * T;
+      const TabDesc td = tab(t);
+      const u64 obase = (u64)b * out_row_bytes + td.out_off;
+      u64 key = 0; u32 off = 0;
+      const bool a = lookup_key(c, td, lact, r, t, key, off);
+      const u32 am = __ballot_sync(FULL, a);
+      const u32 endm = __ballot_sync(FULL, last);
+      const u32 npos = __popc(__ballot_sync(FULL, lact));
+      if (q0 >= counted) lookups += __popc(am);   // passes the fast path never reached
+      for (u32 s = 0; s < npos; ++s) {
+        if ((am >> s) & 1u) {
+          const Row1 r1 = row_one(c, __shfl_sync(FULL, key, s), __shfl_sync(FULL, off, s), who, gw);
+          if (!r1.ok) return false;
+          a0 += (double)r1.v.x; a1 += (double)r1.v.y; a2 += (double)r1.v.z; a3 += (double)r1.v.w;
+        }
+        if ((endm >> s) & 1u) {
+          store_pooled(__shfl_sync(FULL, obase, s), __shfl_sync(FULL, td.flags, s), a0, a1, a2, a3);
+          a0 = a1 = a2 = a3 = 0.0;
+        }
+      }
+    }
+    return true;
+  }
+
+  __device__ __forceinline__ void store_pooled(u64 ob, u32 fl, double a0, double a1, double a2, double a3) const {
+    const u32 lane = lane_id();
+    uint8_t* o8 = out + ob;
+    if (lane * 4 < D) {
+      if (fl & TAB_PARTIAL_F64) {
+        reinterpret_cast<double2*>(o8)[2 * lane] = make_double2(a0, a1);
+        reinterpret_cast<double2*>(o8)[2 * lane + 1] = make_double2(a2, a3);
+      } else {
+        reinterpret_cast<float4*>(o8)[lane] = make_float4((float)a0, (float)a1, (float)a2, (float)a3);
+      }
+    }
+  }
+
+  // one row slice (lane: dims [4*lane, 4*lane+4)) of the lookup (key, off), read and validated on
+  // its own: access (claim or attach on a miss), wait READY, read, re-read the tag identity
+  struct Row1 { float4 v; u32 ok; };
+  __device__ __noinline__ Row1 row_one(const DevCtx& c, u64 kl, u32 ol, u32 who, u32 gw) const {
+    const u32 lane = lane_id();
+    Row1 res;
+    res.v = make_float4(0.f, 0.f, 0.f, 0.f);
+    res.ok = 0;
+    Spin s3;
+    while (true) {
+      if (aborted(c)) return res;
+      const Req r = access_warp(c, lane == 0, kl, false, who, gw, false);
+      const int kind = __shfl_sync(FULL, r.kind, 0);
+      if (kind == R_HIT || kind == R_FILLING || kind == R_MISS) {
+        const u32 ln = __shfl_sync(FULL, r.line, 0);
+        u64 w = 0;
+        Spin s4;
+        while (true) {
+          w = ld_acquire(&c.tags[ln]);
+          if (!tw_live(w) || tw_key(w) != kl) break;
+          if (tw_state(w) == ST_READY || tw_state(w) == ST_MODIFIED) break;
+          if (!s4.again(c, 1024, __LINE__ + 100000 * SPIN_FILE_ID)) return res;
+        }
+        if (tw_live(w) && tw_key(w) == kl && tw_state(w) >= ST_READY) {
+          float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (lane * 4 < D) v = __ldcg(reinterpret_cast<const float4*>(line_ptr(c, ln) + ol) + lane);
+          const u64 z = dep_zero(__reduce_or_sync(FULL, __float_as_uint(v.x) | __float_as_uint(v.w)));
+          if (((ld_relaxed(&c.tags[ln] + z) ^ w) & IDENT_MASK) == 0) {
+            res.v = v;
+            res.ok = 1;
+            return res;
+          }
+        }
+      }
+      if (!s3.again(c, 1024, __LINE__ + 100000 * SPIN_FILE_ID)) return res;
+    }
   }
 
   struct Acc4 { double v[4]; u32 ok; };

@@ -316,6 +316,30 @@ class AgileSystem:
                                                  out.ctypes.data), "evict_blocks")
         return out
 
+    def set_launch_mode(self, mode: str) -> None:
+        """'split' | 'fused' | 'solo' (split launch whose user grid may run alone: profiling of
+        all-hit replays under a kernel-serialising tool)."""
+        code = {"split": 0, "fused": 1, "solo": 2}[mode]
+        self._check(self._lib.agile_set_launch_mode(self._ctx, code), "set_launch_mode")
+        self.launch_mode = "fused" if mode == "fused" else "split"
+
+    def array_get(self, dev, idx, elem_size: int = 4):
+        """AgileApi.array_get (gpu_api.py:250-278): synchronous element read, the device viewed as a
+        little-endian array of elem_size-byte elements.  Scalars return an int; arrays of indices
+        (with a scalar or per-element dev) return a list of ints (elem_size > 8) or a uint64 array."""
+        if elem_size <= 0 or BLOCK % elem_size:
+            raise ValueError("element size must divide the block size")
+        scalar = np.isscalar(idx)
+        idx = np.atleast_1d(np.ascontiguousarray(idx, dtype=np.uint64))
+        dev = np.ascontiguousarray(np.broadcast_to(np.asarray(dev, dtype=np.uint32), idx.shape))
+        out = np.zeros((len(idx), elem_size), dtype=np.uint8)
+        self._check(self._lib.agile_array_get(self._ctx, dev.ctypes.data, idx.ctypes.data, len(idx), elem_size,
+                                              out.ctypes.data), "array_get")
+        vals = [int.from_bytes(row.tobytes(), "little") for row in out]
+        if scalar:
+            return vals[0]
+        return np.array(vals, dtype=np.uint64) if elem_size <= 8 else vals
+
     def run_gather(self, keys, tasks, epochs, gathers, async_mode, compute_ns):
         import torch
         dev = torch.device("cuda", self.cuda_device)

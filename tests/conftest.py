@@ -26,6 +26,8 @@ def small_config(**kw):
     cfg.service.warps = kw.pop("warps", 2)
     cfg.engine.warps = kw.pop("engine_warps", 4)
     cfg.seed = kw.pop("seed", 0)
+    cfg.cache.policy = kw.pop("policy", "clock")
+    cfg.cache.busy_choice = kw.pop("busy_choice", "wait")
     for k, v in kw.items():
         setattr(cfg, k, v)
     return cfg

@@ -82,10 +82,13 @@ class SetAssocClock(CachePolicy):
         return None
 
 
-def serialized_run(stream, lines, sets=None, blocks=256, with_bytes=False, seed_pages=None):
-    """A.1: one task, async_read + wait per request, full stack."""
-    system = AgileSystem(small_config(pairs=2, cache_lines=lines, blocks=blocks, warps=2),
-                         recorder=TraceRecorder())
+def serialized_run(stream, lines, sets=None, blocks=256, with_bytes=False, seed_pages=None, policy=None):
+    """A.1: one task, async_read + wait per request, full stack.  policy = (name, busy_choice)
+    selects the reference's own plug-in through the config (system.py:23-31)."""
+    cfg = small_config(pairs=2, cache_lines=lines, blocks=blocks, warps=2)
+    if policy is not None:
+        cfg.cache.policy, cfg.cache.busy_choice = policy
+    system = AgileSystem(cfg, recorder=TraceRecorder())
     if sets is not None:
         p = SetAssocClock(sets)
         system.cache.policy = p
@@ -183,6 +186,12 @@ def main():
         r = serialized_run(stream7, 32, sets=S, blocks=512)
         g["a2_setassoc"][str(S)] = {"outcomes": r["outcomes"], "victims": r["victims"]}
     g["a2_stream"] = stream7
+    # the reference's ModuloPolicy (software_cache.py:129-143) through cache.policy = modulo
+    g["a3_modulo"] = {}
+    for lines in (16, 32):
+        for busy in ("wait", "find_another"):
+            r = serialized_run(stream7, lines, blocks=512, policy=("modulo", busy))
+            g["a3_modulo"][f"{lines}_{busy}"] = {"outcomes": r["outcomes"], "victims": r["victims"]}
     # tests/test_software_cache.py:195-210 small streams through the reference test oracle
     sys.path.insert(0, os.path.join(os.path.dirname(REF), "tests"))
     from test_software_cache import _reference_clock

@@ -7,7 +7,7 @@ import numpy as np
 import pytest
 
 from oracle import audit
-from oracle.cache import clock_sequence
+from oracle.cache import clock_sequence, modulo_sequence
 from oracle.pages import page_bytes
 
 pytestmark = pytest.mark.gpu
@@ -36,6 +36,30 @@ def test_a2_set_associative_sequences(gpu_system, sets):
     out, vic, _ = s.run_seq(np.zeros(len(GOLD["a2_stream"])), GOLD["a2_stream"])
     assert ["hit" if o == 0 else "miss" for o in out] == g["outcomes"]
     assert _victims(vic) == g["victims"]
+
+
+@pytest.mark.parametrize("case", ["16_wait", "16_find_another", "32_wait", "32_find_another"])
+def test_a3_modulo_policy_sequences(gpu_system, case):
+    """cache.policy = modulo with one set (ways = lines): the reference's ModuloPolicy exactly."""
+    g = GOLD["a3_modulo"][case]
+    lines, busy = int(case.split("_")[0]), case.split("_", 1)[1]
+    s = gpu_system(cache_lines=lines, ways=lines, blocks=512, policy="modulo", busy_choice=busy)
+    out, vic, _ = s.run_seq(np.zeros(len(GOLD["a2_stream"])), GOLD["a2_stream"])
+    assert ["hit" if o == 0 else "miss" for o in out] == g["outcomes"]
+    assert _victims(vic) == g["victims"]
+
+
+@pytest.mark.parametrize("ways", [8, 32, 64])
+def test_modulo_policy_set_associative_vs_oracle(gpu_system, ways):
+    rng = np.random.default_rng(ways + 1)
+    blk = rng.integers(0, 3000, size=3000)
+    s = gpu_system(cache_lines=512, ways=ways, blocks=4096, pairs=4, policy="modulo", busy_choice="find_another")
+    s.fill_store(0, seed=5)
+    out, vic, pages = s.run_seq(np.zeros_like(blk), blk, pages=True)
+    eo, ev = modulo_sequence([(0, int(b)) for b in blk], 512, ways)
+    assert ["hit" if o == 0 else "miss" for o in out] == eo
+    assert _victims(vic) == [k[1] for _, k in ev]
+    assert np.array_equal(pages, page_bytes(5, 0, blk))
 
 
 @pytest.mark.parametrize("ways", [4, 8, 16, 32])

@@ -49,6 +49,23 @@ def test_exactly_once_under_stress(gpu_system, pairs, depth, conc):
     assert st["completions"] == conc * per and st["misses"] == conc * per
 
 
+@pytest.mark.parametrize("busy", ["wait", "find_another"])
+def test_modulo_policy_exactly_once_under_contention(gpu_system, busy):
+    """cache.policy = modulo (software_cache.py:129-143) with both busy_eviction_choice modes
+    (software_cache.py:366-371) under concurrent misses on a small cache: every command still
+    completes exactly once, every line sees one fill per miss, nothing deadlocks."""
+    conc, per = 512, 24
+    s = gpu_system(pairs=4, sq_depth=16, cq_depth=16, cache_lines=256, ways=32, blocks=1 << 16, warps=4,
+                   engine_warps=8, trace=True, policy="modulo", busy_choice=busy)
+    s.run_loop(conc, warmup_ns=0, measure_ns=10**10, max_per_task=per)
+    recs = s.events().records
+    q = audit.queue_protocol(recs)
+    assert q["enqueues"] == conc * per
+    assert q["fetches"] == q["completions"] == q["releases"] == q["issues"] == q["enqueues"]
+    audit.cache_states(recs)
+    assert audit.single_fill(recs) == conc * per
+
+
 def test_two_level_coalescing(gpu_system):
     """32 lanes async_read one block -> exactly one device READ, 32 identical buffers
     (test_acceptance.py:211-240)."""

@@ -8,7 +8,7 @@ import numpy as np
 import pytest
 
 from oracle import audit
-from oracle.cache import clock_sequence, reference_clock
+from oracle.cache import clock_sequence, modulo_sequence, reference_clock
 from oracle.pages import load_image, page_bytes, page_floats, page_words, save_image
 from oracle.ssd import completion_times, cq_window_rings, plateau_gbps
 
@@ -28,6 +28,16 @@ def test_full_stack_serialized_sequence():
 def test_set_associative_plugin_sequences(sets):
     r = GOLD["a2_setassoc"][sets]
     o, v = clock_sequence([(0, b) for b in GOLD["a2_stream"]], 32, 32 // int(sets))
+    assert o == r["outcomes"]
+    assert [k[1] for _, k in v] == r["victims"]
+
+
+@pytest.mark.parametrize("case", ["16_wait", "16_find_another", "32_wait", "32_find_another"])
+def test_modulo_policy_sequences(case):
+    """The reference's own ModuloPolicy (cache.policy = modulo, software_cache.py:129-143)."""
+    r = GOLD["a3_modulo"][case]
+    lines = int(case.split("_")[0])
+    o, v = modulo_sequence([(0, b) for b in GOLD["a2_stream"]], lines, lines)
     assert o == r["outcomes"]
     assert [k[1] for _, k in v] == r["victims"]
 

@@ -6,9 +6,11 @@
              all hits and its rows stream from HBM — the no-reuse roofline case.
     zipf:    the bench's hashed Zipf 1.05 batch over the same tables (L2 reuse of hot rows).
 Prints one JSON line: ms per launch, algorithmic GB/s and fraction of the measured HBM peak.
-Profile: AGILE_LAUNCH=split AGILE_SOLO_USERS=1 ncu -k regex:agile_user_kernel -s 2 -c 1 ...
-(the infra grid leaves after 100 ms when the user grid cannot start beside it; all hits need no
-engine), so the capture is the production user kernel with its own register budget.
+Profile: K5_SOLO=1 ncu -k regex:agile_user_kernel -c 1 python tools/k5_probe.py uniform 1: the
+warm-up runs take the launch mode the co-residency probe picks (fused under ncu: they need the
+engine for their misses), then the timed all-hit replays switch to split-solo (the infra grid
+leaves after 100 ms when the user grid cannot start beside it; all hits need no engine), so the
+capture is the production user kernel with its own register budget.
 """
 import json
 import os
@@ -59,6 +61,8 @@ def main():
     for _ in range(2):   # fill, then make sure every page is resident
         s.embbag_sharded(idx, tabs, out, cnt, D, stream=st.cuda_stream)
     s.sync(st.cuda_stream)
+    if os.environ.get("K5_SOLO") == "1":
+        s.set_launch_mode("solo")
     cnt.zero_()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record(st)
