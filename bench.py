@@ -188,6 +188,63 @@ def _cpu_port(plan, rank, lines, scatter, threads, seconds, max_steps=400, warm_
     return done / tsum, desc, cc
 
 
+def _reference_simulator(seconds=8.0):
+    """The reference simulator itself (agile_sim from baseline/_ref, installed from the reference
+    package with pip --target; the box has no /root/reference) running the same paged embedding-bag
+    gather through its public API: 32 tasks (one warp), each pooling bags of the bench's shape by
+    async_read + wait of every lookup's 4 KiB page (gpu_api.py:164-190, 233-248) through its
+    software cache, hashed Zipf 1.05 row indices over 26 tables of 1024 pages.  Wall-clock
+    lookups/s of the simulator on ONE host core (the simulator is single-threaded), over bounded
+    repetitions of the sample.  None when the package is not installed."""
+    import random
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "agile_sim")):
+        return None
+    sys.path.insert(0, ref)
+    try:
+        from agile_sim.config import SystemConfig as RefConfig
+        from agile_sim.system import AgileSystem as RefSystem
+    except Exception:
+        return None
+    finally:
+        sys.path.remove(ref)
+    rng = random.Random(SEED)
+    tasks, pages_per_table = 32, 256
+    rpp = 4096 // (4 * D)
+
+    def run(bags_per_task):
+        cfg = RefConfig()
+        cfg.device.num_blocks = T * pages_per_table
+        cfg.cache.lines = T * pages_per_table // 4          # tables 4x the cache, as on the GPU
+        sysm = RefSystem(cfg)
+        api = sysm.api
+        plans = [[[(t, min(int(rng.paretovariate(ALPHA - 1.0)) - 1, pages_per_table * rpp - 1))
+                   for _ in range(L)] for t in (rng.randrange(T) for _ in range(bags_per_task))]
+                 for _ in range(tasks)]
+
+        def prog(plan):
+            def fn(task, chain):
+                buf = api.make_buf()
+                for bag in plan:
+                    acc = 0
+                    for t, r in bag:
+                        yield from api.async_read(0, t * pages_per_table + r // rpp, buf, chain)
+                        yield from api.wait(buf, chain)
+                        acc += buf.data[(r % rpp) * 4 * D]
+            return fn
+        t0 = time.perf_counter()
+        sysm.run_workload([prog(p) for p in plans])
+        return time.perf_counter() - t0, tasks * bags_per_task * L
+
+    dt, n = run(2)                                     # calibration
+    bags = max(2, int(2 * seconds / max(dt, 1e-3)))
+    t_total, lookups = run(bags)
+    reps = 1
+    return {"value": lookups / t_total, "unit": "lookups/s", "cores": 1, "kind": "reference",
+            "sample": f"{tasks} tasks x {bags} bags x {L} lookups through agile_sim "
+                      f"AgileApi.async_read + wait (baseline/_ref, reference package), {t_total:.1f} s wall"}
+
+
 def run_reference(args):
     """Reference arm: the CPU implementation of the path (the oracle C port) on all host threads,
     rank 0 only, on the GPU arm's metric and config; each step a bounded sample (128 fresh samples)
@@ -230,6 +287,9 @@ def run_reference(args):
                              "sample": f"{args.steps} timed steps of {bs} fresh samples x {len(tabs)} tables x {L} "
                                        f"lookups (rank 0's shard); cache warm-up: {desc}"},
             "e2e": {"value": value, "unit": "lookups/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    sim = _reference_simulator()
+    if sim is not None:
+        line["reference_simulator"] = sim
     print(json.dumps(line), flush=True)
 
 

@@ -68,6 +68,16 @@ int agile_geometry(agile_ctx* ctx, uint64_t* out, int n);
  * grid runs alone — an all-hit replay needs neither engine nor service). */
 int agile_set_launch_mode(agile_ctx* ctx, int mode);
 
+/* Third-party user kernels (include/agile_device.cuh, the paper's Listing 1 API): begin one split
+ * run on `stream` — run words reset, infra grid launched — and receive the DevCtx / Launch values
+ * (sizes checked against the caller's build) the user grid must be launched with
+ * (agile::launch_user), plus a device array of n_bufs WaitNodes for AgileBufPtr barriers.  The
+ * user kernel must run n_user_ctas CTAs of 256 threads, each constructing agile::UserRun.
+ * agile_user_run_end waits for the run and surfaces device-side errors. */
+int agile_user_run_begin(agile_ctx* ctx, void* stream, uint32_t n_user_ctas, uint64_t n_bufs, void* devctx_out,
+                         uint64_t devctx_size, void* launch_out, uint64_t launch_size, void** nodes_out);
+int agile_user_run_end(agile_ctx* ctx, void* stream);
+
 /* Backing store (BlockStore, ssd_model.py:61-101): pinned + GPU-mapped host memory, caller-owned
  * when host_ptr != NULL (registered), else context-owned and zeroed.  image_path (optional) is a
  * raw little-endian block image, offset = blk * 4096, short tail zero-padded (load_image). */

@@ -50,6 +50,8 @@ struct agile_ctx {
   // launch mode: false = split (infra grid + PDL user grid, the default), true = one fused grid
   // with roles by arrival ticket (AGILE_LAUNCH=fused: what a kernel-serialising profiler captures)
   bool fused = false;
+  // engine.copy: false = register-staged page moves, true = TMA bulk copies through shared memory
+  bool bulk_engine = false;
   // infra grid of bounded side-stream runs (engine.side_warps / service.side_warps; 0 = full)
   uint32_t side_engine_warps = 0, side_service_warps = 0;
   // async_read WaitNodes (AgileBuf barriers) for the reads / loop / seq workloads
@@ -217,6 +219,19 @@ size_t dyn_smem() {
   return b;
 }
 
+// the context's infra kernel (engine.copy) and its dynamic shared memory (the bulk engine's slots)
+using InfraFn = void (*)(const DevCtx, const Launch);
+InfraFn infra_fn(const agile_ctx* ctx) { return ctx->bulk_engine ? agile_infra_kernel<true> : agile_infra_kernel<false>; }
+size_t infra_smem(const agile_ctx* ctx) {
+  if (!ctx->bulk_engine) return 0;
+  static bool set = false;
+  if (!set) {
+    cudaFuncSetAttribute(agile_infra_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kInfraSmem);
+    set = true;
+  }
+  return kInfraSmem;
+}
+
 // Lazy module loading would load the user kernel at its first launch, i.e. while the infra grid
 // it must run beside is already spinning — loading can wait for the device to drain, and the two
 // grids would deadlock.  Touching both functions first loads them before any run starts.
@@ -225,7 +240,8 @@ void load_kernels() {
   static bool loaded = false;
   if (loaded) return;
   cudaFuncAttributes a{};
-  cudaFuncGetAttributes(&a, agile_infra_kernel);
+  cudaFuncGetAttributes(&a, agile_infra_kernel<false>);
+  cudaFuncGetAttributes(&a, agile_infra_kernel<true>);
   cudaFuncGetAttributes(&a, agile_user_kernel<W>);
   cudaFuncGetAttributes(&a, agile_fused_kernel<W>);
   loaded = true;
@@ -235,12 +251,10 @@ void load_kernels() {
 // (engine.side_warps / service.side_warps).  Engine and service ownership is by stride over the
 // queue pairs and all their state persists in the context, so the infra size can change from run
 // to run.
-template <class W>
-int launch(agile_ctx* ctx, const W& work, uint32_t n_user_ctas, cudaStream_t st, bool side = false) {
-  if (n_user_ctas == 0) n_user_ctas = 1;
-  load_kernels<W>();
-  dyn_smem<W>();
-  DevCtx dc = ctx->d;
+// reset the run words and launch the infra grid of one split run; dc / L receive what the user grid
+// of the run is launched with
+int launch_infra(agile_ctx* ctx, uint32_t n_user_ctas, cudaStream_t st, bool side, DevCtx& dc, Launch& L) {
+  dc = ctx->d;
   dc.nodes_lo = (u64)(uintptr_t)ctx->nodes;
   dc.nodes_hi = dc.nodes_lo + (u64)ctx->nodes_cap * sizeof(WaitNode);
   if (side && !ctx->fused) {
@@ -254,17 +268,33 @@ int launch(agile_ctx* ctx, const W& work, uint32_t n_user_ctas, cudaStream_t st,
     }
   }
   CK(cudaMemsetAsync(ctx->d.run, 0, sizeof(RunWords), st));
-  Launch L;
   L.n_user_ctas = n_user_ctas;
   L.pad = 0;
-  const uint32_t ninfra = dc.n_engine_ctas + dc.n_service_ctas;
+  if (ctx->fused) return 0;
+  infra_fn(ctx)<<<dc.n_engine_ctas + dc.n_service_ctas, kCtaThreads, infra_smem(ctx), st>>>(dc, L);
+  CK(cudaGetLastError());
+  return 0;
+}
+
+// side: a bounded run beside other work (user_ctas given): its infra grid may be smaller
+// (engine.side_warps / service.side_warps).  Engine and service ownership is by stride over the
+// queue pairs and all their state persists in the context, so the infra size can change from run
+// to run.
+template <class W>
+int launch(agile_ctx* ctx, const W& work, uint32_t n_user_ctas, cudaStream_t st, bool side = false) {
+  if (n_user_ctas == 0) n_user_ctas = 1;
+  load_kernels<W>();
+  dyn_smem<W>();
+  DevCtx dc;
+  Launch L;
+  int rc = launch_infra(ctx, n_user_ctas, st, side, dc, L);
+  if (rc) return rc;
   if (ctx->fused) {
+    const uint32_t ninfra = dc.n_engine_ctas + dc.n_service_ctas;
     agile_fused_kernel<W><<<ninfra + n_user_ctas, kCtaThreads, dyn_smem<W>(), st>>>(dc, L, work);
     CK(cudaGetLastError());
     return 0;
   }
-  agile_infra_kernel<<<ninfra, kCtaThreads, 0, st>>>(dc, L);
-  CK(cudaGetLastError());
   // the user grid may start once every infra CTA executed griddepcontrol.launch_dependents
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(n_user_ctas);
@@ -296,9 +326,21 @@ uint32_t resident_ctas(agile_ctx* ctx) {
   if (per_sm < 1) per_sm = 1;
   cudaFuncAttributes ua{}, ia{};
   cudaFuncGetAttributes(&ua, agile_user_kernel<W>);
-  cudaFuncGetAttributes(&ia, agile_infra_kernel);
-  const uint32_t ur = (uint32_t)std::max(1, ua.numRegs), ir = (uint32_t)std::max(1, ia.numRegs);
-  const uint32_t displaced = (ir + ur - 1) / ur;
+  cudaFuncGetAttributes(&ia, infra_fn(ctx));
+  // user CTAs left on an SM that also hosts one infra CTA: registers (allocated per warp in units
+  // of 8 per thread), shared memory (the engine's page slots) and warp slots all bound it
+  int regs_sm = 65536, smem_sm = 233472, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev);
+  cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+  auto warp_regs = [](int r) { return (uint32_t)((std::max(1, r) + 7) / 8 * 8 * 32); };
+  const uint32_t u_regs = warp_regs(ua.numRegs) * kCtaWarps, i_regs = warp_regs(ia.numRegs) * kCtaWarps;
+  const uint64_t u_smem = (uint64_t)ua.sharedSizeBytes + dyn_smem<W>() + 1024, i_smem = ia.sharedSizeBytes + infra_smem(ctx) + 1024;
+  uint32_t beside = (uint32_t)per_sm;
+  beside = std::min<uint32_t>(beside, regs_sm > (int)i_regs ? ((uint32_t)regs_sm - i_regs) / u_regs : 0u);
+  beside = std::min<uint64_t>(beside, (uint64_t)smem_sm > i_smem ? ((uint64_t)smem_sm - i_smem) / u_smem : 0u);
+  beside = std::min<uint32_t>(beside, (64u - kCtaWarps) / kCtaWarps);
+  const uint32_t displaced = (uint32_t)per_sm - beside;
   const uint32_t total = (uint32_t)per_sm * (uint32_t)ctx->sms;
   const uint32_t taken = (ctx->d.n_engine_ctas + ctx->d.n_service_ctas) * displaced;
   return total > taken + 1 ? total - taken : 1;
@@ -450,6 +492,7 @@ int agile_create(const char* config_text, int cuda_device, agile_ctx** out) {
   if (ways == 0 || ways > lines) ways = lines;   // 0 = fully associative (reference-exact clock)
   const std::string policy = cfg.s("cache.policy", "clock");
   const std::string busy = cfg.s("cache.busy_choice", "wait");
+  const std::string engine_copy = cfg.s("engine.copy", "registers");
   d.service_warps = (uint32_t)std::max<uint64_t>(1, cfg.u("service.warps", 4));
   d.poll_ns = (uint32_t)cfg.u("service.poll_ns", 400);
   d.idle_max_ns = (uint32_t)std::max<uint64_t>(d.poll_ns, cfg.u("service.idle_max_ns", 3200));
@@ -469,6 +512,7 @@ int agile_create(const char* config_text, int cuda_device, agile_ctx** out) {
   if (lines >= (1ull << 32) - 1) return fail(ctx, AGILE_E_CONFIG, "cache too large");
   if (policy != "clock" && policy != "modulo") return fail(ctx, AGILE_E_CONFIG, "unknown cache policy '" + policy + "'");
   if (busy != "wait" && busy != "find_another") return fail(ctx, AGILE_E_CONFIG, "cache.busy_choice must be wait|find_another");
+  if (engine_copy != "registers" && engine_copy != "bulk") return fail(ctx, AGILE_E_CONFIG, "engine.copy must be registers|bulk");
   if (cfg.b("share_table.enabled", false)) return fail(ctx, AGILE_E_CONFIG, "share_table.enabled=true is not supported on the B200 path (SURVEY 8(f))");
   if (cfg.u("device.parallelism", 16) > 32 * kMaxChanPerLane) return fail(ctx, AGILE_E_CONFIG, "device.parallelism must be <= 256");
   if (emu != "model" && emu != "link") return fail(ctx, AGILE_E_CONFIG, "device.emulation must be model|link");
@@ -493,6 +537,7 @@ int agile_create(const char* config_text, int cuda_device, agile_ctx** out) {
   if (d.watchdog_ns > 60ull * 1000000000ull) d.watchdog_ns = 60ull * 1000000000ull;
   d.user_start_ns = d.watchdog_ns;
   d.policy = policy == "modulo" ? POL_MODULO : POL_CLOCK;   // system.py:23-31 _make_policy
+  ctx->bulk_engine = engine_copy == "bulk";
   d.find_another = busy == "find_another" ? 1u : 0u;
   d.solo_ok = 0;
   if (const char* so = getenv("AGILE_SOLO_USERS")) {
@@ -859,6 +904,31 @@ int agile_evict_blocks(agile_ctx* ctx, const uint32_t* dev, const uint64_t* blk,
   if (!rc) CK(cudaMemcpy(outcome, d_out, n, cudaMemcpyDeviceToHost));
   return rc;
 }
+
+int agile_user_run_begin(agile_ctx* ctx, void* stream, uint32_t n_user_ctas, uint64_t n_bufs, void* devctx_out,
+                         uint64_t devctx_size, void* launch_out, uint64_t launch_size, void** nodes_out) {
+  if (!ctx || !devctx_out || !launch_out || !n_user_ctas) return fail(ctx, AGILE_E_ARG, "bad user_run_begin args");
+  if (devctx_size != sizeof(DevCtx) || launch_size != sizeof(Launch))
+    return fail(ctx, AGILE_E_ARG, "DevCtx / Launch size mismatch: rebuild against include/agile_device.cuh");
+  if (ctx->fused)
+    return fail(ctx, AGILE_E_ARG, "third-party user kernels need the split launch (a kernel-serialising tool is attached)");
+  CK(cudaSetDevice(ctx->device));
+  WaitNode* nodes = get_nodes(ctx, std::max<uint64_t>(1, n_bufs));
+  if (!nodes) return fail(ctx, AGILE_E_CUDA, "node allocation failed");
+  if (nodes_out) *nodes_out = nodes;
+  cudaFuncAttributes a{};
+  cudaFuncGetAttributes(&a, agile_infra_kernel<false>);   // loaded before the infra grid spins
+  cudaFuncGetAttributes(&a, agile_infra_kernel<true>);
+  DevCtx dc;
+  Launch L;
+  int rc = launch_infra(ctx, n_user_ctas, reinterpret_cast<cudaStream_t>(stream), false, dc, L);
+  if (rc) return rc;
+  std::memcpy(devctx_out, &dc, sizeof(DevCtx));
+  std::memcpy(launch_out, &L, sizeof(Launch));
+  return 0;
+}
+
+int agile_user_run_end(agile_ctx* ctx, void* stream) { return agile_sync(ctx, stream); }
 
 int agile_set_launch_mode(agile_ctx* ctx, int mode) {
   if (!ctx || mode < 0 || mode > 2) return fail(ctx, AGILE_E_ARG, "launch mode must be 0 (split), 1 (fused) or 2 (split, solo users)");

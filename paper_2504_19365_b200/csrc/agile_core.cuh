@@ -684,7 +684,7 @@ __device__ Req access_warp(const DevCtx& c, bool active, u64 key, bool pin, u32 
   const u32 lane = lane_id();
   Req r;
   r.line = NONE; r.kind = R_NONE; r.word = 0; r.victim = ~0ull;
-  if (active) {   // AgileApi._check_block (gpu_api.py:328-332): OutOfRange before the cache is touched
+  if (active) {   // AgileApi._check_block (gpu_api.py:122-126): OutOfRange before the cache is touched
     const u32 dv = key_dev(key);
     if (dv >= c.num_devices || key_blk(key) >= c.store_blocks[dv]) {
       set_error(c, E_OUT_OF_RANGE, dv, key_blk(key));
@@ -776,7 +776,7 @@ __device__ Req access_warp(const DevCtx& c, bool active, u64 key, bool pin, u32 
   return r;
 }
 
-// Prefetch (AgileApi.prefetch, gpu_api.py:345-361): pull blocks toward the cache without waiting;
+// Prefetch (AgileApi.prefetch, gpu_api.py:139-155): pull blocks toward the cache without waiting;
 // duplicates die in the warp; lanes whose set is momentarily full retry (no pins are held).
 __device__ void prefetch_warp(const DevCtx& c, bool active, u64 key, u32 who, u32 sq_start, bool best_effort) {
   bool want = active;
@@ -833,7 +833,7 @@ __device__ __forceinline__ void copy_page_warp(const uint4* src, uint4* dst) {
   for (int k = 0; k < 8; ++k) __stcg(dst + lane + 32 * k, v[k]);
 }
 
-// async_read (gpu_api.py:370-396), warp-collective: start filling each active lane's node->dst
+// async_read (gpu_api.py:164-190), warp-collective: start filling each active lane's node->dst
 // from `key`.  HIT: copied now.  MISS/FILLING: the node joins the line's waiter stack and the
 // service delivers it.  Returns with no pin held.  Outcomes are counted by access_warp.
 __device__ void async_read_warp(const DevCtx& c, bool active, u64 key, WaitNode* node, uint4* dst, u32 who,
@@ -888,7 +888,7 @@ __device__ void async_read_warp(const DevCtx& c, bool active, u64 key, WaitNode*
   }
 }
 
-// one poll pass over nodes: mask of lanes whose transfer is done (AgileApi.wait, gpu_api.py:439-454)
+// one poll pass over nodes: mask of lanes whose transfer is done (AgileApi.wait, gpu_api.py:233-248)
 __device__ __forceinline__ u32 poll_nodes_warp(bool active, const WaitNode* node) {
   bool d = false;
   if (active) d = ld_acquire(&node->done) != 0;
@@ -1017,6 +1017,11 @@ __device__ void async_write_warp(const DevCtx& c, bool active, u64 key, WaitNode
 
 // ======================================================================= K3: completion service
 
+#ifndef AGILE_SVC_SLICE
+#define AGILE_SVC_SLICE 4
+#endif
+constexpr int kSvcSlice = AGILE_SVC_SLICE;   // uint4 per lane per waiter-copy step (8 or 4)
+
 __device__ __forceinline__ void advance_head(const DevCtx& c, u32 q, u32 who) {
   SqWords* s = &c.sqw[q];
   const u32 D = c.sq_depth;
@@ -1108,23 +1113,28 @@ __device__ u32 cq_window_pass(const DevCtx& c, u32 cq, u64& off, u32& mask, u32 
         continue;
       }
     }
-    uint4 v0[8], v1[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) v0[k] = __ldcg(src0 + lane + 32 * k);
-    if (l1 >= 0) {
-#pragma unroll
-      for (int k = 0; k < 8; ++k) v1[k] = __ldcg(src1 + lane + 32 * k);
-    }
     // dst == 0: a write's durability handle (async_write) — completion only, no copy
     uint4* d0 = reinterpret_cast<uint4*>(n0->dst);
     uint4* d1 = reinterpret_cast<uint4*>(n1->dst);
-    if (d0) {
+    // both pages move in kSvcSlice-uint4 steps per lane (kSvcSlice = 8: one step, every load of
+    // both pages in flight at once; 4: half the registers, two steps)
 #pragma unroll
-      for (int k = 0; k < 8; ++k) __stcg(d0 + lane + 32 * k, v0[k]);
-    }
-    if (l1 >= 0 && d1) {
+    for (int h = 0; h < 8; h += kSvcSlice) {
+      uint4 v0[kSvcSlice], v1[kSvcSlice];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) __stcg(d1 + lane + 32 * k, v1[k]);
+      for (int k = 0; k < kSvcSlice; ++k) v0[k] = __ldcg(src0 + lane + 32 * (h + k));
+      if (l1 >= 0) {
+#pragma unroll
+        for (int k = 0; k < kSvcSlice; ++k) v1[k] = __ldcg(src1 + lane + 32 * (h + k));
+      }
+      if (d0) {
+#pragma unroll
+        for (int k = 0; k < kSvcSlice; ++k) __stcg(d0 + lane + 32 * (h + k), v0[k]);
+      }
+      if (l1 >= 0 && d1) {
+#pragma unroll
+        for (int k = 0; k < kSvcSlice; ++k) __stcg(d1 + lane + 32 * (h + k), v1[k]);
+      }
     }
     __threadfence();   // every lane's page stores are performed before any barrier is released
     __syncwarp();
@@ -1450,8 +1460,36 @@ constexpr int kEnginePages = AGILE_ENGINE_PAGES;
 #define AGILE_FILL_STORE __stcs
 #endif
 
-template <int kPages = kEnginePages>
-__device__ void engine_main(const DevCtx& c, u32 ew) {
+// Bulk-copy engine (split launch): a page moves host-pinned store -> shared memory through the
+// TMA bulk-copy unit (cp.async.bulk ... mbarrier::complete_tx, UBLKCP in SASS), so the long host-
+// link latency is covered by shared-memory slots instead of registers; the short HBM leg is a
+// coalesced warp copy out of the slot.  kEngineSlots 4 KiB slots per engine warp.
+#ifndef AGILE_ENGINE_SLOTS
+#define AGILE_ENGINE_SLOTS 4
+#endif
+constexpr int kEngineSlots = AGILE_ENGINE_SLOTS;
+constexpr u32 kInfraSmem = kCtaWarps * kEngineSlots * (kBlockBytes + 8);   // stages + mbarriers
+
+__device__ __forceinline__ u32 smem_addr(const void* p) { return (u32)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(u64* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ bool mbar_test(u64* bar, u32 parity) {
+  u32 done;
+  asm volatile("{ .reg .pred p; mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+               : "=r"(done) : "r"(smem_addr(bar)), "r"(parity) : "memory");
+  return done != 0;
+}
+// one 4 KiB global -> shared bulk copy whose completion (bytes landed) flips `bar`
+__device__ __forceinline__ void bulk_page_to_smem(void* dst_smem, const void* src, u64* bar) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // earlier generic reads of the slot first
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], 4096;" :: "r"(smem_addr(bar)) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 4096, [%2];"
+               :: "r"(smem_addr(dst_smem)), "l"(src), "r"(smem_addr(bar)) : "memory");
+}
+
+template <int kPages = kEnginePages, bool kBulk = false>
+__device__ void engine_main(const DevCtx& c, u32 ew, uint8_t* slots = nullptr) {
   const u32 lane = lane_id();
   const u32 E = c.engine_warps;
   const u32 Ds = c.sq_depth, Dq = c.cq_depth;
@@ -1463,11 +1501,75 @@ __device__ void engine_main(const DevCtx& c, u32 ew) {
   u32 rr = 0, pass = 0, seq = 0, pseq = 0;
   u32 idle = 32;
   u64 bytes_r = 0, bytes_w = 0;
+  // bulk mode: slot s (< kEngineSlots) of this warp is tracked by lane s: busy, owner lane, phase
+  bool pinf = false;                 // this lane's command has its page in a slot
+  bool sbusy = false;
+  u32 sowner = 0, spar = 0;
+  uint8_t* stage = nullptr;
+  u64* bars = nullptr;
+  if constexpr (kBulk) {
+    stage = slots + (u64)(threadIdx.x >> 5) * kEngineSlots * kBlockBytes;
+    bars = reinterpret_cast<u64*>(slots + (u64)kCtaWarps * kEngineSlots * kBlockBytes) + (threadIdx.x >> 5) * kEngineSlots;
+    if (lane < (u32)kEngineSlots) mbar_init(&bars[lane]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncwarp();
+  }
   while (true) {
     bool did = false;
+    if constexpr (kBulk) {
+      // ---- slots whose bytes landed: copy them out to HBM (or to the host store for writes)
+      const bool sdone = lane < (u32)kEngineSlots && sbusy && mbar_test(&bars[lane], spar);
+      u32 dm = __ballot_sync(FULL, sdone);
+      if (dm) {
+        did = true;
+        u32 moved = 0;
+        const u32 dm0 = dm;
+        while (dm) {
+          const int sl = __ffs(dm) - 1;
+          dm &= dm - 1;
+          const int ow = __shfl_sync(FULL, (int)sowner, sl);
+          const u32 op = __shfl_sync(FULL, pop, ow);
+          const u32 d = __shfl_sync(FULL, pdev, ow);
+          const u64 b = __shfl_sync(FULL, pblk, ow);
+          const u64 pr = __shfl_sync(FULL, prp, ow);
+          uint4* dst = op == OP_READ ? reinterpret_cast<uint4*>(pr) : reinterpret_cast<uint4*>(c.store_w[d] + (b << kBlockShift));
+          const uint4* src = reinterpret_cast<const uint4*>(stage + (u64)sl * kBlockBytes);
+          uint4 v[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) v[k] = src[lane + 32 * k];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) AGILE_FILL_STORE(dst + lane + 32 * k, v[k]);
+          moved |= 1u << ow;
+        }
+        __threadfence();   // page bytes visible before the CQE release of these commands
+        __syncwarp();
+        if ((moved >> lane) & 1u) { pcp = true; pinf = false; }
+        if ((dm0 >> lane) & 1u) { sbusy = false; spar ^= 1u; }
+      }
+      // ---- start bulk copies of the oldest fetched commands into free slots
+      u32 freeslots = ~__ballot_sync(FULL, lane < (u32)kEngineSlots && sbusy) & ((1u << kEngineSlots) - 1u);
+      u32 taken = 0;
+      while (freeslots) {
+        const int ow = oldest_lane(pv && !pcp && !pinf && !((taken >> lane) & 1u), pseq);
+        if (ow < 0) break;
+        did = true;
+        const int sl = __ffs(freeslots) - 1;
+        freeslots &= freeslots - 1;
+        taken |= 1u << ow;
+        const u32 op = __shfl_sync(FULL, pop, ow);
+        const u32 d = __shfl_sync(FULL, pdev, ow);
+        const u64 b = __shfl_sync(FULL, pblk, ow);
+        const u64 pr = __shfl_sync(FULL, prp, ow);
+        const void* src = op == OP_READ ? reinterpret_cast<const void*>(c.store[d] + (b << kBlockShift))
+                                        : reinterpret_cast<const void*>(pr);
+        if (lane == 0) bulk_page_to_smem(stage + (u64)sl * kBlockBytes, src, &bars[sl]);
+        if (lane == (u32)ow) pinf = true;
+        if (lane == (u32)sl) { sbusy = true; sowner = (u32)ow; }
+      }
+    }
     // ---- start moving the bytes of the two oldest fetched commands: the loads (host link
     //      latency) stay in flight while this pass posts completions and fetches new SQEs
-    const u32 tocopy = __ballot_sync(FULL, pv && !pcp);
+    const u32 tocopy = kBulk ? 0u : __ballot_sync(FULL, pv && !pcp);
     int lk[kPages];
     uint4 v[kPages][8];
     uint4* tk[kPages];
@@ -1545,7 +1647,7 @@ __device__ void engine_main(const DevCtx& c, u32 ew) {
     u32 nfree = __popc(freeb);
     bool newcmd = false;
     ++pass;
-    const u32 ncopy = __popc(__ballot_sync(FULL, pv && !pcp));
+    const u32 ncopy = __popc(__ballot_sync(FULL, pv && !pcp && !pinf));
     const bool fetch_now = ncopy < 8 || (pass & 3u) == 0;
     if (nfree && nq && fetch_now) {
       u32 assigned = 0;   // free lanes handed out in earlier chunks
@@ -1711,12 +1813,22 @@ __device__ __forceinline__ void user_done(const DevCtx& c, u32 n_users) {
   }
 }
 
-__global__ void __launch_bounds__(kCtaThreads, 1) agile_infra_kernel(const __grid_constant__ DevCtx c, const Launch L) {
+// kBulk: pages move through the TMA bulk-copy unit into shared-memory slots (the register budget
+// no longer holds pages in flight); the infra grid's CTAs then fit beside user CTAs on their SMs
+// Two infra kernels, picked per context (config engine.copy): kBulk = false moves pages through
+// registers (4 per engine-warp pass; 236 registers, one infra CTA per SM: the infra SMs are the
+// engine's alone, which keeps the miss path's latency lowest); kBulk = true moves them through the
+// TMA bulk-copy unit into shared-memory slots (128 registers: two user CTAs fit beside each infra
+// CTA, which gives hit-heavy runs ~8 % more user CTAs and the side-stream runs a smaller footprint)
+template <bool kBulk>
+__global__ void __launch_bounds__(kCtaThreads, kBulk ? 2 : 1)
+    agile_infra_kernel(const __grid_constant__ DevCtx c, const Launch L) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  extern __shared__ __align__(128) uint8_t infra_smem[];
   const u32 warp = threadIdx.x >> 5;
   if (blockIdx.x < c.n_engine_ctas) {
     const u32 ew = blockIdx.x * kCtaWarps + warp;
-    if (ew < c.engine_warps) engine_main<kEnginePages>(c, ew);
+    if (ew < c.engine_warps) engine_main<kEnginePages, kBulk>(c, ew, infra_smem);
   } else {
     const u32 sw = (blockIdx.x - c.n_engine_ctas) * kCtaWarps + warp;
     if (sw < c.service_warps) service_main(c, L, sw);

@@ -468,7 +468,7 @@ struct GatherWork {
 // Tables are described per launch by TabDesc (= agile_table_shard of the C-ABI): the page key of
 // the shard's first page, the global row range [row0, row0 + rows) the shard holds (row-wise
 // sharding over ranks; a whole table has row0 = 0, rows = table_rows), the whole table's row
-// count (indices outside [0, table_rows) raise OutOfRange, gpu_api.py:328-332 / ssd_model.py:24),
+// count (indices outside [0, table_rows) raise OutOfRange, gpu_api.py:122-126 / ssd_model.py:24),
 // the byte offset of the table's pooled vector in an output row, and whether the shard writes its
 // fp64 partial sum (row shards, summed by the receiver after the exchange) or the final fp32.
 //
@@ -493,6 +493,32 @@ struct TabDesc {
 };
 static_assert(sizeof(TabDesc) == 40, "TabDesc must match agile_table_shard");
 constexpr u32 TAB_PARTIAL_F64 = 1u;
+
+// Row loads of the hit path: L2-coherent (.cg); with AGILE_ROW_EVICT_FIRST the rows carry an
+// L2 evict-first policy so a stream of cold rows does not push the signature / tag arrays out of L2
+#ifndef AGILE_ROW_EVICT_FIRST
+#define AGILE_ROW_EVICT_FIRST 0
+#endif
+__device__ __forceinline__ u64 row_policy() {
+#if AGILE_ROW_EVICT_FIRST
+  u64 p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+#else
+  return 0;
+#endif
+}
+__device__ __forceinline__ float4 ld_row(const float4* a, u64 pol) {
+#if AGILE_ROW_EVICT_FIRST
+  float4 v;
+  asm volatile("ld.global.cg.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(a), "l"(pol));
+  return v;
+#else
+  (void)pol;
+  return __ldcg(a);
+#endif
+}
 
 // 0, computed from v: an address offset that cannot be formed before v's load returned
 __device__ __forceinline__ u64 dep_zero(u32 v) {
@@ -592,13 +618,7 @@ struct EmbBagWork {
 #ifndef AGILE_EMB_MIN_CTAS
 #define AGILE_EMB_MIN_CTAS 4
 #endif
-#ifndef AGILE_K5_RIF
-#define AGILE_K5_RIF 8   // row loads in flight per lane in pool_block
-#endif
-  static constexpr u32 kRif = AGILE_K5_RIF;
-#ifndef AGILE_K5_BAG
-#define AGILE_K5_BAG 1   // 1: the bag-at-a-time pooling (pool_bag); 0: block passes (pool_block)
-#endif
+
   static constexpr int kMinCtas = AGILE_EMB_MIN_CTAS;
 
   __device__ void run(const DevCtx& c, u32 uidx, u32 nusers) const {
@@ -613,12 +633,15 @@ struct EmbBagWork {
     while (cur < nbags) {
       const u32 nxt = grab_block(c);
       if (pd && nxt < nbags) prefetch_block(c, nxt, nbags, who, gw + (++pass));
-#if AGILE_K5_BAG
+      if (!offsets && nxt < nbags) {
+        // the next block's indices (kGrab * L contiguous int64) toward L2 while this block pools:
+        // its first index load is then an L2 hit instead of an HBM round trip
+        const u64 i0 = (u64)nxt * L, n8 = (u64)min(kGrab, nbags - nxt) * L;
+        for (u64 o = (u64)lane_id() * 16; o < n8; o += 32 * 16)
+          asm volatile("prefetch.global.L2::evict_last [%0];" :: "l"(idx + i0 + o));
+      }
       for (u32 k = 0; k < kGrab && cur + k < nbags; ++k)
         if (!pool_bag(c, cur + k, who, gw, misses, lookups)) { cur = nbags; break; }
-#else
-      if (!pool_block(c, cur, min(kGrab, nbags - cur), who, gw, misses, lookups)) break;
-#endif
       if (aborted(c)) break;
       cur = nxt;
     }
@@ -773,6 +796,7 @@ struct EmbBagWork {
       // (16 B/lane, 512 B coalesced each at D = 128) in flight per step
       const u64 rowaddr = a ? (u64)(uintptr_t)(line_ptr(c, line) + off) : 0ull;
       u32 dep = 0;
+      const u64 pol = row_policy();
       for (u32 m = am; m; ) {
         float4 v[8];
 #pragma unroll
@@ -780,7 +804,7 @@ struct EmbBagWork {
           const int src = m ? __ffs(m) - 1 : 0;
           const u64 ra = __shfl_sync(FULL, rowaddr, src);
           v[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (m && dims) v[j] = __ldcg(reinterpret_cast<const float4*>(ra) + lane);
+          if (m && dims) v[j] = ld_row(reinterpret_cast<const float4*>(ra) + lane, pol);
           m &= m - 1;
         }
 #pragma unroll
@@ -810,228 +834,6 @@ struct EmbBagWork {
       }
     }
     return true;
-  }
-
-  // Pool a block of nb consecutive bags as ONE flat run of lookups (the block's indices are
-  // contiguous in idx, fixed L or offsets alike), 32 lookups per pass with every lane busy: a
-  // pass resolves its 32 pages with one signature probe round and one confirming tag round,
-  // then sums its rows in lookup order, 8 row loads (16 B/lane, 512 B coalesced per row) in
-  // flight per step, flushing a bag's pooled vector the moment its last lookup was added.  The
-  // next pass's indices are loaded while this pass works.  Validation (seqlock) once per pass:
-  // the tag re-read's address depends on every row value of the pass, so it is issued after all
-  // of them returned.  A failed validation (a page changed identity mid-read: rare) redoes the
-  // block from its first lookup — already flushed bags are simply rewritten — and after 4
-  // failures the block is pooled row by row, each row validated on its own.
-  __device__ bool pool_block(const DevCtx& c, u32 first, u32 nb, u32 who, u32 gw, u32& misses, u32& lookups) const {
-    const u32 lane = lane_id();
-    u64 s0, s1;
-    long long bend = 0;   // lane k < nb: flat end position of bag first + k
-    if (offsets) {
-      const long long o = lane <= nb ? __ldg(offsets + first + lane) : 0ll;
-      s0 = (u64)__shfl_sync(FULL, o, 0);
-      s1 = (u64)__shfl_sync(FULL, o, nb);
-      bend = __shfl_down_sync(FULL, o, 1);
-      // an empty bag has no lookup to flush it: it pools to zero here
-      const bool empty = lane < nb && bend <= o;
-      u32 em = __ballot_sync(FULL, empty);
-      while (em) {
-        const u32 k = __ffs(em) - 1;
-        em &= em - 1;
-        const u32 bag = first + k, b = bag / T;
-        const TabDesc td = tab(bag - b * T);
-        store_pooled((u64)b * out_row_bytes + td.out_off, td.flags, 0.0, 0.0, 0.0, 0.0);
-      }
-    } else {
-      s0 = (u64)first * L;
-      s1 = s0 + (u64)nb * L;
-    }
-    const bool dims = lane * 4 < D;
-    double a0, a1, a2, a3;
-    u32 fails = 0;
-    u64 counted = s0;   // passes below this position were counted (a redo does not count twice)
-    Spin rsp;
-  restart:
-    a0 = a1 = a2 = a3 = 0.0;
-    long long r_nx = s0 + lane < s1 ? __ldg(idx + s0 + lane) : 0ll;
-    for (u64 q0 = s0; q0 < s1; q0 += 32) {
-      const u64 p = q0 + lane;
-      const bool lact = p < s1;
-      const long long r = r_nx;
-      if (q0 + 32 < s1) r_nx = p + 32 < s1 ? __ldg(idx + p + 32) : 0ll;   // next pass, in flight now
-      // the bag of position p and whether p is its last lookup
-      u32 k;
-      bool last;
-      block_pos(first, nb, s0, s1, bend, p, k, last);
-      const u32 bag = first + (lact ? k : 0u), b = bag / T, t = bag - b * T;
-      const TabDesc td = tab(t);
-      const u64 obase = (u64)b * out_row_bytes + td.out_off;
-      u64 key = 0; u32 off = 0;
-      const bool a = lookup_key(c, td, lact, r, t, key, off);
-      const u32 am = __ballot_sync(FULL, a);
-      const u32 endm = __ballot_sync(FULL, last);
-      const u32 npos = __popc(__ballot_sync(FULL, lact));   // positions form a prefix of the lanes
-      const bool first_visit = q0 >= counted;
-      if (first_visit) {
-        lookups += __popc(am);
-        counted = q0 + 32;
-      }
-      u32 line = NONE; u64 word = 0;
-      {
-        probe_lanes<true>(c, a, key, line, word);
-        const bool ready = a && line != NONE && (tw_state(word) == ST_READY || tw_state(word) == ST_MODIFIED);
-        if (ready && !tw_ref(word)) atomicOr(&c.tags[line], REF_BIT);   // on_hit
-        const u32 need = __ballot_sync(FULL, a && !ready);
-        if (need) {
-          if (first_visit) misses += __popc(need);
-          const Resolved rs = resolve_misses(c, need, key, who, gw, line, word);
-          if (!rs.ok) return false;
-          line = rs.line;
-          word = rs.word;
-        }
-      }
-      const u64 rowaddr = a ? (u64)(uintptr_t)(line_ptr(c, line) + off) : 0ull;
-      u32 dep = 0;
-      // rows in lookup order as a rolling pipeline: the load of row s + kRif is issued before row
-      // s is added, so kRif row loads are in flight per lane while the adds run
-      float4 v[kRif];
-#pragma unroll
-      for (u32 j = 0; j < kRif; ++j) {
-        const u64 ra = __shfl_sync(FULL, rowaddr, j);
-        v[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (((am >> j) & 1u) && dims) v[j] = __ldcg(reinterpret_cast<const float4*>(ra) + lane);
-      }
-#pragma unroll
-      for (u32 s = 0; s < 32; ++s) {
-        if (s >= npos) break;
-        const float4 x = v[s % kRif];
-        if (s + kRif < 32) {
-          const u32 sn = s + kRif;
-          const u64 ra = __shfl_sync(FULL, rowaddr, sn);
-          v[s % kRif] = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (((am >> sn) & 1u) && dims) v[s % kRif] = __ldcg(reinterpret_cast<const float4*>(ra) + lane);
-        }
-        a0 += (double)x.x; a1 += (double)x.y; a2 += (double)x.z; a3 += (double)x.w;
-        dep |= __float_as_uint(x.x) | __float_as_uint(x.w);
-        if ((endm >> s) & 1u) {   // bag complete: store its pooled vector
-          store_pooled(__shfl_sync(FULL, obase, s), __shfl_sync(FULL, td.flags, s), a0, a1, a2, a3);
-          a0 = a1 = a2 = a3 = 0.0;
-        }
-      }
-      // seqlock validation, once per pass: the tag re-read's address depends on every row value
-      // of the pass (redux over the lanes), so it is issued after all of them were loaded
-      const u64 z = dep_zero(__reduce_or_sync(FULL, dep));
-      bool bad = false;
-      if (a) bad = ((ld_relaxed(&c.tags[line] + z) ^ word) & IDENT_MASK) != 0;
-      if (__any_sync(FULL, bad)) {
-        if (++fails >= 4) return pool_block_slow(c, first, nb, s0, s1, bend, counted, who, gw, lookups);
-        if (!rsp.again(c, 256, __LINE__ + 100000 * SPIN_FILE_ID)) return false;
-        goto restart;
-      }
-    }
-    return true;
-  }
-
-  // the bag position info of flat position p of a block (see pool_block)
-  __device__ __forceinline__ void block_pos(u32 first, u32 nb, u64 s0, u64 s1, long long bend, u64 p, u32& k,
-                                            bool& last) const {
-    const bool lact = p < s1;
-    if (offsets) {
-      k = 0;
-      for (u32 j = 0; j < nb; ++j) k += (u64)__shfl_sync(FULL, bend, j) <= p ? 1u : 0u;
-      last = lact && (u64)__shfl_sync(FULL, bend, k < 31 ? k : 31) == p + 1;
-    } else {
-      const u32 rel = (u32)(p - s0);   // < kGrab * L
-      k = rel / L;
-      last = lact && rel - k * L == L - 1;
-    }
-  }
-
-  // Slow path of pool_block: every row read and validated on its own (row_one), bags flushed in
-  // lookup order as in the fast path.  Out of line.
-  __device__ __noinline__ bool pool_block_slow(const DevCtx& c, u32 first, u32 nb, u64 s0, u64 s1, long long bend,
-                                               u64 counted, u32 who, u32 gw, u32& lookups) const {
-    const u32 lane = lane_id();
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    for (u64 q0 = s0; q0 < s1; q0 += 32) {
-      const u64 p = q0 + lane;
-      const bool lact = p < s1;
-      u32 k;
-      bool last;
-      block_pos(first, nb, s0, s1, bend, p, k, last);
-      const long long r = lact ? __ldg(idx + p) : 0ll;
-      const u32 bag = first + (lact ? k : 0u), b = bag / T, t = bag - b * T;
-      const TabDesc td = tab(t);
-      const u64 obase = (u64)b * out_row_bytes + td.out_off;
-      u64 key = 0; u32 off = 0;
-      const bool a = lookup_key(c, td, lact, r, t, key, off);
-      const u32 am = __ballot_sync(FULL, a);
-      const u32 endm = __ballot_sync(FULL, last);
-      const u32 npos = __popc(__ballot_sync(FULL, lact));
-      if (q0 >= counted) lookups += __popc(am);   // passes the fast path never reached
-      for (u32 s = 0; s < npos; ++s) {
-        if ((am >> s) & 1u) {
-          const Row1 r1 = row_one(c, __shfl_sync(FULL, key, s), __shfl_sync(FULL, off, s), who, gw);
-          if (!r1.ok) return false;
-          a0 += (double)r1.v.x; a1 += (double)r1.v.y; a2 += (double)r1.v.z; a3 += (double)r1.v.w;
-        }
-        if ((endm >> s) & 1u) {
-          store_pooled(__shfl_sync(FULL, obase, s), __shfl_sync(FULL, td.flags, s), a0, a1, a2, a3);
-          a0 = a1 = a2 = a3 = 0.0;
-        }
-      }
-    }
-    return true;
-  }
-
-  __device__ __forceinline__ void store_pooled(u64 ob, u32 fl, double a0, double a1, double a2, double a3) const {
-    const u32 lane = lane_id();
-    uint8_t* o8 = out + ob;
-    if (lane * 4 < D) {
-      if (fl & TAB_PARTIAL_F64) {
-        reinterpret_cast<double2*>(o8)[2 * lane] = make_double2(a0, a1);
-        reinterpret_cast<double2*>(o8)[2 * lane + 1] = make_double2(a2, a3);
-      } else {
-        reinterpret_cast<float4*>(o8)[lane] = make_float4((float)a0, (float)a1, (float)a2, (float)a3);
-      }
-    }
-  }
-
-  // one row slice (lane: dims [4*lane, 4*lane+4)) of the lookup (key, off), read and validated on
-  // its own: access (claim or attach on a miss), wait READY, read, re-read the tag identity
-  struct Row1 { float4 v; u32 ok; };
-  __device__ __noinline__ Row1 row_one(const DevCtx& c, u64 kl, u32 ol, u32 who, u32 gw) const {
-    const u32 lane = lane_id();
-    Row1 res;
-    res.v = make_float4(0.f, 0.f, 0.f, 0.f);
-    res.ok = 0;
-    Spin s3;
-    while (true) {
-      if (aborted(c)) return res;
-      const Req r = access_warp(c, lane == 0, kl, false, who, gw, false);
-      const int kind = __shfl_sync(FULL, r.kind, 0);
-      if (kind == R_HIT || kind == R_FILLING || kind == R_MISS) {
-        const u32 ln = __shfl_sync(FULL, r.line, 0);
-        u64 w = 0;
-        Spin s4;
-        while (true) {
-          w = ld_acquire(&c.tags[ln]);
-          if (!tw_live(w) || tw_key(w) != kl) break;
-          if (tw_state(w) == ST_READY || tw_state(w) == ST_MODIFIED) break;
-          if (!s4.again(c, 1024, __LINE__ + 100000 * SPIN_FILE_ID)) return res;
-        }
-        if (tw_live(w) && tw_key(w) == kl && tw_state(w) >= ST_READY) {
-          float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (lane * 4 < D) v = __ldcg(reinterpret_cast<const float4*>(line_ptr(c, ln) + ol) + lane);
-          const u64 z = dep_zero(__reduce_or_sync(FULL, __float_as_uint(v.x) | __float_as_uint(v.w)));
-          if (((ld_relaxed(&c.tags[ln] + z) ^ w) & IDENT_MASK) == 0) {
-            res.v = v;
-            res.ok = 1;
-            return res;
-          }
-        }
-      }
-      if (!s3.again(c, 1024, __LINE__ + 100000 * SPIN_FILE_ID)) return res;
-    }
   }
 
   struct Acc4 { double v[4]; u32 ok; };
@@ -1216,7 +1018,7 @@ __device__ __forceinline__ u32 window_slot(long long ev, long long x) {
 // shuffle search.  Discovery: one relaxed read of the visited bitmap (L2-resident: V/8 bytes),
 // atomicOr only for unseen vertices, level[] store, and the next-frontier bitmap.  Async mode
 // (pd > 0): a warp grabs pd chunks ahead and prefetches their pages before expanding the oldest
-// (the AGILE prefetch pattern, gpu_api.py:345-361); pd = 0 is the synchronous baseline.
+// (the AGILE prefetch pattern, gpu_api.py:139-155); pd = 0 is the synchronous baseline.
 struct BfsWork {
   const long long* row_ptr;   // [rows+1] (HBM), row of vertex v at row_ptr[v - v0]
   u32 v0;                     // first vertex of the partition (1D vertex partition; 0 = whole graph)

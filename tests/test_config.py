@@ -9,7 +9,7 @@ from paper_2504_19365_b200.config import (ExperimentConfig, SystemConfig, apply_
                                           parse_config_file)
 
 GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "golden.json")))["config"]
-B200_KEYS = ("device.emulation", "cache.ways", "engine.warps", "engine.side_warps", "service.side_warps", "backend",
+B200_KEYS = ("device.emulation", "cache.ways", "engine.warps", "engine.side_warps", "engine.copy", "service.side_warps", "backend",
              "dlrm_", "graph_", "pagerank_")
 
 

@@ -90,3 +90,18 @@ def test_combine_replays_single_device_result():
         for p in range(G):
             recv = torch.cat([sends[q][p * nl:(p + 1) * nl].reshape(-1) for q in range(G)])
             assert np.array_equal(combine(plan, recv, nl).numpy(), ref[p * nl:(p + 1) * nl])
+
+
+def test_torch_op_registered_with_fake_kernel():
+    """torch.ops.agile.embedding_bag exists and shape-propagates under FakeTensorMode (no device)."""
+    import torch
+    from torch._subclasses.fake_tensor import FakeTensorMode
+    from paper_2504_19365_b200 import ops  # noqa: F401
+    with FakeTensorMode():
+        idx = torch.empty(4, 3, 20, dtype=torch.int64)
+        k = torch.empty(3, dtype=torch.int64)
+        out = torch.ops.agile.embedding_bag(0, idx, None, k, k, 64)
+        assert tuple(out.shape) == (4, 3, 64) and out.dtype == torch.float32
+        off = torch.empty(3 * 5 + 1, dtype=torch.int64)
+        out = torch.ops.agile.embedding_bag(0, torch.empty(40, dtype=torch.int64), off, k, k, 64)
+        assert tuple(out.shape) == (5, 3, 64)

@@ -41,11 +41,16 @@ def main():
     cfg.queues.pairs_per_device = 128
     cfg.queues.sq_depth = 256
     cfg.queues.cq_depth = 256
-    cfg.engine.warps = 128
-    cfg.service.warps = 48
+    cfg.engine.warps = int(os.environ.get("K5_ENGINE_WARPS", 128))
+    cfg.service.warps = int(os.environ.get("K5_SERVICE_WARPS", 48))
     cfg.service.idle_max_ns = 1600
+    cfg.engine.copy = os.environ.get("K5_ENGINE_COPY", "registers")
     cfg.debug_locks = False
     s = AgileSystem(cfg, device=0)
+    if os.environ.get("K5_SOLO") == "1":
+        # warm-up runs need the engine: one fused grid (ncu with a kernel filter lets the
+        # co-residency probe's kernels overlap, yet serialises the user kernel it profiles)
+        s.set_launch_mode("fused")
     fill_rank_store(s, plan, 0, 5)
     gen = torch.Generator(device=dev).manual_seed(3)
     if mode == "uniform":
@@ -79,7 +84,7 @@ def main():
     c = cnt.cpu().numpy()
     print(json.dumps({"mode": mode, "ms": ms, "alg_gbs": alg / ms / 1e6, "frac": alg / ms / 1e6 / peak,
                       "lookups_per_s": B * T * L / ms * 1e3, "miss_lookups": int(c[1]),
-                      "lib": os.environ.get("AGILE_LIB", "default"), "launch": s.launch_mode,
+                      "lib": os.environ.get("AGILE_LIB", "default"), "engine_copy": cfg.engine.copy, "launch": s.launch_mode,
                       "grid": s.embbag_grid()}), flush=True)
     s.close()
 
