@@ -139,8 +139,10 @@ int agile_run_loop_rw(agile_ctx* ctx, uint32_t conc, uint64_t warmup_ns, uint64_
  * victim is claimed) and is written through to the device store before the call returns. */
 int agile_write_blocks(agile_ctx* ctx, const uint32_t* dev, const uint64_t* blk, int64_t n, const void* pages);
 
-/* SoftwareCache.evict per block (software_cache.py:268-281): outcome[i] 0 = RESET (the READY line
- * was dropped), 1 = DEFERRED (busy, pinned or modified), 2 = not resident. */
+/* SoftwareCache.evict per block (software_cache.py:268-281, _evict_locked 335-353): outcome[i]
+ * 0 = RESET (the READY line was dropped), 1 = DEFERRED (busy or pinned), 2 = not resident (the
+ * reference reports RESET for an absent / INVALID line), 3 = WRITEBACK_STARTED (a MODIFIED line:
+ * written back, then INVALID). */
 int agile_evict_blocks(agile_ctx* ctx, const uint32_t* dev, const uint64_t* blk, int64_t n, int8_t* outcome);
 
 /* AgileApi.array_get (gpu_api.py:250-278), n elements at once, host arrays: element idx[i] of
@@ -150,6 +152,21 @@ int agile_evict_blocks(agile_ctx* ctx, const uint32_t* dev, const uint64_t* blk,
  * bytes land at out + i * elem_size. */
 int agile_array_get(agile_ctx* ctx, const uint32_t* dev, const uint64_t* idx, int64_t n, uint32_t elem_size,
                     void* out);
+
+/* SoftwareCache.flush (software_cache.py:283-298): write back every MODIFIED line (lines the share
+ * table drained into the cache) and wait for durability; *flushed = lines written back. */
+int agile_flush(agile_ctx* ctx, uint64_t* flushed);
+/* ShareTable.live_entries (share_table.py:198-199) */
+int agile_share_live(agile_ctx* ctx, uint64_t* live);
+/* The reference's coherence replay workload (tests/test_coherence.py:27-60) with share_table.enabled
+ * on or off: tasks (<= 8, one warp each) run plans of op[t][i] (0 read, 1 write) on block
+ * blk[t][i] of device 0 after think[t][i] ns; writes carry the prefix 1<<30 | t<<16 | i; reads
+ * observe the first 8 bytes of the buffer they got (seen[t][i]); with the table every read holds
+ * its reference to the end, then releases; finally every MODIFIED line is flushed (*flushed).  The
+ * event log (agile_trace_enable) carries the reference's install / write_commit / observe records
+ * in a commit-consistent order for the sequential replay. */
+int agile_run_coherence(agile_ctx* ctx, const uint8_t* op, const uint32_t* blk, const uint32_t* think, uint32_t tasks,
+                        uint32_t ops, uint64_t* seen, uint64_t* flushed);
 
 /* Gather epochs (bench/sweeps.py:39-88): keys[tasks][epochs][gathers]; values = u32 element 0
  * of every gathered block; epoch_t[2] = start/end. */

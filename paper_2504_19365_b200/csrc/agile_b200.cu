@@ -513,7 +513,10 @@ int agile_create(const char* config_text, int cuda_device, agile_ctx** out) {
   if (policy != "clock" && policy != "modulo") return fail(ctx, AGILE_E_CONFIG, "unknown cache policy '" + policy + "'");
   if (busy != "wait" && busy != "find_another") return fail(ctx, AGILE_E_CONFIG, "cache.busy_choice must be wait|find_another");
   if (engine_copy != "registers" && engine_copy != "bulk") return fail(ctx, AGILE_E_CONFIG, "engine.copy must be registers|bulk");
-  if (cfg.b("share_table.enabled", false)) return fail(ctx, AGILE_E_CONFIG, "share_table.enabled=true is not supported on the B200 path (SURVEY 8(f))");
+  const bool st_on = cfg.b("share_table.enabled", false);
+  const uint64_t st_buckets = cfg.u("share_table.buckets", 256);
+  if (st_on && (st_buckets < 2 || !pow2(st_buckets) || st_buckets > (1ull << 24)))
+    return fail(ctx, AGILE_E_CONFIG, "share_table.buckets must be a power of two >= 2");   // share_table.py:57-58
   if (cfg.u("device.parallelism", 16) > 32 * kMaxChanPerLane) return fail(ctx, AGILE_E_CONFIG, "device.parallelism must be <= 256");
   if (emu != "model" && emu != "link") return fail(ctx, AGILE_E_CONFIG, "device.emulation must be model|link");
   if (jitter != "none" && jitter != "uniform" && jitter != "exponential") return fail(ctx, AGILE_E_CONFIG, "unknown jitter kind");
@@ -563,6 +566,11 @@ int agile_create(const char* config_text, int cuda_device, agile_ctx** out) {
   if ((rc = dalloc(ctx, &d.wl, lines))) return rc;
   if ((rc = dalloc(ctx, &d.set_lock, d.num_sets))) return rc;
   if ((rc = dalloc(ctx, &d.hand, d.num_sets))) return rc;
+  d.st_buckets = st_on ? (uint32_t)st_buckets : 0u;
+  if (st_on) {
+    if ((rc = dalloc(ctx, &d.st, st_buckets))) return rc;
+    if ((rc = dalloc(ctx, &d.st_lock, st_buckets))) return rc;
+  }
   if ((rc = dalloc(ctx, &d.lines, lines * kBlockBytes))) return rc;
   const size_t nsq = (size_t)d.num_qp * d.sq_depth;
   if ((rc = dalloc(ctx, &d.sqe, nsq * 4))) return rc;
@@ -778,6 +786,10 @@ int agile_reset(agile_ctx* ctx, int flags) {
     CK(cudaMemset(d.wl, 0, (size_t)d.num_lines * 8));
     CK(cudaMemset(d.hand, 0, (size_t)d.num_sets * 4));
     CK(cudaMemset(d.set_lock, 0, (size_t)d.num_sets * 4));
+    if (d.st_buckets) {
+      CK(cudaMemset(d.st, 0, (size_t)d.st_buckets * sizeof(ShareEntry)));
+      CK(cudaMemset(d.st_lock, 0, (size_t)d.st_buckets * 4));
+    }
   }
   if (flags & 2) {
     const size_t nsq = (size_t)d.num_qp * d.sq_depth;
@@ -935,6 +947,68 @@ int agile_set_launch_mode(agile_ctx* ctx, int mode) {
   ctx->fused = mode == 1;
   ctx->d.solo_ok = mode == 2 ? 1u : 0u;
   ctx->d.user_start_ns = mode == 2 ? 100ull * 1000 * 1000 : ctx->d.watchdog_ns;
+  return 0;
+}
+
+int agile_run_coherence(agile_ctx* ctx, const uint8_t* op, const uint32_t* blk, const uint32_t* think, uint32_t tasks,
+                        uint32_t ops, uint64_t* seen, uint64_t* flushed) {
+  if (!ctx || !tasks || tasks > kCtaWarps || !ops || !op || !blk || !think || !seen)
+    return fail(ctx, AGILE_E_ARG, "bad coherence args (1..8 tasks)");
+  CK(cudaSetDevice(ctx->device));
+  const size_t n = (size_t)tasks * ops;
+  for (size_t i = 0; i < n; ++i)
+    if (blk[i] >= ctx->store_blocks[0]) return fail(ctx, AGILE_E_OUT_OF_RANGE, "block out of range");
+  DevTmp tmp;
+  uint8_t* d_op; uint32_t* d_blk; uint32_t* d_think; uint64_t* d_seen; uint64_t* d_fl; uint4* d_w; uint4* d_r; uint4* d_s;
+  CK(tmp.alloc(&d_op, n));
+  CK(tmp.alloc(&d_blk, n * 4));
+  CK(tmp.alloc(&d_think, n * 4));
+  CK(tmp.alloc(&d_seen, n * 8));
+  CK(tmp.alloc(&d_fl, 8));
+  CK(tmp.alloc(&d_w, (size_t)tasks * kBlockBytes));
+  CK(tmp.alloc(&d_r, n * kBlockBytes));
+  CK(tmp.alloc(&d_s, (size_t)tasks * kBlockBytes));
+  CK(cudaMemcpy(d_op, op, n, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(d_blk, blk, n * 4, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(d_think, think, n * 4, cudaMemcpyHostToDevice));
+  CK(cudaMemset(d_seen, 0, n * 8));
+  CoherenceWork w;
+  w.op = d_op; w.blk = d_blk; w.think = d_think; w.tasks = tasks; w.ops = ops;
+  w.wbuf = d_w; w.rbuf = d_r; w.snap = d_s; w.seen = reinterpret_cast<u64*>(d_seen);
+  w.flushed = reinterpret_cast<u64*>(d_fl);
+  w.nodes = get_nodes(ctx, n + tasks + 32);
+  if (!w.nodes) return fail(ctx, AGILE_E_CUDA, "node allocation failed");
+  int rc = launch(ctx, w, 1, ctx->stream);
+  if (!rc) rc = agile_sync(ctx, ctx->stream);
+  if (!rc) CK(cudaMemcpy(seen, d_seen, n * 8, cudaMemcpyDeviceToHost));
+  if (!rc && flushed) CK(cudaMemcpy(flushed, d_fl, 8, cudaMemcpyDeviceToHost));
+  return rc;
+}
+
+int agile_flush(agile_ctx* ctx, uint64_t* flushed) {
+  if (!ctx) return AGILE_E_ARG;
+  CK(cudaSetDevice(ctx->device));
+  DevTmp tmp;
+  uint64_t* d_fl;
+  CK(tmp.alloc(&d_fl, 8));
+  FlushWork w;
+  w.nodes = get_nodes(ctx, 32);
+  w.flushed = reinterpret_cast<u64*>(d_fl);
+  if (!w.nodes) return fail(ctx, AGILE_E_CUDA, "node allocation failed");
+  int rc = launch(ctx, w, 1, ctx->stream);
+  if (!rc) rc = agile_sync(ctx, ctx->stream);
+  if (!rc && flushed) CK(cudaMemcpy(flushed, d_fl, 8, cudaMemcpyDeviceToHost));
+  return rc;
+}
+
+int agile_share_live(agile_ctx* ctx, uint64_t* live) {
+  if (!ctx || !live) return AGILE_E_ARG;
+  *live = 0;
+  if (!ctx->d.st_buckets) return 0;
+  CK(cudaSetDevice(ctx->device));
+  std::vector<ShareEntry> e(ctx->d.st_buckets);
+  CK(cudaMemcpy(e.data(), ctx->d.st, e.size() * sizeof(ShareEntry), cudaMemcpyDeviceToHost));
+  for (const auto& x : e) *live += x.key >= 2 ? 1 : 0;   // share_table.py:198-199 live_entries
   return 0;
 }
 

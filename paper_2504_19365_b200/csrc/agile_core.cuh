@@ -18,7 +18,10 @@ constexpr u32 FULL = 0xffffffffu;
 constexpr u32 NONE = 0xffffffffu;
 
 // access outcomes (software_cache.py:37-41)
-enum : int { R_NONE = -1, R_HIT = 0, R_FILLING = 1, R_MISS = 2, R_RETRY = 3 };
+// R_WBEVICT: the chosen victim was MODIFIED; the claimant started its write-back (the line is
+// BUSY with the OLD key until the write is durable, then INVALID) and must submit that WRITE
+// (K_WB_EVICT) and retry (software_cache.py:348-353, 482-486)
+enum : int { R_NONE = -1, R_HIT = 0, R_FILLING = 1, R_MISS = 2, R_RETRY = 3, R_WBEVICT = 4 };
 
 struct Launch {
   u32 n_user_ctas;
@@ -350,6 +353,27 @@ __device__ int claim_key_warp(const DevCtx& c, u64 key, u32 pin_n, u32 who, u32&
       unlock_set(c, set);
       return R_RETRY;
     }
+    if (tw_state(old) == ST_MODIFIED) {
+      // MODIFIED victim: write it back first (R_WBEVICT), claim the freed line on the retry
+      const u64 nwb = tw_make(ST_BUSY, tw_key(old), tw_ver(old) + 1, false, 0);
+      u64 pv = 0;
+      if (lane == 0) {
+        st_relaxed(&c.wl[base + v], ((u64)((tw_ver(old) + 1) & 0x1FFu)) << 55);
+        pv = atom_cas_acqrel(&c.tags[base + v], old, nwb);
+      }
+      pv = __shfl_sync(FULL, pv, 0);
+      if (pv != old) continue;
+      if (lane == 0) {
+        st_relaxed(&c.hand[set], new_hand);
+        log_ev(c, who, M_CACHE, A_EVICT_WB, base + v, key_dev(tw_key(old)), key_blk(tw_key(old)));
+        log_state(c, who, (u32)(base + v), ST_MODIFIED, ST_BUSY, tw_key(old));
+      }
+      unlock_set(c, set);
+      victim_key = tw_key(old);
+      line = (u32)(base + v);
+      word = nwb;
+      return R_WBEVICT;
+    }
     const u64 nw = tw_make(ST_BUSY, key, tw_ver(old) + 1, true, pin_n);
     u64 prev = 0;
     if (lane == 0) {
@@ -457,7 +481,22 @@ __device__ int claim_lanes(const DevCtx& c, bool want, u64 key, u32 pin_n, u32 w
           settled = true;
         } else {
           const u64 old = ld_relaxed(&c.tags[base + v]);
-          if (tw_state(old) != ST_BUSY && tw_pins(old) == 0) {
+          if (tw_state(old) == ST_MODIFIED && tw_pins(old) == 0) {
+            // MODIFIED victim: write it back first, claim the freed line on the retry
+            const u64 nw = tw_make(ST_BUSY, tw_key(old), tw_ver(old) + 1, false, 0);
+            st_relaxed(&c.wl[base + v], ((u64)((tw_ver(old) + 1) & 0x1FFu)) << 55);
+            if (atom_cas_acqrel(&c.tags[base + v], old, nw) == old) {
+              for (u32 m = cleared; m; m &= m - 1) atomicAnd(&c.tags[base + (__ffs(m) - 1)], ~REF_BIT);
+              st_relaxed(&c.hand[set], nh);
+              victim_key = tw_key(old);
+              log_ev(c, who, M_CACHE, A_EVICT_WB, base + v, key_dev(victim_key), key_blk(victim_key));
+              log_state(c, who, (u32)(base + v), ST_MODIFIED, ST_BUSY, victim_key);
+              kind = R_WBEVICT;
+              line = (u32)(base + v);
+              word = nw;
+              settled = true;
+            }
+          } else if (tw_state(old) != ST_BUSY && tw_pins(old) == 0) {
             const u64 nw = tw_make(ST_BUSY, key, tw_ver(old) + 1, true, pin_n);
             st_relaxed(&c.wl[base + v], ((u64)((tw_ver(old) + 1) & 0x1FFu)) << 55);   // open the waiter list
             if (atom_cas_acqrel(&c.tags[base + v], old, nw) == old) {
@@ -713,7 +752,9 @@ __device__ Req access_warp(const DevCtx& c, bool active, u64 key, bool pin, u32 
   }
   // misses: lane-parallel claims under per-set locks (W <= 32); one key at a time otherwise
   const u32 mb = __ballot_sync(FULL, leader && !resolved);
-  bool need_submit = false;
+  bool need_submit = false, need_wb = false;
+  u32 wb_line = NONE;
+  u64 wb_key = 0;
   if (mb) {
     if (c.ways <= 32) {
       u32 cl = NONE; u64 cw = 0, vk = ~0ull;
@@ -721,6 +762,7 @@ __device__ Req access_warp(const DevCtx& c, bool active, u64 key, bool pin, u32 
       const int kind = claim_lanes(c, wl, key, pin ? gsize : 0u, who, cl, cw, vk);
       if (wl) {
         if (kind == R_RETRY || kind == R_NONE) r.kind = R_RETRY;
+        else if (kind == R_WBEVICT) { r.kind = R_RETRY; need_wb = true; wb_line = cl; wb_key = vk; }
         else { r.line = cl; r.word = cw; r.kind = kind; r.victim = vk; need_submit = kind == R_MISS; }
       }
     } else {
@@ -734,15 +776,21 @@ __device__ Req access_warp(const DevCtx& c, bool active, u64 key, bool pin, u32 
         const int kind = claim_key_warp(c, k, pn, __shfl_sync(FULL, who, src), cl, cw, vk);
         if (lane == (u32)src) {
           if (kind == R_RETRY) r.kind = R_RETRY;
+          else if (kind == R_WBEVICT) { r.kind = R_RETRY; need_wb = true; wb_line = cl; wb_key = vk; }
           else { r.line = cl; r.word = cw; r.kind = kind; r.victim = vk; need_submit = kind == R_MISS; }
         }
       }
     }
   }
-  // submit fills (warp-aggregated)
-  if (__any_sync(FULL, need_submit)) {
-    if (!submit_warp(c, need_submit, key_dev(key), key_blk(key), r.line, K_FILL, OP_READ, 0, key, who, sq_start))
-      if (need_submit) r.kind = R_NONE;
+  // submit fills and eviction write-backs (warp-aggregated)
+  if (__any_sync(FULL, need_submit || need_wb)) {
+    const bool sub = need_submit || need_wb;
+    const u64 sk = need_wb ? wb_key : key;
+    if (!submit_warp(c, sub, key_dev(sk), key_blk(sk), need_wb ? wb_line : r.line, need_wb ? K_WB_EVICT : K_FILL,
+                     need_wb ? OP_WRITE : OP_READ, 0, sk, who, sq_start))
+      if (sub) r.kind = R_NONE;
+    const u32 nwb = __popc(__ballot_sync(FULL, need_wb));
+    if (lane == 0 && nwb) atomicAdd(&c.stats[S_WRITEBACKS], (u64)nwb);
   }
   // accounting + trace
   u32 hits = 0, attaches = 0, misses = 0;
@@ -914,18 +962,25 @@ __device__ __forceinline__ bool wait_ready_lane(const DevCtx& c, u32 line, u64 k
   return tw_state(w) == ST_READY || tw_state(w) == ST_MODIFIED;
 }
 
-// async_write (gpu_api.py:192-227 -> SoftwareCache._try_write / _install_locked /
-// _allocate_locked, software_cache.py:458-523, eager=True): the 4 KiB at `src` land in the
-// block's cache line and a device write (WB_KEEP) starts at once; the line is BUSY until the
-// write is durable, then READY (complete_io, software_cache.py:533-537).  `node` is the
-// write-back barrier: the service clears it when the write completed (node->dst = 0: no copy).
-// Resident READY/MODIFIED line with no pins: CAS -> BUSY, version + 1 (readers validating the
-// old identity see the change).  Not resident: a victim is claimed exactly like a fill (evicting
-// a READY line; every line is written through, so no MODIFIED victim exists without the share
-// table).  BUSY or pinned lines, and later lanes writing a block an earlier lane of the warp
-// writes, retry (RETRY + ready_wait in the reference).  Warp-collective; no pin is held.
-__device__ void async_write_warp(const DevCtx& c, bool active, u64 key, WaitNode* node, const uint4* src,
-                                 u32 who, u32 sq_start) {
+__device__ void deliver_waiters_warp(const DevCtx& c, u64 cur, u32 line);
+
+// Block write (SoftwareCache._try_write / _install_locked / _allocate_locked,
+// software_cache.py:458-523), warp-collective: the 4 KiB at `src` land in the block's cache line.
+//   eager (async_write, gpu_api.py:192-227; write_block, software_cache.py:221-235): a device write
+//     (WB_KEEP) starts at once and the line is BUSY until it is durable, then READY
+//     (complete_io); `node` is the durability handle, released by the service.
+//   !eager (install_modified, software_cache.py:242-254: share-table data draining back): no device
+//     write — the line is left MODIFIED; async_read waiters that attached meanwhile get the new bytes;
+//     `node` is released on return.
+// Resident READY/MODIFIED line with no pins: CAS -> BUSY, version + 1 (readers validating the old
+// identity see the change).  Not resident: a victim is claimed like a fill; a MODIFIED victim is
+// written back first (WB_EVICT) and the claim retried.  BUSY or pinned lines, and later lanes writing
+// a block an earlier lane of the warp writes, retry (RETRY + ready_wait in the reference).  No pin
+// is held.
+// once: a single attempt (callers that re-check other state between attempts, the share table);
+// returns true for lanes still pending.
+__device__ bool write_block_warp(const DevCtx& c, bool active, u64 key, WaitNode* node, const uint4* src,
+                                 u32 who, u32 sq_start, bool eager, bool once = false) {
   const u32 lane = lane_id();
   if (active) {
     const u32 dv = key_dev(key);
@@ -969,12 +1024,17 @@ __device__ void async_write_warp(const DevCtx& c, bool active, u64 key, WaitNode
       }
     }
     const u32 mb = __ballot_sync(FULL, go && line == NONE);
+    bool need_wb = false;
+    u32 wb_line = NONE;
+    u64 wb_key = 0;
     if (mb) {
       u32 cl = NONE; u64 cw = 0, vk = ~0ull;
       const bool wl = (mb >> lane) & 1u;
-      const int kind = c.ways <= 32 ? claim_lanes(c, wl, key, 0u, who, cl, cw, vk) : R_RETRY;
-      if (wl && kind == R_MISS) { own = true; line = cl; word = cw; ver = tw_ver(cw); }
-      if (c.ways > 32) {
+      if (c.ways <= 32) {
+        const int kind = claim_lanes(c, wl, key, 0u, who, cl, cw, vk);
+        if (wl && kind == R_MISS) { own = true; line = cl; word = cw; ver = tw_ver(cw); }
+        if (wl && kind == R_WBEVICT) { need_wb = true; wb_line = cl; wb_key = vk; }
+      } else {
         // generic geometry: one key at a time
         u32 m2 = mb;
         while (m2) {
@@ -983,12 +1043,21 @@ __device__ void async_write_warp(const DevCtx& c, bool active, u64 key, WaitNode
           u32 l2; u64 w2, v2;
           const int k2 = claim_key_warp(c, __shfl_sync(FULL, key, l), 0u, __shfl_sync(FULL, who, l), l2, w2, v2);
           if (lane == (u32)l && k2 == R_MISS) { own = true; line = l2; word = w2; ver = tw_ver(w2); }
+          if (lane == (u32)l && k2 == R_WBEVICT) { need_wb = true; wb_line = l2; wb_key = v2; }
         }
       }
     }
-    // owners: register the durability handle, land the bytes, start the write-back
+    // a MODIFIED victim's write-back: submitted now, the claim is retried once it is durable
+    if (__any_sync(FULL, need_wb)) {
+      if (!submit_warp(c, need_wb, key_dev(wb_key), key_blk(wb_key), wb_line, K_WB_EVICT, OP_WRITE, 0, wb_key, who,
+                       sq_start))
+        break;
+      const u32 nwb = __popc(__ballot_sync(FULL, need_wb));
+      if (lane == 0 && nwb) atomicAdd(&c.stats[S_WRITEBACKS], (u64)nwb);
+    }
+    // owners: register the durability handle (eager), land the bytes
     bool pushed = false;
-    if (own) pushed = wl_push(c, line, ver, node);
+    if (own && eager) pushed = wl_push(c, line, ver, node);
     u32 ob = __ballot_sync(FULL, own);
     while (ob) {
       const int l = __ffs(ob) - 1;
@@ -1000,19 +1069,39 @@ __device__ void async_write_warp(const DevCtx& c, bool active, u64 key, WaitNode
     __syncwarp();
     if (__any_sync(FULL, own)) {
       if (own) log_ev(c, who, M_CACHE, A_INSTALL, key_dev(key), key_blk(key), *reinterpret_cast<const u64*>(src));
-      const u32 nwb = __popc(__ballot_sync(FULL, own));
-      if (lane == 0) atomicAdd(&c.stats[S_WRITEBACKS], (u64)nwb);
-      if (!submit_warp(c, own, key_dev(key), key_blk(key), line, K_WB_KEEP, OP_WRITE, 0, key, who, sq_start)) {
-        if (own) want = false;
-        break;
+      if (eager) {
+        const u32 nwb = __popc(__ballot_sync(FULL, own));
+        if (lane == 0) atomicAdd(&c.stats[S_WRITEBACKS], (u64)nwb);
+        if (!submit_warp(c, own, key_dev(key), key_blk(key), line, K_WB_KEEP, OP_WRITE, 0, key, who, sq_start)) {
+          if (own) want = false;
+          break;
+        }
+      } else {
+        // no device write: the bytes are visible, hand them to attached readers, then MODIFIED
+        __threadfence();
+        u64 wlh = 0;
+        if (own) wlh = atom_exch_acqrel(&c.wl[line], ((u64)(ver & 0x1FFu) << 55) | WL_CLOSED);
+        deliver_waiters_warp(c, own ? (wlh & WL_PTR_MASK) : 0ull, line);
+        if (own) {
+          atom_add_release(&c.tags[line], (u64)(ST_MODIFIED - ST_BUSY) << ST_SHIFT);   // BUSY -> MODIFIED
+          log_state(c, who, line, ST_BUSY, ST_MODIFIED, key);
+          st_release(&node->done, 1u);
+        }
       }
     }
     if (own) {
-      if (!pushed) st_release(&node->done, 1u);   // cannot happen (the list was opened by us)
+      if (eager && !pushed) st_release(&node->done, 1u);   // cannot happen (the list was opened by us)
       want = false;
     }
+    if (once) break;
     if (__any_sync(FULL, want) && !sp.again(c, 2048, __LINE__ + 100000 * SPIN_FILE_ID)) break;
   }
+  return want;
+}
+
+__device__ __forceinline__ void async_write_warp(const DevCtx& c, bool active, u64 key, WaitNode* node,
+                                                 const uint4* src, u32 who, u32 sq_start) {
+  write_block_warp(c, active, key, node, src, who, sq_start, true);
 }
 
 // ======================================================================= K3: completion service
@@ -1021,6 +1110,66 @@ __device__ void async_write_warp(const DevCtx& c, bool active, u64 key, WaitNode
 #define AGILE_SVC_SLICE 4
 #endif
 constexpr int kSvcSlice = AGILE_SVC_SLICE;   // uint4 per lane per waiter-copy step (8 or 4)
+
+// Waiter delivery (_drain_waiters, software_cache.py:563-570), warp-collective: every lane with a
+// closed waiter list (cur = its first node, 0 = none) of `line` copies the line into each waiting
+// AgileBuf and releases its barrier; two lists are walked per step.
+__device__ void deliver_waiters_warp(const DevCtx& c, u64 cur, u32 line) {
+  const u32 lane = lane_id();
+  while (true) {
+    u32 cb = __ballot_sync(FULL, cur != 0);
+    if (!cb) break;
+    const int l0 = __ffs(cb) - 1;
+    cb &= cb - 1;
+    const int l1 = cb ? __ffs(cb) - 1 : -1;
+    const int s1 = l1 < 0 ? l0 : l1;
+    const uint4* src0 = reinterpret_cast<const uint4*>(line_ptr(c, __shfl_sync(FULL, line, l0)));
+    const uint4* src1 = reinterpret_cast<const uint4*>(line_ptr(c, __shfl_sync(FULL, line, s1)));
+    WaitNode* n0 = reinterpret_cast<WaitNode*>(__shfl_sync(FULL, cur, l0) << 4);
+    WaitNode* n1 = reinterpret_cast<WaitNode*>(__shfl_sync(FULL, cur, s1) << 4);
+    {
+      // a waiter list only ever links this run's WaitNodes: anything else is a corrupted list
+      const u64 a0 = (u64)(uintptr_t)n0, a1 = (u64)(uintptr_t)n1;
+      const bool bad = a0 < c.nodes_lo || a0 >= c.nodes_hi || a1 < c.nodes_lo || a1 >= c.nodes_hi;
+      if (bad) {
+        if (lane == 0) set_error(c, E_ILLEGAL_STATE, a0, 0xD0000000ull | (u64)__LINE__);
+        if ((int)lane == l0 || (int)lane == l1) cur = 0;
+        continue;
+      }
+    }
+    // dst == 0: a write's durability handle (async_write) — completion only, no copy
+    uint4* d0 = reinterpret_cast<uint4*>(n0->dst);
+    uint4* d1 = reinterpret_cast<uint4*>(n1->dst);
+    // both pages move in kSvcSlice-uint4 steps per lane (kSvcSlice = 8: one step, every load of
+    // both pages in flight at once; 4: half the registers, two steps)
+#pragma unroll
+    for (int h = 0; h < 8; h += kSvcSlice) {
+      uint4 v0[kSvcSlice], v1[kSvcSlice];
+#pragma unroll
+      for (int k = 0; k < kSvcSlice; ++k) v0[k] = __ldcg(src0 + lane + 32 * (h + k));
+      if (l1 >= 0) {
+#pragma unroll
+        for (int k = 0; k < kSvcSlice; ++k) v1[k] = __ldcg(src1 + lane + 32 * (h + k));
+      }
+      if (d0) {
+#pragma unroll
+        for (int k = 0; k < kSvcSlice; ++k) __stcg(d0 + lane + 32 * (h + k), v0[k]);
+      }
+      if (l1 >= 0 && d1) {
+#pragma unroll
+        for (int k = 0; k < kSvcSlice; ++k) __stcg(d1 + lane + 32 * (h + k), v1[k]);
+      }
+    }
+    __threadfence();   // every lane's page stores are performed before any barrier is released
+    __syncwarp();
+    // The owning lane reads its node's link BEFORE releasing the barrier: once DONE, the
+    // requester may reuse the node at once (its next async_read re-links it into another line's
+    // list), so a link read after the release could walk into a foreign list.
+    if ((int)lane == l0) { cur = n0->next; st_release(&n0->done, 1u); }
+    if ((int)lane == l1) { cur = n1->next; st_release(&n1->done, 1u); }
+  }
+}
+
 
 __device__ __forceinline__ void advance_head(const DevCtx& c, u32 q, u32 who) {
   SqWords* s = &c.sqw[q];
@@ -1077,7 +1226,7 @@ __device__ u32 cq_window_pass(const DevCtx& c, u32 cq, u64& off, u32& mask, u32 
       }
       const u32 os = atom_cas_acqrel(&c.sq_state[idx], SQ_ISSUED, SQ_EMPTY);
       atomicExch(&c.sq_done_v[idx], x.vidx + 1);
-      cache = x.line != NONE && (x.kind == K_FILL || x.kind == K_WB_KEEP);
+      cache = x.line != NONE && (x.kind == K_FILL || x.kind == K_WB_KEEP || x.kind == K_WB_EVICT);
       if (cache) {
         // close the waiter stack of this fill (its version is the BUSY word's)
         const u64 tw = ld_relaxed(&c.tags[x.line]);
@@ -1091,63 +1240,23 @@ __device__ u32 cq_window_pass(const DevCtx& c, u32 cq, u64& off, u32& mask, u32 
   __syncwarp();
   // drain waiters: copy the filled line into every waiting AgileBuf and clear its barrier while
   // the line is still BUSY (not evictable), then flip it READY (software_cache.py:538-541,563-570)
-  u64 cur = (valid && cache) ? (wlh & ((1ull << 54) - 1)) : 0ull;   // per-lane waiter cursor
-  while (true) {
-    u32 cb = __ballot_sync(FULL, cur != 0);
-    if (!cb) break;
-    const int l0 = __ffs(cb) - 1;
-    cb &= cb - 1;
-    const int l1 = cb ? __ffs(cb) - 1 : -1;
-    const int s1 = l1 < 0 ? l0 : l1;
-    const uint4* src0 = reinterpret_cast<const uint4*>(line_ptr(c, __shfl_sync(FULL, x.line, l0)));
-    const uint4* src1 = reinterpret_cast<const uint4*>(line_ptr(c, __shfl_sync(FULL, x.line, s1)));
-    WaitNode* n0 = reinterpret_cast<WaitNode*>(__shfl_sync(FULL, cur, l0) << 4);
-    WaitNode* n1 = reinterpret_cast<WaitNode*>(__shfl_sync(FULL, cur, s1) << 4);
-    {
-      // a waiter list only ever links this run's WaitNodes: anything else is a corrupted list
-      const u64 a0 = (u64)(uintptr_t)n0, a1 = (u64)(uintptr_t)n1;
-      const bool bad = a0 < c.nodes_lo || a0 >= c.nodes_hi || a1 < c.nodes_lo || a1 >= c.nodes_hi;
-      if (bad) {
-        if (lane == 0) set_error(c, E_ILLEGAL_STATE, a0, 0xD0000000ull | (u64)__LINE__);
-        if ((int)lane == l0 || (int)lane == l1) cur = 0;
-        continue;
-      }
-    }
-    // dst == 0: a write's durability handle (async_write) — completion only, no copy
-    uint4* d0 = reinterpret_cast<uint4*>(n0->dst);
-    uint4* d1 = reinterpret_cast<uint4*>(n1->dst);
-    // both pages move in kSvcSlice-uint4 steps per lane (kSvcSlice = 8: one step, every load of
-    // both pages in flight at once; 4: half the registers, two steps)
-#pragma unroll
-    for (int h = 0; h < 8; h += kSvcSlice) {
-      uint4 v0[kSvcSlice], v1[kSvcSlice];
-#pragma unroll
-      for (int k = 0; k < kSvcSlice; ++k) v0[k] = __ldcg(src0 + lane + 32 * (h + k));
-      if (l1 >= 0) {
-#pragma unroll
-        for (int k = 0; k < kSvcSlice; ++k) v1[k] = __ldcg(src1 + lane + 32 * (h + k));
-      }
-      if (d0) {
-#pragma unroll
-        for (int k = 0; k < kSvcSlice; ++k) __stcg(d0 + lane + 32 * (h + k), v0[k]);
-      }
-      if (l1 >= 0 && d1) {
-#pragma unroll
-        for (int k = 0; k < kSvcSlice; ++k) __stcg(d1 + lane + 32 * (h + k), v1[k]);
-      }
-    }
-    __threadfence();   // every lane's page stores are performed before any barrier is released
-    __syncwarp();
-    // The owning lane reads its node's link BEFORE releasing the barrier: once DONE, the
-    // requester may reuse the node at once (its next async_read re-links it into another line's
-    // list), so a link read after the release could walk into a foreign list.
-    if ((int)lane == l0) { cur = n0->next; st_release(&n0->done, 1u); }
-    if ((int)lane == l1) { cur = n1->next; st_release(&n1->done, 1u); }
-  }
-  if (valid && cache) {
+  deliver_waiters_warp(c, (valid && cache) ? (wlh & WL_PTR_MASK) : 0ull, x.line);
+  if (valid && cache && x.kind != K_WB_EVICT) {
     const u64 ot = atom_add_release(&c.tags[x.line], 1ull << ST_SHIFT);   // BUSY -> READY
     if (tw_state(ot) != ST_BUSY) set_error(c, E_ILLEGAL_STATE, x.line, ot);
     log_state(c, who, x.line, ST_BUSY, ST_READY, x.key);
+  } else if (valid && cache) {
+    // eviction write-back durable (complete_io WB_EVICT, software_cache.py:538-553): the old key's
+    // bytes are on the device; the line turns INVALID (version + 1, pins kept) for the claimant's retry
+    u64 ot = ld_relaxed(&c.tags[x.line]);
+    while (true) {
+      if (tw_state(ot) != ST_BUSY) { set_error(c, E_ILLEGAL_STATE, x.line, ot); break; }
+      const u64 nt = (ot & PIN_MASK) | tw_make(ST_INVALID, 0, tw_ver(ot) + 1, false, 0);
+      const u64 pv = atom_cas_acqrel(&c.tags[x.line], ot, nt);
+      if (pv == ot) break;
+      ot = pv;
+    }
+    log_state(c, who, x.line, ST_BUSY, ST_INVALID, x.key);
   }
   if (valid) {
     lat_acc += gtimer() - x.t_submit;

@@ -7,6 +7,7 @@
 #pragma once
 #include <climits>
 #include "agile_core.cuh"
+#include "agile_share.cuh"
 #undef SPIN_FILE_ID
 #define SPIN_FILE_ID 2
 
@@ -95,10 +96,10 @@ struct SeqWork {
 
 // ------------------------------------------------------------------ EvictWork
 // SoftwareCache.evict (software_cache.py:268-281 -> _evict_locked, 335-353) per block, serially
-// by one warp: a resident READY line with no pins is reset (INVALID, version + 1, evict_reset);
-// a BUSY or pinned line is DEFERRED; a MODIFIED line would need a write-back first and is
-// reported DEFERRED as well (the write path writes through, so none exists without the share
-// table).  outcome: 0 RESET, 1 DEFERRED, 2 not resident.
+// by one warp: a resident READY line with no pins is reset (INVALID, version + 1, evict_reset); a
+// MODIFIED line with no pins starts its write-back (BUSY with the old key until durable, then
+// INVALID: WB_EVICT); a BUSY or pinned line is DEFERRED.  outcome: 0 RESET, 1 DEFERRED, 2 not
+// resident (the reference returns RESET for an absent or INVALID line), 3 WRITEBACK_STARTED.
 struct EvictWork {
   const u32* dev;
   const u64* blk;
@@ -114,6 +115,7 @@ struct EvictWork {
       u64 word = 0;
       probe_lanes(c, lane == 0, key, line, word);
       int oc = 2;
+      bool wb = false;
       if (lane == 0 && line != NONE) {
         const u32 set = line / c.ways;
         oc = 1;
@@ -129,10 +131,23 @@ struct EvictWork {
               log_state(c, who, line, ST_READY, ST_INVALID, key);
               atomicAdd(&c.stats[S_RESETS], 1ull);
             }
+          } else if (tw_state(w) == ST_MODIFIED && tw_pins(w) == 0) {
+            const u32 ver = tw_ver(w) + 1;
+            st_relaxed(&c.wl[line], ((u64)(ver & 0x1FFu)) << 55);
+            if (atom_cas_acqrel(&c.tags[line], w, tw_make(ST_BUSY, key, ver, false, 0)) == w) {
+              oc = 3;
+              wb = true;
+              log_ev(c, who, M_CACHE, A_EVICT_WB, line, key_dev(key), key_blk(key));
+              log_state(c, who, line, ST_MODIFIED, ST_BUSY, key);
+              atomicAdd(&c.stats[S_WRITEBACKS], 1ull);
+            }
           }
           st_release(&c.set_lock[set], 0u);
         }
       }
+      line = __shfl_sync(FULL, line, 0);
+      if (__any_sync(FULL, wb) && !submit_warp(c, wb, key_dev(key), key_blk(key), line, K_WB_EVICT, OP_WRITE, 0, key, who, 0))
+        return;
       if (lane == 0) outcome[i] = (signed char)oc;
       __syncwarp();
     }
@@ -285,6 +300,97 @@ struct LoopWork {
     for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
     if (lane_id() == 0 && s) atomicAdd(&counters[0], (u64)s);
     if (uidx == 0 && threadIdx.x == 0) { counters[1] = ws; counters[2] = we; }
+  }
+};
+
+// ------------------------------------------------------------------ CoherenceWork
+// The reference's coherence replay workload (tests/test_coherence.py:27-60): `tasks` tasks, one
+// warp each (lane 0 carries the task, lockstep verbs), run their plans of (read | write, block,
+// think time); writes carry a unique 8-byte prefix; every read observes the first 8 bytes of the
+// buffer it got (its own, or the shared one the table returned) and logs ("test", "observe") at
+// that instant — under the block's share-table home lock when the table is on, the instant a
+// writer into that shared buffer also commits under.  With the table, every read keeps its
+// reference to the end, then releases (the last release of a Modified buffer installs it into
+// the cache).  Finally warp 0 flushes every MODIFIED line to the device (the reference's flusher).
+struct CoherenceWork {
+  const unsigned char* op;   // [tasks][ops] 0 read, 1 write, 2 read whose think time falls between its
+                             // completion and its observe (test_coherence.py:112-135 hazard reader)
+  const u32* blk;            // [tasks][ops]
+  const u32* think;          // [tasks][ops] ns
+  u32 tasks, ops;
+  uint4* wbuf;               // [tasks][256] write payload page
+  uint4* rbuf;               // [tasks][ops][256] read buffers (one AgileBuf per read)
+  uint4* snap;               // [tasks][256] release snapshot pages
+  WaitNode* nodes;           // [tasks][ops] op nodes, [tasks] install nodes, [32] flush nodes
+  u64* seen;                 // [tasks][ops] observed prefixes
+  u64* flushed;              // [1]
+  __device__ void run(const DevCtx& c, u32 uidx, u32 nusers) const {
+    if (uidx != 0) return;
+    const u32 w = threadIdx.x >> 5, lane = lane_id();
+    const bool act = lane == 0 && w < tasks;
+    const u32 who = WHO_USER | w;   // task "u<w>" (system.py spawn_user naming)
+    const u32 sq = w;
+    WaitNode* inst = nodes + (u64)tasks * ops + (w < tasks ? w : 0);
+    uint4* sp = snap + (u64)(w < tasks ? w : 0) * 256;
+    if (w < tasks) {
+      for (u32 i = 0; i < ops; ++i) {
+        if (aborted(c)) break;
+        const u64 t = (u64)w * ops + i;
+        if (op[t] != 2) compute_spin(think[t]);   // op 2: read, think, then observe (the hazard reader)
+        const u64 key = make_key(0, blk[t]);
+        WaitNode* nd = nodes + t;
+        if (op[t] == 1) {
+          // payload: prefix (1 << 30 | task << 16 | op) + zeros (test_coherence.py:20-24)
+          uint4* pb = wbuf + (u64)w * 256;
+          for (u32 k = lane; k < 256; k += 32) pb[k] = make_uint4(0u, 0u, 0u, 0u);
+          __syncwarp();
+          if (lane == 0) *reinterpret_cast<u64*>(pb) = (1ull << 30) | ((u64)w << 16) | i;
+          __syncwarp();
+          async_write_t(c, act, key, nd, pb, who, sq, sp, inst);
+          wait_nodes_warp(c, act, nd);
+        } else {
+          WaitNode* eff = nd;
+          async_read_t(c, act, key, nd, rbuf + t * 256, who, sq, eff);
+          wait_nodes_warp(c, act, eff);
+          if (op[t] == 2) compute_spin(think[t]);
+          if (act) {
+            const bool tab = c.st_buckets != 0;
+            const u32 h = tab ? st_home(c, key) : 0u;
+            if (!tab || st_lock(c, h)) {
+              const u64 v = __ldcg(reinterpret_cast<const unsigned long long*>(eff->dst));
+              log_ev(c, who, M_TEST, A_OBSERVE, 0, blk[t], v);
+              seen[t] = v;
+              if (tab) st_unlock(c, h);
+            }
+          }
+          __syncwarp();
+        }
+      }
+      if (c.st_buckets) {
+        for (u32 i = 0; i < ops; ++i) {
+          const u64 t = (u64)w * ops + i;
+          release_shared_warp(c, act && op[t] != 1, make_key(0, blk[t]), sp, inst, who, sq);
+        }
+      }
+    }
+    __syncthreads();
+    if (w == 0) {
+      const u64 n = flush_warp(c, nodes + (u64)tasks * ops + tasks, who, sq);
+      if (lane == 0) flushed[0] = n;
+    }
+  }
+};
+
+// ------------------------------------------------------------------ FlushWork
+// SoftwareCache.flush (software_cache.py:283-298) as an API call: one warp writes every MODIFIED
+// line back and waits for durability.
+struct FlushWork {
+  WaitNode* nodes;   // [32]
+  u64* flushed;
+  __device__ void run(const DevCtx& c, u32 uidx, u32 nusers) const {
+    if (uidx != 0 || threadIdx.x >= 32) return;
+    const u64 n = flush_warp(c, nodes, user_who(0), 0);
+    if (lane_id() == 0) flushed[0] = n;
   }
 };
 

@@ -316,6 +316,32 @@ class AgileSystem:
                                                  out.ctypes.data), "evict_blocks")
         return out
 
+    def flush(self) -> int:
+        """SoftwareCache.flush (software_cache.py:283-298): write back every MODIFIED line."""
+        n = C.c_uint64(0)
+        self._check(self._lib.agile_flush(self._ctx, C.byref(n)), "flush")
+        return int(n.value)
+
+    def share_live(self) -> int:
+        """ShareTable.live_entries (share_table.py:198-199); 0 when the table is disabled."""
+        n = C.c_uint64(0)
+        self._check(self._lib.agile_share_live(self._ctx, C.byref(n)), "share_live")
+        return int(n.value)
+
+    def run_coherence(self, op, blk, think):
+        """The reference's coherence workload (tests/test_coherence.py:27-60) on the device:
+        op/blk/think are [tasks][ops] arrays (op 0 read, 1 write).  Returns (seen [tasks][ops]
+        observed prefixes, lines flushed at the end)."""
+        op = np.ascontiguousarray(op, dtype=np.uint8)
+        tasks, ops = op.shape
+        blk = np.ascontiguousarray(blk, dtype=np.uint32).reshape(tasks, ops)
+        think = np.ascontiguousarray(think, dtype=np.uint32).reshape(tasks, ops)
+        seen = np.zeros((tasks, ops), dtype=np.uint64)
+        fl = C.c_uint64(0)
+        self._check(self._lib.agile_run_coherence(self._ctx, op.ctypes.data, blk.ctypes.data, think.ctypes.data,
+                                                  tasks, ops, seen.ctypes.data, C.byref(fl)), "run_coherence")
+        return seen, int(fl.value)
+
     def set_launch_mode(self, mode: str) -> None:
         """'split' | 'fused' | 'solo' (split launch whose user grid may run alone: profiling of
         all-hit replays under a kernel-serialising tool)."""

@@ -11,18 +11,23 @@ from __future__ import annotations
 
 import numpy as np
 
-MODULES = ("nvme", "ssd", "svc", "cache", "api")
+MODULES = ("nvme", "ssd", "svc", "cache", "api", "table", "test")
 ACTIONS = ("enqueue", "sqe_updated", "sqe_issued", "doorbell", "sqe_release", "head",
            "fetch", "complete", "cqe_post", "cqe_stall",
            "window_ring", "drain_ring", "stop", "start", "cqe_process",
-           "state", "miss", "hit", "attach", "evict_reset", "drain", "async_read", "prefetch", "install")
+           "state", "miss", "hit", "attach", "evict_reset", "drain", "async_read", "prefetch", "install",
+           "write_commit", "observe", "register", "share", "release", "modified", "propagate", "duty_transfer",
+           "evict_wb", "write_intent")
 STATES = ("INVALID", "BUSY", "READY", "MODIFIED")
 OPS = ("READ", "WRITE")
 ARITY = {"enqueue": 6, "sqe_updated": 2, "sqe_issued": 3, "doorbell": 4, "sqe_release": 3,
          "head": 2, "fetch": 4, "complete": 5, "cqe_post": 4, "cqe_stall": 3,
          "window_ring": 3, "drain_ring": 3, "stop": 0, "start": 1, "cqe_process": 4,
          "state": 5, "miss": 2, "hit": 2, "attach": 2, "evict_reset": 3, "drain": 2,
-         "async_read": 2, "prefetch": 2, "install": 3}
+         "async_read": 2, "prefetch": 2, "install": 3,
+         "write_commit": 3, "observe": 3, "register": 2, "share": 4, "release": 3, "modified": 2, "propagate": 2,
+         "duty_transfer": 3, "evict_wb": 3, "write_intent": 2}
+SHARE_STATES = ("Exclusive", "Shared", "Modified")
 
 RECORD = np.dtype([("t", "<u8"), ("who", "<u4"), ("modact", "<u4"), ("a", "<u8", (6,))])
 
@@ -80,5 +85,7 @@ def render_event_log(raw: bytes | np.ndarray, recorder: TraceRecorder | None = N
         elif act == "state":
             det[1] = STATES[det[1]]
             det[2] = STATES[det[2]]
+        elif act == "share":
+            det[3] = SHARE_STATES[det[3]]
         rec.emit(int(r["t"]) - t0, _who(int(r["who"])), mod, act, tuple(det))
     return rec
