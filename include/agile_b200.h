@@ -63,9 +63,10 @@ const char* agile_last_error(agile_ctx* ctx);
 int agile_geometry(agile_ctx* ctx, uint64_t* out, int n);
 
 /* Launch mode of later runs: 0 split (infra grid + PDL user grid), 1 fused (one grid, roles by
- * arrival ticket), 2 split with solo users (profiling: when a kernel-serialising tool keeps the
- * user grid from starting beside the infra grid, the infra grid leaves after 100 ms and the user
- * grid runs alone — an all-hit replay needs neither engine nor service). */
+ * arrival ticket), 2 split with solo users (when a kernel-serialising tool keeps the user grid
+ * from starting beside the infra grid, the infra grid leaves after 100 ms and the user grid runs
+ * alone), 3 users only (profiling: no infra grid; an all-hit replay needs neither engine nor
+ * service, a miss ends in the watchdog). */
 int agile_set_launch_mode(agile_ctx* ctx, int mode);
 
 /* Third-party user kernels (include/agile_device.cuh, the paper's Listing 1 API): begin one split

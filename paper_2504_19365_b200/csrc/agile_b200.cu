@@ -52,6 +52,8 @@ struct agile_ctx {
   bool fused = false;
   // engine.copy: false = register-staged page moves, true = TMA bulk copies through shared memory
   bool bulk_engine = false;
+  // launch mode 3 (profiling): the user grid runs without an infra grid
+  bool users_only = false;
   // infra grid of bounded side-stream runs (engine.side_warps / service.side_warps; 0 = full)
   uint32_t side_engine_warps = 0, side_service_warps = 0;
   // async_read WaitNodes (AgileBuf barriers) for the reads / loop / seq workloads
@@ -271,6 +273,14 @@ int launch_infra(agile_ctx* ctx, uint32_t n_user_ctas, cudaStream_t st, bool sid
   L.n_user_ctas = n_user_ctas;
   L.pad = 0;
   if (ctx->fused) return 0;
+  if (ctx->users_only) {
+    // profiling replays of all-hit batches: no infra grid at all; the user grid finds the
+    // "infra gave up" mark and runs alone (a miss would end in the watchdog)
+    static const u32 gave_up = kInfraGaveUp;
+    CK(cudaMemcpyAsync(&ctx->d.run->users_started, &gave_up, 4, cudaMemcpyHostToDevice, st));
+    dc.n_engine_ctas = dc.n_service_ctas = 0;
+    return 0;
+  }
   infra_fn(ctx)<<<dc.n_engine_ctas + dc.n_service_ctas, kCtaThreads, infra_smem(ctx), st>>>(dc, L);
   CK(cudaGetLastError());
   return 0;
@@ -943,9 +953,11 @@ int agile_user_run_begin(agile_ctx* ctx, void* stream, uint32_t n_user_ctas, uin
 int agile_user_run_end(agile_ctx* ctx, void* stream) { return agile_sync(ctx, stream); }
 
 int agile_set_launch_mode(agile_ctx* ctx, int mode) {
-  if (!ctx || mode < 0 || mode > 2) return fail(ctx, AGILE_E_ARG, "launch mode must be 0 (split), 1 (fused) or 2 (split, solo users)");
+  if (!ctx || mode < 0 || mode > 3)
+    return fail(ctx, AGILE_E_ARG, "launch mode must be 0 (split), 1 (fused), 2 (split, solo users) or 3 (users only)");
   ctx->fused = mode == 1;
-  ctx->d.solo_ok = mode == 2 ? 1u : 0u;
+  ctx->users_only = mode == 3;
+  ctx->d.solo_ok = mode >= 2 ? 1u : 0u;
   ctx->d.user_start_ns = mode == 2 ? 100ull * 1000 * 1000 : ctx->d.watchdog_ns;
   return 0;
 }

@@ -343,9 +343,9 @@ class AgileSystem:
         return seen, int(fl.value)
 
     def set_launch_mode(self, mode: str) -> None:
-        """'split' | 'fused' | 'solo' (split launch whose user grid may run alone: profiling of
-        all-hit replays under a kernel-serialising tool)."""
-        code = {"split": 0, "fused": 1, "solo": 2}[mode]
+        """'split' | 'fused' | 'solo' (split launch whose user grid may run alone) | 'users' (no
+        infra grid: profiling of all-hit replays under a kernel-serialising tool)."""
+        code = {"split": 0, "fused": 1, "solo": 2, "users": 3}[mode]
         self._check(self._lib.agile_set_launch_mode(self._ctx, code), "set_launch_mode")
         self.launch_mode = "fused" if mode == "fused" else "split"
 

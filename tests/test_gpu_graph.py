@@ -127,3 +127,39 @@ def test_pagerank_matches_oracle(gpu_system):
     # sums may differ in their last bits between summation orders)
     f32 = pagerank_f32(rowT.cpu().numpy(), colT.cpu().numpy(), outdeg.cpu().numpy(), 10)
     assert np.max(np.abs(r.cpu().numpy() - f32) / f32) < 2.5e-7
+
+
+def test_rmat22_bfs_spmv_pagerank_match_c_oracle(gpu_system):
+    """RMAT scale 22 (4.2 M vertices, 67 M edges), cache = 25 % of the paged arrays, async mode,
+    against the C oracle (oracle/graph_oracle.c): BFS levels bit-exact, SpMV and PageRank within
+    1e-5 relative."""
+    from oracle import cgraph
+    dev, row_ptr, col, _ = _graph(22, seed=4)
+    V, E = row_ptr.numel() - 1, col.numel()
+    npg = pages_for(E)
+    s = gpu_system(cache_lines=max(64, (2 * npg // 4) // 32 * 32), ways=32, blocks=2 * npg + 8, pairs=64,
+                   sq_depth=256, cq_depth=256, engine_warps=64, warps=16)
+    nxt = write_paged(s, 0, 0, col)
+    vals = edge_values(E, 4, dev)
+    write_paged(s, 0, nxt, vals)
+    rp = row_ptr.cpu().numpy()
+    col_h = col.cpu().numpy()
+    src = pick_source(row_ptr, 0)
+    level, _ = run_bfs(s, row_ptr, V, src, 0, 2)
+    assert np.array_equal(level.cpu().numpy(), cgraph.bfs_levels(rp, col_h, src))
+    x = torch.rand(V, device=dev)
+    s.reset()
+    y, _ = run_spmv(s, row_ptr, V, E, 0, nxt, x, 1, 2)
+    vh, xh = vals.cpu().numpy(), x.cpu().numpy()
+    exp = cgraph.spmv_f32(rp, col_h, vh, xh).astype(np.float64)
+    mag = cgraph.spmv_f32(rp, col_h, np.abs(vh), np.abs(xh)).astype(np.float64)
+    assert np.all(np.abs(y.cpu().numpy() - exp) <= 1e-5 * np.abs(exp) + 1e-12 * mag)
+    # PageRank on the transpose (in-edge CSR) of a second graph
+    _, rowT, colT, outdeg = _graph(22, seed=5, transpose=True)
+    ET = colT.numel()
+    s2 = gpu_system(cache_lines=max(64, (pages_for(ET) // 4) // 32 * 32), ways=32, blocks=pages_for(ET) + 8, pairs=64,
+                    sq_depth=256, cq_depth=256, engine_warps=64, warps=16)
+    write_paged(s2, 0, 0, colT)
+    r, _ = run_pagerank(s2, rowT, V, ET, 0, outdeg, 10, prefetch_distance=2)
+    pexp = cgraph.pagerank_f32(rowT.cpu().numpy(), colT.cpu().numpy(), outdeg.cpu().numpy(), 10).astype(np.float64)
+    assert np.max(np.abs(r.cpu().numpy() - pexp) / pexp) < 1e-5

@@ -73,6 +73,15 @@ def bfs(scale, frac):
     line = {"workload": "bfs", "scale": scale, "vertices": V, "edges": E, "cache_frac": frac,
             "cache_lines": s.num_lines, "gen_s": gen_s, "sync": out[0], "async": out[2],
             "async_vs_sync": out[0]["ms"] / out[2]["ms"]}
+    if os.environ.get("GRAPH_CHECK", "1") == "1":
+        # the C oracle (oracle/graph_oracle.c) over the same CSR: col_idx straight from the pinned
+        # page store the GPU read it from, row_ptr copied back
+        from oracle import cgraph
+        t1 = time.time()
+        col_h = s.store_view(0)[:E * 4].view("<i4")
+        exp = cgraph.bfs_levels(row_ptr.cpu().numpy(), col_h, pick_source(row_ptr, 0))
+        line["oracle"] = {"levels_equal_oracle": bool((ref.cpu().numpy() == exp).all()), "kind": "oracle/graph_oracle.c",
+                          "seconds": time.time() - t1}
     print(json.dumps(line), flush=True)
     s.close()
 
@@ -93,6 +102,7 @@ def spmv(scale, frac, iters):
     x = torch.rand(V, device=dev)
     res = {}
     ys = {}
+    rs = {}
     for pd in (0, 2):
         s.reset()
         f0 = s.stats()["fills"]
@@ -101,7 +111,7 @@ def spmv(scale, frac, iters):
         ys[pd] = y
         s.reset()
         f0 = s.stats()["fills"]
-        _, pr = run_pagerank(s, rowT, V, E, 0, outdeg, iters, prefetch_distance=pd)
+        rs[pd], pr = run_pagerank(s, rowT, V, E, 0, outdeg, iters, prefetch_distance=pd)
         pr["page_misses"] = s.stats()["fills"] - f0
         res[pd] = {"spmv_ms": st["ms"], "spmv_gflops": st["gflops"], "spmv_page_fills": st["page_misses"],
                    "spmv_link_gbs": st["page_misses"] * 4096 / st["ms"] / 1e6,
@@ -114,6 +124,28 @@ def spmv(scale, frac, iters):
             "spmv_equal_sync": bool(torch.equal(ys[0], ys[2])),
             "spmv_async_vs_sync": res[0]["spmv_ms"] / res[2]["spmv_ms"],
             "pagerank_async_vs_sync": res[0]["pagerank_ms"] / res[2]["pagerank_ms"]}
+    if os.environ.get("GRAPH_CHECK", "1") == "1":
+        # the C oracle over the same CSR (col / val straight from the pinned page store): y within
+        # 1e-5 relative (north_star; guarded by sum |a x| for cancelling rows), PageRank within 1e-5
+        import numpy as np
+        from oracle import cgraph
+        t1 = time.time()
+        view = s.store_view(0)
+        colT_h = view[:E * 4].view("<i4")
+        vals_h = view[nxt * 4096:nxt * 4096 + E * 4].view("<f4")
+        rp = rowT.cpu().numpy()
+        xh = x.cpu().numpy()
+        exp = cgraph.spmv_f32(rp, colT_h, vals_h, xh).astype(np.float64)
+        mag = cgraph.spmv_f32(rp, colT_h, np.abs(vals_h), np.abs(xh)).astype(np.float64)
+        got = ys[0].cpu().numpy().astype(np.float64)
+        err = np.abs(got - exp) / np.maximum(np.abs(exp), 1e-30)
+        ok = np.abs(got - exp) <= 1e-5 * np.abs(exp) + 1e-12 * mag
+        pr_exp = cgraph.pagerank_f32(rp, colT_h, outdeg.cpu().numpy(), iters).astype(np.float64)
+        pr_err = np.abs(rs[0].cpu().numpy().astype(np.float64) - pr_exp) / pr_exp
+        line["oracle"] = {"kind": "oracle/graph_oracle.c", "spmv_within_1e-5": bool(ok.all()),
+                          "spmv_median_rel_err": float(np.median(err)),
+                          "pagerank_max_rel_err": float(pr_err.max()), "pagerank_within_1e-5": bool(pr_err.max() < 1e-5),
+                          "seconds": time.time() - t1}
     print(json.dumps(line), flush=True)
     s.close()
 

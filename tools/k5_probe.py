@@ -9,8 +9,8 @@ Prints one JSON line: ms per launch, algorithmic GB/s and fraction of the measur
 Profile: K5_SOLO=1 ncu -k regex:agile_user_kernel -c 1 python tools/k5_probe.py uniform 1: the
 warm-up runs take the launch mode the co-residency probe picks (fused under ncu: they need the
 engine for their misses), then the timed all-hit replays switch to split-solo (the infra grid
-leaves after 100 ms when the user grid cannot start beside it; all hits need no engine), so the
-capture is the production user kernel with its own register budget.
+is not launched at all: launch mode "users"; all hits need no engine), so the capture is the
+production user kernel with its own register budget and grid.
 """
 import json
 import os
@@ -67,7 +67,7 @@ def main():
         s.embbag_sharded(idx, tabs, out, cnt, D, stream=st.cuda_stream)
     s.sync(st.cuda_stream)
     if os.environ.get("K5_SOLO") == "1":
-        s.set_launch_mode("solo")
+        s.set_launch_mode("users")
     cnt.zero_()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record(st)
