@@ -68,6 +68,9 @@ int agile_geometry(agile_ctx* ctx, uint64_t* out, int n);
  * alone), 3 users only (profiling: no infra grid; an all-hit replay needs neither engine nor
  * service, a miss ends in the watchdog). */
 int agile_set_launch_mode(agile_ctx* ctx, int mode);
+/* engine.copy of later runs: 0 registers (register-staged page moves, whole infra SMs), 1 bulk
+ * (TMA bulk copies through shared-memory slots; user CTAs fit beside the infra CTAs) */
+int agile_set_engine_copy(agile_ctx* ctx, int bulk);
 
 /* Third-party user kernels (include/agile_device.cuh, the paper's Listing 1 API): begin one split
  * run on `stream` — run words reset, infra grid launched — and receive the DevCtx / Launch values

@@ -54,6 +54,7 @@ void oracle_spmv(const int64_t* row_ptr, const int32_t* col, const float* val, c
 void oracle_pagerank(const int64_t* rowT, const int32_t* colT, const int64_t* outdeg, int64_t V, int iters, double d,
                      float* r) {
   float* x = (float*)malloc((size_t)V * sizeof(float));
+  if (!x) return;
   for (int64_t v = 0; v < V; ++v) r[v] = (float)(1.0 / (double)V);
   const float alpha = (float)d, base = (float)((1.0 - d) / (double)V);
   for (int it = 0; it < iters; ++it) {

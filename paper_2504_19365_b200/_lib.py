@@ -45,6 +45,7 @@ SIGNATURES = {
     "agile_evict_blocks": (_int, [_vp, _vp, _vp, _i64, _vp]),
     "agile_array_get": (_int, [_vp, _vp, _vp, _i64, _u32, _vp]),
     "agile_set_launch_mode": (_int, [_vp, _int]),
+    "agile_set_engine_copy": (_int, [_vp, _int]),
     "agile_user_run_begin": (_int, [_vp, _vp, _u32, _u64, _vp, _u64, _vp, _u64, C.POINTER(_vp)]),
     "agile_user_run_end": (_int, [_vp, _vp]),
     "agile_flush": (_int, [_vp, C.POINTER(_u64)]),

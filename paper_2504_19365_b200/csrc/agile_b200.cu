@@ -952,6 +952,12 @@ int agile_user_run_begin(agile_ctx* ctx, void* stream, uint32_t n_user_ctas, uin
 
 int agile_user_run_end(agile_ctx* ctx, void* stream) { return agile_sync(ctx, stream); }
 
+int agile_set_engine_copy(agile_ctx* ctx, int bulk) {
+  if (!ctx) return AGILE_E_ARG;
+  ctx->bulk_engine = bulk != 0;
+  return 0;
+}
+
 int agile_set_launch_mode(agile_ctx* ctx, int mode) {
   if (!ctx || mode < 0 || mode > 3)
     return fail(ctx, AGILE_E_ARG, "launch mode must be 0 (split), 1 (fused), 2 (split, solo users) or 3 (users only)");

@@ -726,10 +726,7 @@ struct EmbBagWork {
 #endif
 
   static constexpr int kMinCtas = AGILE_EMB_MIN_CTAS;
-#ifndef AGILE_K5_DEFER
-#define AGILE_K5_DEFER 1   // defer each bag's last seqlock re-read past the next bag's pooling
-#endif
-  static constexpr bool kDefer = AGILE_K5_DEFER != 0;
+
 
   __device__ void run(const DevCtx& c, u32 uidx, u32 nusers) const {
     const u32 gw = uidx * kCtaWarps + (threadIdx.x >> 5);
@@ -737,8 +734,6 @@ struct EmbBagWork {
     if (prefetch_only) { run_prefetch(c, gw, who); return; }
     const u32 nbags = B * T;
     u32 misses = 0, lookups = 0;
-    Deferred pend;
-    pend.bag = NONE;
     u32 cur = grab_block(c);
     if (pd && cur < nbags) prefetch_block(c, cur, nbags, who, gw);
     u32 pass = 0;
@@ -752,38 +747,15 @@ struct EmbBagWork {
         for (u64 o = (u64)lane_id() * 16; o < n8; o += 32 * 16)
           asm volatile("prefetch.global.L2::evict_last [%0];" :: "l"(idx + i0 + o));
       }
-      for (u32 k = 0; k < kGrab && cur + k < nbags; ++k) {
-        // the previous bag's seqlock re-read is issued now and checked after this bag pooled:
-        // its round trip hides under this bag's probe and row loads
-        const bool chk = pend.bag != NONE;
-        const u64 rv = chk && pend.addr ? ld_relaxed(pend.addr) : 0ull;
-        Deferred nd;
-        if (!pool_bag(c, cur + k, who, gw, misses, lookups, kDefer ? &nd : nullptr)) { cur = nbags; pend.bag = NONE; break; }
-        if (!kDefer) nd.bag = NONE;
-        const bool bad = chk && pend.addr && ((rv ^ pend.word) & IDENT_MASK) != 0;
-        if (__any_sync(FULL, bad) && !repool(c, pend.bag, who, gw)) { cur = nbags; pend.bag = NONE; break; }
-        pend = nd;
-      }
+      for (u32 k = 0; k < kGrab && cur + k < nbags; ++k)
+        if (!pool_bag(c, cur + k, who, gw, misses, lookups)) { cur = nbags; break; }
       if (aborted(c)) break;
       cur = nxt;
-    }
-    if (pend.bag != NONE && !aborted(c)) {
-      const bool bad = pend.addr && ((ld_relaxed(pend.addr) ^ pend.word) & IDENT_MASK) != 0;
-      if (__any_sync(FULL, bad)) repool(c, pend.bag, who, gw);
     }
     if (lane_id() == 0) {
       atomicAdd(&lookups_miss[0], (u64)lookups);
       atomicAdd(&lookups_miss[1], (u64)misses);
     }
-  }
-
-  // A bag's last-chunk validation, deferred (pool_bag with `defer`): the tag word address (its
-  // offset carries the data dependency on the chunk's row values) and the word it must still equal
-  struct Deferred { const u64* addr; u64 word; u32 bag; };
-  // a bag whose deferred validation failed is pooled again, validating in place (not counted again)
-  __device__ __noinline__ bool repool(const DevCtx& c, u32 bag, u32 who, u32 gw) const {
-    u32 m = 0, l = 0;
-    return pool_bag(c, bag, who, gw, m, l, nullptr);
   }
 
   // batch-level async (AGILE prefetch, gpu_api.py:139-162): submit every missing page of the
@@ -885,11 +857,7 @@ struct EmbBagWork {
   // pool one bag (fp64, 4 dims per lane) and store it; false when the run aborts.  A chunk whose
   // validation fails restarts the bag (rare: a page was evicted while the warp read it); after 4
   // failures the bag is pooled row by row, each row validated on its own.
-  // defer != null: the LAST chunk's seqlock validation is not performed here but described in
-  // *defer for the caller to check after its next bag (the output is stored before validation; a
-  // failed check re-pools the bag and overwrites it)
-  __device__ bool pool_bag(const DevCtx& c, u32 bag, u32 who, u32 gw, u32& misses, u32& lookups,
-                           Deferred* defer) const {
+  __device__ bool pool_bag(const DevCtx& c, u32 bag, u32 who, u32 gw, u32& misses, u32& lookups) const {
     const u32 lane = lane_id();
     const u32 b = bag / T, t = bag - b * T;
     const TabDesc td = tab(t);
@@ -900,7 +868,6 @@ struct EmbBagWork {
     u32 fails = 0;
     u32 counted = 0;   // chunks below this position were counted (a restart does not count twice)
     Spin rsp;
-    if (defer) { defer->addr = nullptr; defer->word = 0; defer->bag = bag; }
   restart:
     a0 = a1 = a2 = a3 = 0.0;
     for (u32 c0 = 0; c0 < n; c0 += 32) {
@@ -956,12 +923,6 @@ struct EmbBagWork {
       // seqlock validation, once per chunk: the tag re-read's address depends on every row value
       // of the warp (redux over the lanes), so it is issued after all of them were loaded
       const u64 z = dep_zero(__reduce_or_sync(FULL, dep));
-      if (defer && c0 + 32 >= n) {
-        defer->addr = a ? &c.tags[line] + z : nullptr;
-        defer->word = word;
-        defer->bag = bag;
-        break;
-      }
       bool bad = false;
       if (a) bad = ((ld_relaxed(&c.tags[line] + z) ^ word) & IDENT_MASK) != 0;
       if (__any_sync(FULL, bad)) {

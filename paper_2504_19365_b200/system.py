@@ -137,6 +137,7 @@ class AgileSystem:
          self.ways, self.num_sets, self.engine_warps, self.service_warps, self.infra_ctas,
          fused) = [int(x) for x in g]
         self.launch_mode = "fused" if fused else "split"
+        self.engine_copy = self.cfg.engine.copy
         self.devices = [_Device(self, d) for d in range(self.num_devices)]
         self._views = {}
 
@@ -341,6 +342,11 @@ class AgileSystem:
         self._check(self._lib.agile_run_coherence(self._ctx, op.ctypes.data, blk.ctypes.data, think.ctypes.data,
                                                   tasks, ops, seen.ctypes.data, C.byref(fl)), "run_coherence")
         return seen, int(fl.value)
+
+    def set_engine_copy(self, mode: str) -> None:
+        """engine.copy of later runs: 'registers' | 'bulk'."""
+        self._check(self._lib.agile_set_engine_copy(self._ctx, {"registers": 0, "bulk": 1}[mode]), "set_engine_copy")
+        self.engine_copy = mode
 
     def set_launch_mode(self, mode: str) -> None:
         """'split' | 'fused' | 'solo' (split launch whose user grid may run alone) | 'users' (no

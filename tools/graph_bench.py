@@ -8,10 +8,17 @@ configs[3]: SpMV + PageRank (10 iterations) on RMAT scale 27 with next-chunk pre
 Both run in sync (prefetch distance 0) and async (distance 2) mode on a cold cache; levels /
 results of the two modes are compared (bit-exact BFS levels; identical SpMV sums).
 """
+import faulthandler
 import json
 import os
 import sys
 import time
+
+faulthandler.enable()
+
+
+def note(msg):
+    print(f"[graph_bench {time.strftime('%H:%M:%S')}] {msg}", file=sys.stderr, flush=True)
 
 sys.path.insert(0, os.getcwd())
 import torch
@@ -89,6 +96,7 @@ def bfs(scale, frac):
 def spmv(scale, frac, iters):
     dev = torch.device("cuda", 0)
     t0 = time.time()
+    note(f"spmv scale {scale}: generating")
     rowT, colT, outdeg = rmat_csr(scale, 16, 2, dev, transpose=True)
     V, E = rowT.numel() - 1, colT.numel()
     vals = edge_values(E, 2, dev)
@@ -104,6 +112,7 @@ def spmv(scale, frac, iters):
     ys = {}
     rs = {}
     for pd in (0, 2):
+        note(f"spmv pd={pd}")
         s.reset()
         f0 = s.stats()["fills"]
         y, st = run_spmv(s, rowT, V, E, 0, nxt, x, 1, pd)
@@ -111,6 +120,7 @@ def spmv(scale, frac, iters):
         ys[pd] = y
         s.reset()
         f0 = s.stats()["fills"]
+        note(f"pagerank pd={pd}")
         rs[pd], pr = run_pagerank(s, rowT, V, E, 0, outdeg, iters, prefetch_distance=pd)
         pr["page_misses"] = s.stats()["fills"] - f0
         res[pd] = {"spmv_ms": st["ms"], "spmv_gflops": st["gflops"], "spmv_page_fills": st["page_misses"],
@@ -130,6 +140,7 @@ def spmv(scale, frac, iters):
         import numpy as np
         from oracle import cgraph
         t1 = time.time()
+        note("oracle: spmv")
         view = s.store_view(0)
         colT_h = view[:E * 4].view("<i4")
         vals_h = view[nxt * 4096:nxt * 4096 + E * 4].view("<f4")
@@ -140,6 +151,7 @@ def spmv(scale, frac, iters):
         got = ys[0].cpu().numpy().astype(np.float64)
         err = np.abs(got - exp) / np.maximum(np.abs(exp), 1e-30)
         ok = np.abs(got - exp) <= 1e-5 * np.abs(exp) + 1e-12 * mag
+        note("oracle: pagerank")
         pr_exp = cgraph.pagerank_f32(rp, colT_h, outdeg.cpu().numpy(), iters).astype(np.float64)
         pr_err = np.abs(rs[0].cpu().numpy().astype(np.float64) - pr_exp) / pr_exp
         line["oracle"] = {"kind": "oracle/graph_oracle.c", "spmv_within_1e-5": bool(ok.all()),

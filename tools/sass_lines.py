@@ -25,7 +25,7 @@ def line_map(so, fn_sub):
     for ln in dis.splitlines():
         m = re.match(r"\.text\.(\S+):", ln)
         if m:
-            cur = m.group(1) if fn_sub in m.group(1) and "agile_kernel" in m.group(1) else None
+            cur = m.group(1) if fn_sub in m.group(1) and ("agile_kernel" in m.group(1) or "agile_user_kernel" in m.group(1)) else None
             continue
         if cur is None:
             continue
