@@ -18,6 +18,7 @@
  *   AGILE_E_ILLEGAL      IllegalState        (software_cache.py:26)
  *   AGILE_E_LIVELOCK     LivelockSuspected   (sim_core.py:23)
  *   AGILE_E_BUFFER_BUSY  BufferBusy          (gpu_api.py:21)
+ *   AGILE_E_LOCK_CYCLE   DeadlockDetector report (lock_chain.py:70-121; debug_locks = on)
  * Config errors (unknown key / bad value) return AGILE_E_CONFIG (ValueError/KeyError in Python).
  */
 #ifndef AGILE_B200_H
@@ -40,6 +41,7 @@ typedef struct agile_ctx agile_ctx;
 #define AGILE_E_ILLEGAL (-104)
 #define AGILE_E_LIVELOCK (-105)
 #define AGILE_E_BUFFER_BUSY (-106)
+#define AGILE_E_LOCK_CYCLE (-107)
 
 /* stats slots (agile_stats) — software_cache.py:166-170, agile_service.py:75-87, ssd_model.py:125-128 */
 enum {
@@ -157,6 +159,11 @@ int agile_evict_blocks(agile_ctx* ctx, const uint32_t* dev, const uint64_t* blk,
 int agile_array_get(agile_ctx* ctx, const uint32_t* dev, const uint64_t* idx, int64_t n, uint32_t elem_size,
                     void* out);
 
+/* debug_locks demonstration (tests/test_lock_chain.py:26-95): mode 0 plants a ring of n warps, each
+ * holding set lock w and taking set lock (w+1) mod n; mode 1 has one warp take set lock 0 twice.
+ * With debug_locks the wait-for cycle is reported in the event log ("lock", "deadlock") and the
+ * call returns AGILE_E_LOCK_CYCLE; without it the spins end in LivelockSuspected. */
+int agile_lock_cycle_demo(agile_ctx* ctx, uint32_t n, int mode);
 /* SoftwareCache.flush (software_cache.py:283-298): write back every MODIFIED line (lines the share
  * table drained into the cache) and wait for durability; *flushed = lines written back. */
 int agile_flush(agile_ctx* ctx, uint64_t* flushed);

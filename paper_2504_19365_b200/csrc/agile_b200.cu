@@ -175,9 +175,9 @@ int device_error(agile_ctx* ctx) {
   CK(cudaMemcpy(&pw, ctx->d.pw, sizeof(pw), cudaMemcpyDeviceToHost));
   if (!pw.error_code) return 0;
   static const char* names[] = {"ok", "ProtocolViolation", "UnknownCid", "OutOfRange", "IllegalState",
-                                "LivelockSuspected", "BufferBusy"};
+                                "LivelockSuspected", "BufferBusy", "LockCycle"};
   char buf[256];
-  snprintf(buf, sizeof buf, "%s (device) a=%llu b=%llu", pw.error_code < 7 ? names[pw.error_code] : "?",
+  snprintf(buf, sizeof buf, "%s (device) a=%llu b=%llu", pw.error_code < 8 ? names[pw.error_code] : "?",
            (unsigned long long)pw.error_a, (unsigned long long)pw.error_b);
   ctx->err = buf;
   const int code = -(100 + (int)pw.error_code);
@@ -577,6 +577,14 @@ int agile_create(const char* config_text, int cuda_device, agile_ctx** out) {
   if ((rc = dalloc(ctx, &d.set_lock, d.num_sets))) return rc;
   if ((rc = dalloc(ctx, &d.hand, d.num_sets))) return rc;
   d.st_buckets = st_on ? (uint32_t)st_buckets : 0u;
+  // debug_locks (lock_chain.py DeadlockDetector): holder word per lock, wait word per user thread
+  d.dbg_locks = cfg.b("debug_locks", true) ? 1u : 0u;
+  if (d.dbg_locks) {
+    d.dbg_threads = (uint32_t)ctx->sms * 2048u + 65536u;
+    if ((rc = dalloc(ctx, &d.lk_holder, (size_t)d.num_sets + (size_t)d.num_devices * d.pairs_per_device + d.st_buckets)))
+      return rc;
+    if ((rc = dalloc(ctx, &d.lk_wait, d.dbg_threads))) return rc;
+  }
   if (st_on) {
     if ((rc = dalloc(ctx, &d.st, st_buckets))) return rc;
     if ((rc = dalloc(ctx, &d.st_lock, st_buckets))) return rc;
@@ -1028,6 +1036,17 @@ int agile_share_live(agile_ctx* ctx, uint64_t* live) {
   CK(cudaMemcpy(e.data(), ctx->d.st, e.size() * sizeof(ShareEntry), cudaMemcpyDeviceToHost));
   for (const auto& x : e) *live += x.key >= 2 ? 1 : 0;   // share_table.py:198-199 live_entries
   return 0;
+}
+
+int agile_lock_cycle_demo(agile_ctx* ctx, uint32_t n, int mode) {
+  if (!ctx || n < 1 || n > kCtaWarps || mode < 0 || mode > 1) return fail(ctx, AGILE_E_ARG, "bad lock demo args");
+  CK(cudaSetDevice(ctx->device));
+  LockCycleWork w;
+  w.n = n;
+  w.mode = (uint32_t)mode;
+  int rc = launch(ctx, w, 1, ctx->stream);
+  if (!rc) rc = agile_sync(ctx, ctx->stream);
+  return rc;
 }
 
 int agile_array_get(agile_ctx* ctx, const uint32_t* dev, const uint64_t* idx, int64_t n, uint32_t elem_size,

@@ -259,19 +259,75 @@ __device__ __forceinline__ int modulo_pick_serial(const DevCtx& c, u64 base, u32
   return -1;
 }
 
-__device__ __forceinline__ bool lock_set(const DevCtx& c, u32 set) {
+// ---------------------------------------------------------------- debug_locks: wait-for cycles
+// The reference's DeadlockDetector (lock_chain.py:70-121), restated as a wait-for graph over device
+// words: every lock (set locks, SQ doorbell locks, share-table bucket locks) publishes its holder
+// thread, every thread publishes the lock it is failing to take; a failed attempt walks
+// lock -> holder -> the lock that holder waits for -> ... and a path back to the caller is a cycle:
+// it is logged ("lock", "deadlock") and the run aborts with the cycle instead of spinning into
+// the watchdog.  Off (one predictable branch per lock operation) unless debug_locks is set.
+__device__ __forceinline__ u32 lk_set_id(const DevCtx& c, u32 set) { (void)c; return set; }
+__device__ __forceinline__ u32 lk_db_id(const DevCtx& c, u32 q) { return c.num_sets + q; }
+__device__ __forceinline__ u32 lk_bucket_id(const DevCtx& c, u32 h) { return c.num_sets + c.num_qp + h; }
+__device__ __forceinline__ u32 lk_me() { return blockIdx.x * blockDim.x + threadIdx.x; }
+__device__ __forceinline__ void lk_acquired(const DevCtx& c, u32 id) {
+  if (!c.dbg_locks) return;
+  const u32 me = lk_me();
+  if (me >= c.dbg_threads) return;
+  st_relaxed(&c.lk_holder[id], me + 1);
+  st_relaxed(&c.lk_wait[me], 0u);
+}
+__device__ __forceinline__ void lk_released(const DevCtx& c, u32 id) {
+  if (c.dbg_locks) st_relaxed(&c.lk_holder[id], 0u);
+}
+__device__ __forceinline__ void lk_stop_waiting(const DevCtx& c) {
+  if (!c.dbg_locks) return;
+  const u32 me = lk_me();
+  if (me < c.dbg_threads) st_relaxed(&c.lk_wait[me], 0u);
+}
+__device__ __noinline__ bool lk_failed_slow(const DevCtx& c, u32 id, u32 who) {
+  const u32 me = lk_me();
+  if (me >= c.dbg_threads) return false;
+  st_relaxed(&c.lk_wait[me], id + 1);
+  u32 cur = id, path[4] = {NONE, NONE, NONE, NONE}, np = 0;
+  for (u32 hop = 0; hop < 64; ++hop) {
+    const u32 h = ld_relaxed(&c.lk_holder[cur]);
+    if (h == 0) return false;
+    if (np < 4) path[np] = cur;
+    ++np;
+    if (h - 1 == me) {
+      // re-validate once (lock_chain.py:117-121): the first hop must still be held by the same thread
+      if (ld_relaxed(&c.lk_holder[id]) == 0) return false;
+      log_ev(c, who, M_LOCK, A_DEADLOCK, id, np, path[0], path[1], path[2], path[3]);
+      set_error(c, E_LOCK_CYCLE, id, np);
+      return true;
+    }
+    const u32 w = ld_relaxed(&c.lk_wait[h - 1]);
+    if (w == 0) return false;
+    cur = w - 1;
+  }
+  return false;
+}
+__device__ __forceinline__ bool lk_failed(const DevCtx& c, u32 id, u32 who) {
+  return c.dbg_locks ? lk_failed_slow(c, id, who) : false;
+}
+
+__device__ __forceinline__ bool lock_set(const DevCtx& c, u32 set, u32 who = WHO_USER) {
   int ok = 1;
   if (lane_id() == 0) {
     Spin sp;
     while (atom_cas_acquire(&c.set_lock[set], 0u, 1u) != 0u) {
+      lk_failed(c, lk_set_id(c, set), who);
       if (!sp.again(c, 256, __LINE__ + 100000 * SPIN_FILE_ID)) { ok = 0; break; }
     }
+    if (ok) lk_acquired(c, lk_set_id(c, set));
+    else lk_stop_waiting(c);
   }
   return __shfl_sync(FULL, ok, 0) != 0;
 }
 __device__ __forceinline__ void unlock_set(const DevCtx& c, u32 set) {
   __syncwarp();
-  if (lane_id() == 0) st_release(&c.set_lock[set], 0u);
+  if (lane_id() == 0) { lk_released(c, lk_set_id(c, set)); st_release(&c.set_lock[set], 0u); }
 }
 
 // Pin a line found by a lock-free probe: CAS the pin count up by n (capped, so a hot page can
@@ -304,7 +360,7 @@ __device__ int claim_key_warp(const DevCtx& c, u64 key, u32 pin_n, u32 who, u32&
   const u32 W = c.ways;
   victim_key = ~0ull;
   if (lane == 0) log_ev(c, who, M_CACHE, A_MISS, key_dev(key), key_blk(key));
-  if (!lock_set(c, set)) return R_RETRY;
+  if (!lock_set(c, set, who)) return R_RETRY;
   for (int attempt = 0;; ++attempt) {
     if (aborted(c)) { unlock_set(c, set); return R_RETRY; }
     u32 l; u64 w;
@@ -426,7 +482,11 @@ __device__ int claim_lanes(const DevCtx& c, bool want, u64 key, u32 pin_n, u32 w
     const bool mine = (pending >> lane) & 1u;
     bool got = false;
     bool settled = false;
-    if (mine) got = atom_cas_acquire(&c.set_lock[set], 0u, 1u) == 0u;
+    if (mine) {
+      got = atom_cas_acquire(&c.set_lock[set], 0u, 1u) == 0u;
+      if (got) lk_acquired(c, lk_set_id(c, set));
+      else lk_failed(c, lk_set_id(c, set), who);
+    }
     if (got) {
       u32 avail = 0, ref1 = 0;
       int found = -1;
@@ -521,6 +581,7 @@ __device__ int claim_lanes(const DevCtx& c, bool want, u64 key, u32 pin_n, u32 w
           // else: a hitter pinned/touched the victim between scan and CAS: re-evaluate next pass
         }
       }
+      lk_released(c, lk_set_id(c, set));
       st_release(&c.set_lock[set], 0u);
     }
     const u32 progressed = __ballot_sync(FULL, got);
@@ -532,6 +593,7 @@ __device__ int claim_lanes(const DevCtx& c, bool want, u64 key, u32 pin_n, u32 w
       }
     }
   }
+  if (want) lk_stop_waiting(c);
   const u32 nf = __popc(__ballot_sync(FULL, fills != 0));
   const u32 nr = __popc(__ballot_sync(FULL, resets != 0));
   if (lane == 0) {
@@ -563,11 +625,18 @@ __device__ bool ring_doorbell_until(const DevCtx& c, u32 q, u64 target, u32 who)
     // doorbell is almost never past them yet); afterwards check the doorbell before retrying
     if (!first) {
       const u64 db = ld_acquire(&s->db);
-      if (db >= target) return true;
+      if (db >= target) {
+        if (lane == 0) lk_stop_waiting(c);
+        return true;
+      }
     }
     first = false;
     int got = 0;
-    if (lane == 0) got = atom_cas_acquire(&s->db_lock, 0u, 1u) == 0u;
+    if (lane == 0) {
+      got = atom_cas_acquire(&s->db_lock, 0u, 1u) == 0u;
+      if (got) lk_acquired(c, lk_db_id(c, q));
+      else lk_failed(c, lk_db_id(c, q), who);
+    }
     got = __shfl_sync(FULL, got, 0);
     if (got) {
       const u64 old = ld_relaxed(&s->db);
@@ -598,6 +667,7 @@ __device__ bool ring_doorbell_until(const DevCtx& c, u32 q, u64 target, u32 who)
           st_release(&s->db, v);   // the doorbell is a release fence
           atomicAdd(&c.stats[S_DOORBELLS], 1ull);
         }
+        lk_released(c, lk_db_id(c, q));
         st_release(&s->db_lock, 0u);
       }
       __syncwarp();
@@ -1008,6 +1078,7 @@ __device__ bool write_block_warp(const DevCtx& c, bool active, u64 key, WaitNode
       // open waiter lists under the same lock, so no list opened here can be clobbered)
       const u32 set = line / c.ways;
       if (atom_cas_acquire(&c.set_lock[set], 0u, 1u) == 0u) {
+        lk_acquired(c, lk_set_id(c, set));
         const u64 w = ld_relaxed(&c.tags[line]);
         const u32 st = tw_state(w);
         if (tw_live(w) && tw_key(w) == key && (st == ST_READY || st == ST_MODIFIED) && tw_pins(w) == 0) {
@@ -1020,7 +1091,10 @@ __device__ bool write_block_warp(const DevCtx& c, bool active, u64 key, WaitNode
             log_state(c, who, line, st, ST_BUSY, key);
           }
         }
+        lk_released(c, lk_set_id(c, set));
         st_release(&c.set_lock[set], 0u);
+      } else {
+        lk_failed(c, lk_set_id(c, set), who);
       }
     }
     const u32 mb = __ballot_sync(FULL, go && line == NONE);
@@ -1096,6 +1170,7 @@ __device__ bool write_block_warp(const DevCtx& c, bool active, u64 key, WaitNode
     if (once) break;
     if (__any_sync(FULL, want) && !sp.again(c, 2048, __LINE__ + 100000 * SPIN_FILE_ID)) break;
   }
+  if (active) lk_stop_waiting(c);
   return want;
 }
 

@@ -90,6 +90,7 @@ enum : u32 {
   E_ILLEGAL_STATE = 4,          // IllegalState       software_cache.py:26
   E_LIVELOCK = 5,               // LivelockSuspected  sim_core.py:23
   E_BUFFER_BUSY = 6,            // BufferBusy         gpu_api.py:21
+  E_LOCK_CYCLE = 7,             // DeadlockDetector report (lock_chain.py:70-121), debug_locks
 };
 
 // stats slots (software_cache.py:166-170, agile_service.py:75-87, ssd_model.py:125-128)
@@ -100,14 +101,14 @@ enum : int {
 };
 
 // event-log codes (K10); rendered host-side into the reference trace tuples (sim_core.py:162-191)
-enum : u32 { M_NVME = 0, M_SSD = 1, M_SVC = 2, M_CACHE = 3, M_API = 4, M_TABLE = 5, M_TEST = 6 };
+enum : u32 { M_NVME = 0, M_SSD = 1, M_SVC = 2, M_CACHE = 3, M_API = 4, M_TABLE = 5, M_TEST = 6, M_LOCK = 7 };
 enum : u32 {
   A_ENQUEUE = 0, A_SQE_UPDATED, A_SQE_ISSUED, A_DOORBELL, A_SQE_RELEASE, A_HEAD,
   A_FETCH, A_COMPLETE, A_CQE_POST, A_CQE_STALL,
   A_WINDOW_RING, A_DRAIN_RING, A_STOP, A_START, A_CQE_PROCESS,
   A_STATE, A_MISS, A_HIT, A_ATTACH, A_EVICT_RESET, A_DRAIN, A_ASYNC_READ, A_PREFETCH, A_INSTALL,
   A_WRITE_COMMIT, A_OBSERVE, A_REGISTER, A_SHARE, A_RELEASE, A_MODIFIED, A_PROPAGATE, A_DUTY_TRANSFER,
-  A_EVICT_WB, A_WRITE_INTENT
+  A_EVICT_WB, A_WRITE_INTENT, A_DEADLOCK
 };
 enum : u32 { WHO_USER = 0u << 30, WHO_SVC = 1u << 30, WHO_DEV = 2u << 30, WHO_HOST = 3u << 30 };
 
@@ -187,6 +188,8 @@ struct DevCtx {
   u32 policy;               // victim policy inside a set: POL_CLOCK | POL_MODULO (CachePolicy seam)
   u32 find_another;         // busy_eviction_choice: 0 wait, 1 find_another (software_cache.py:366-371)
   u32 st_buckets;           // share table (share_table.py:52-200): buckets (power of two), 0 = disabled
+  u32 dbg_locks;            // debug_locks: wait-for cycle detection on every lock (lock_chain.py)
+  u32 dbg_threads;          // size of lk_wait (user threads tracked)
   u64 watchdog_ns;
   u64 user_start_ns;        // the infra grid gives up on a user grid that has not started by then
   // cache
@@ -199,6 +202,8 @@ struct DevCtx {
   u64 nodes_lo, nodes_hi;   // this run's WaitNode array (range checks on waiter-list walks)
   struct ShareEntry* st;    // share table entries [st_buckets]
   u32* st_lock;             // per-bucket locks [st_buckets]
+  u32* lk_holder;           // debug_locks: holder thread + 1 per lock id (sets, SQ doorbells, buckets)
+  u32* lk_wait;             // debug_locks: lock id + 1 each user thread spins on, 0 = none
   // queues
   uint4* sqe;              // num_qp * sq_depth * 4 (64 B each)
   u32* sq_state;

@@ -39,13 +39,19 @@ __device__ __forceinline__ u32 st_home(const DevCtx& c, u64 key) {   // share_ta
   const u64 h = ((u64)key_dev(key) * 0x9E3779B1ull) ^ (key_blk(key) * 0x85EBCA77ull);
   return (u32)(h & (c.st_buckets - 1));
 }
-__device__ __forceinline__ bool st_lock(const DevCtx& c, u32 h) {
+__device__ __forceinline__ bool st_lock(const DevCtx& c, u32 h, u32 who = WHO_USER) {
   Spin sp;
-  while (atom_cas_acquire(&c.st_lock[h], 0u, 1u) != 0u)
-    if (!sp.again(c, 256, __LINE__ + 100000 * SPIN_FILE_ID)) return false;
+  while (atom_cas_acquire(&c.st_lock[h], 0u, 1u) != 0u) {
+    lk_failed(c, lk_bucket_id(c, h), who);
+    if (!sp.again(c, 256, __LINE__ + 100000 * SPIN_FILE_ID)) { lk_stop_waiting(c); return false; }
+  }
+  lk_acquired(c, lk_bucket_id(c, h));
   return true;
 }
-__device__ __forceinline__ void st_unlock(const DevCtx& c, u32 h) { st_release(&c.st_lock[h], 0u); }
+__device__ __forceinline__ void st_unlock(const DevCtx& c, u32 h) {
+  lk_released(c, lk_bucket_id(c, h));
+  st_release(&c.st_lock[h], 0u);
+}
 
 // linear probe from the home bucket (share_table.py:70-86): the entry's slot or -1, with the first
 // insertable slot (tombstone or empty) and the key word seen there

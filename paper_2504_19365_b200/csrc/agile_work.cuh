@@ -381,6 +381,29 @@ struct CoherenceWork {
   }
 };
 
+// ------------------------------------------------------------------ LockCycleWork
+// Planted lock-order bugs for the debug_locks detector (tests/test_lock_chain.py:26-47, 84-95):
+// mode 0 — warps 0..n-1 each take set lock w, then (after all hold theirs) set lock (w+1) mod n:
+// a ring of n; mode 1 — warp 0 takes set lock 0 twice (a one-cycle).  With debug_locks the
+// cycle is reported and the run aborts with E_LOCK_CYCLE; without it the spins end in the watchdog.
+struct LockCycleWork {
+  u32 n, mode;
+  __device__ void run(const DevCtx& c, u32 uidx, u32 nusers) const {
+    if (uidx != 0) return;
+    const u32 w = threadIdx.x >> 5;
+    const u32 who = WHO_USER | w;
+    const bool part = mode == 0 ? w < n : w == 0;
+    bool held = false;
+    if (part) held = lock_set(c, w % c.num_sets, who);
+    __syncthreads();
+    if (part && held) {
+      const u32 next = mode == 0 ? (w + 1) % n : w;
+      if (lock_set(c, next % c.num_sets, who)) unlock_set(c, next % c.num_sets);
+      unlock_set(c, w % c.num_sets);
+    }
+  }
+};
+
 // ------------------------------------------------------------------ FlushWork
 // SoftwareCache.flush (software_cache.py:283-298) as an API call: one warp writes every MODIFIED
 // line back and waits for durability.

@@ -33,6 +33,10 @@ class LivelockSuspected(AgileError):
     """The device watchdog saw no progress within the budget."""
 
 
+class LockCycle(LivelockSuspected):
+    """debug_locks found a wait-for cycle (the DeadlockDetector report, lock_chain.py:70-121)."""
+
+
 class BufferBusy(AgileError):
     """Buffer reused while its previous transfer is still pending."""
 
@@ -51,4 +55,5 @@ CODE_TO_EXC = {
     -104: IllegalState,
     -105: LivelockSuspected,
     -106: BufferBusy,
+    -107: LockCycle,
 }

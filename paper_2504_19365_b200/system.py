@@ -323,6 +323,11 @@ class AgileSystem:
         self._check(self._lib.agile_flush(self._ctx, C.byref(n)), "flush")
         return int(n.value)
 
+    def lock_cycle_demo(self, n: int, mode: int = 0) -> None:
+        """Planted lock-order bug (mode 0: ring of n warps, 1: a warp re-taking its lock); raises
+        LockCycle when debug_locks reports the wait-for cycle (lock_chain.py DeadlockDetector)."""
+        self._check(self._lib.agile_lock_cycle_demo(self._ctx, n, mode), "lock_cycle_demo")
+
     def share_live(self) -> int:
         """ShareTable.live_entries (share_table.py:198-199); 0 when the table is disabled."""
         n = C.c_uint64(0)

@@ -11,13 +11,13 @@ from __future__ import annotations
 
 import numpy as np
 
-MODULES = ("nvme", "ssd", "svc", "cache", "api", "table", "test")
+MODULES = ("nvme", "ssd", "svc", "cache", "api", "table", "test", "lock")
 ACTIONS = ("enqueue", "sqe_updated", "sqe_issued", "doorbell", "sqe_release", "head",
            "fetch", "complete", "cqe_post", "cqe_stall",
            "window_ring", "drain_ring", "stop", "start", "cqe_process",
            "state", "miss", "hit", "attach", "evict_reset", "drain", "async_read", "prefetch", "install",
            "write_commit", "observe", "register", "share", "release", "modified", "propagate", "duty_transfer",
-           "evict_wb", "write_intent")
+           "evict_wb", "write_intent", "deadlock")
 STATES = ("INVALID", "BUSY", "READY", "MODIFIED")
 OPS = ("READ", "WRITE")
 ARITY = {"enqueue": 6, "sqe_updated": 2, "sqe_issued": 3, "doorbell": 4, "sqe_release": 3,
@@ -26,7 +26,7 @@ ARITY = {"enqueue": 6, "sqe_updated": 2, "sqe_issued": 3, "doorbell": 4, "sqe_re
          "state": 5, "miss": 2, "hit": 2, "attach": 2, "evict_reset": 3, "drain": 2,
          "async_read": 2, "prefetch": 2, "install": 3,
          "write_commit": 3, "observe": 3, "register": 2, "share": 4, "release": 3, "modified": 2, "propagate": 2,
-         "duty_transfer": 3, "evict_wb": 3, "write_intent": 2}
+         "duty_transfer": 3, "evict_wb": 3, "write_intent": 2, "deadlock": 6}
 SHARE_STATES = ("Exclusive", "Shared", "Modified")
 
 RECORD = np.dtype([("t", "<u8"), ("who", "<u4"), ("modact", "<u4"), ("a", "<u8", (6,))])

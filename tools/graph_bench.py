@@ -85,7 +85,7 @@ def bfs(scale, frac):
         # page store the GPU read it from, row_ptr copied back
         from oracle import cgraph
         t1 = time.time()
-        col_h = s.store_view(0)[:E * 4].view("<i4")
+        col_h = s.store_view(0).reshape(-1)[:E * 4].view("<i4")
         exp = cgraph.bfs_levels(row_ptr.cpu().numpy(), col_h, pick_source(row_ptr, 0))
         line["oracle"] = {"levels_equal_oracle": bool((ref.cpu().numpy() == exp).all()), "kind": "oracle/graph_oracle.c",
                           "seconds": time.time() - t1}
@@ -141,7 +141,7 @@ def spmv(scale, frac, iters):
         from oracle import cgraph
         t1 = time.time()
         note("oracle: spmv")
-        view = s.store_view(0)
+        view = s.store_view(0).reshape(-1)    # bytes of the pinned store
         colT_h = view[:E * 4].view("<i4")
         vals_h = view[nxt * 4096:nxt * 4096 + E * 4].view("<f4")
         rp = rowT.cpu().numpy()
