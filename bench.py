@@ -182,7 +182,8 @@ def _cpu_port(plan, rank, lines, scatter, threads, seconds, max_steps=400, warm_
         done += idx.size
         k += 1
     st = cc.stats()
-    desc = (f"{k} fresh batches of {bs} samples x {len(tabs)} tables x {L} lookups after {warm_batches} warm-up "
+    desc = (f"{k} fresh batches of {bs} samples x {len(tabs)} tables x {L} lookups after " if k else "")
+    desc += (f"{warm_batches} warm-up "
             f"batches of {B} ({warm_s:.1f} s; steady-state cache of {lines} lines, 32 ways; "
             f"hit rate {st['hits'] / max(1, st['hits'] + st['misses']):.3f}); oracle/agile_oracle.c on {threads} threads")
     return (done / tsum if tsum > 0 else 0.0), desc, cc
