@@ -452,7 +452,7 @@ def main():
     miss_bytes = fills / args.steps * 4096
     roofline = {"bound": "link", "achieved": miss_bytes / avg_kern_s / 1e9, "peak": link_peak, "unit": "GB/s",
                 "frac": miss_bytes / avg_kern_s / 1e9 / link_peak,
-                "traffic": prof.get("link_bytes_per_launch"),
+                "traffic": prof.get("link_bytes_per_launch"), "traffic_counter": "pcie__read_bytes.sum",
                 "kernel": f"agile_infra_kernel (engine page copies) + agile_user_kernel<EmbBagWork> ({system.launch_mode} launch)",
                 "algorithmic_bytes_per_launch": miss_bytes,
                 "iops": fills / args.steps / avg_kern_s, "page_fills_per_step": fills / args.steps,
@@ -575,6 +575,9 @@ def main():
         c = cnt.cpu().numpy()
         line["roofline_hit"] = {"bound": "hbm", "achieved": alg_bytes / hit_s / 1e9, "peak": hbm_peak,
                                 "unit": "GB/s", "frac": alg_bytes / hit_s / 1e9 / hbm_peak,
+                                "traffic": prof.get("hit_dram_bytes_per_launch"),
+                                "traffic_note": "dram read + write of the production user kernel on the uniform (no-reuse) "
+                                                "all-hit replay (profiles/k5_r02.md); this replay is the bench batch (Zipf)",
                                 "miss_lookups": int(c[1]), "ms_per_launch": hit_s * 1e3,
                                 "lookups_per_s": B * Tg * L / hit_s}
         # ---- end to end through the C-ABI with host buffers (H2D indices, D2H pooled) ----

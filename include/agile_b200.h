@@ -164,6 +164,9 @@ int agile_array_get(agile_ctx* ctx, const uint32_t* dev, const uint64_t* idx, in
  * With debug_locks the wait-for cycle is reported in the event log ("lock", "deadlock") and the
  * call returns AGILE_E_LOCK_CYCLE; without it the spins end in LivelockSuspected. */
 int agile_lock_cycle_demo(agile_ctx* ctx, uint32_t n, int mode);
+/* BufferBusy (gpu_api.py:132-137): a transfer started on a buffer whose previous transfer is still
+ * pending (async_read, then async_read / async_write without wait) returns AGILE_E_BUFFER_BUSY. */
+int agile_buffer_busy_demo(agile_ctx* ctx, int write);
 /* SoftwareCache.flush (software_cache.py:283-298): write back every MODIFIED line (lines the share
  * table drained into the cache) and wait for durability; *flushed = lines written back. */
 int agile_flush(agile_ctx* ctx, uint64_t* flushed);

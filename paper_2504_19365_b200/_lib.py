@@ -50,6 +50,7 @@ SIGNATURES = {
     "agile_user_run_end": (_int, [_vp, _vp]),
     "agile_flush": (_int, [_vp, C.POINTER(_u64)]),
     "agile_lock_cycle_demo": (_int, [_vp, _u32, _int]),
+    "agile_buffer_busy_demo": (_int, [_vp, _int]),
     "agile_share_live": (_int, [_vp, C.POINTER(_u64)]),
     "agile_run_coherence": (_int, [_vp, _vp, _vp, _vp, _u32, _u32, _vp, C.POINTER(_u64)]),
     "agile_embbag_host_submit": (_int, [_vp, _vp, _vp, _vp, _vp, _vp, _u32, _u32, _u32, _u32, _u32, _int]),

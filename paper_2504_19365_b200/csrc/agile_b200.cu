@@ -188,7 +188,7 @@ int device_error(agile_ctx* ctx) {
   return code;
 }
 
-WaitNode* get_nodes(agile_ctx* ctx, size_t n) {
+WaitNode* get_nodes_raw(agile_ctx* ctx, size_t n) {
   if (n > ctx->nodes_cap) {
     if (ctx->nodes) { cudaDeviceSynchronize(); cudaFree(ctx->nodes); }
     ctx->nodes = nullptr;
@@ -198,6 +198,14 @@ WaitNode* get_nodes(agile_ctx* ctx, size_t n) {
     ctx->nodes_cap = n;
   }
   return reinterpret_cast<WaitNode*>(ctx->nodes);
+}
+
+// the run's AgileBuf barriers, zeroed on the run's stream (t_issue 0 = never used: the BufferBusy
+// check of a fresh run never sees a previous run's state)
+WaitNode* get_nodes(agile_ctx* ctx, size_t n, cudaStream_t st = nullptr) {
+  WaitNode* w = get_nodes_raw(ctx, n);
+  if (w && cudaMemsetAsync(w, 0, n * sizeof(WaitNode), st ? st : ctx->stream) != cudaSuccess) return nullptr;
+  return w;
 }
 
 // dynamic shared memory of a workload's launch (W::kDynSmem when it declares one: the embedding-
@@ -943,7 +951,7 @@ int agile_user_run_begin(agile_ctx* ctx, void* stream, uint32_t n_user_ctas, uin
   if (ctx->fused)
     return fail(ctx, AGILE_E_ARG, "third-party user kernels need the split launch (a kernel-serialising tool is attached)");
   CK(cudaSetDevice(ctx->device));
-  WaitNode* nodes = get_nodes(ctx, std::max<uint64_t>(1, n_bufs));
+  WaitNode* nodes = get_nodes(ctx, std::max<uint64_t>(1, n_bufs), reinterpret_cast<cudaStream_t>(stream));
   if (!nodes) return fail(ctx, AGILE_E_CUDA, "node allocation failed");
   if (nodes_out) *nodes_out = nodes;
   cudaFuncAttributes a{};
@@ -1049,6 +1057,22 @@ int agile_lock_cycle_demo(agile_ctx* ctx, uint32_t n, int mode) {
   return rc;
 }
 
+int agile_buffer_busy_demo(agile_ctx* ctx, int write) {
+  if (!ctx) return AGILE_E_ARG;
+  CK(cudaSetDevice(ctx->device));
+  DevTmp tmp;
+  uint4* d_buf;
+  CK(tmp.alloc(&d_buf, kBlockBytes));
+  BusyWork w;
+  w.nodes = get_nodes(ctx, 1);
+  w.buf = d_buf;
+  w.write = write ? 1u : 0u;
+  if (!w.nodes) return fail(ctx, AGILE_E_CUDA, "node allocation failed");
+  int rc = launch(ctx, w, 1, ctx->stream);
+  if (!rc) rc = agile_sync(ctx, ctx->stream);
+  return rc;
+}
+
 int agile_array_get(agile_ctx* ctx, const uint32_t* dev, const uint64_t* idx, int64_t n, uint32_t elem_size,
                     void* out) {
   if (!ctx || n < 0 || (n && (!dev || !idx || !out))) return fail(ctx, AGILE_E_ARG, "bad array_get args");
@@ -1114,7 +1138,7 @@ int agile_run_reads(agile_ctx* ctx, const uint64_t* keys, uint32_t tasks, uint32
   w.epoch_t = reinterpret_cast<u64*>(epoch_t);
   w.tasks = tasks; w.reads = reads; w.epochs = epochs; w.async_mode = async_mode ? 1u : 0u;
   w.compute_ns = compute_ns;
-  w.nodes = get_nodes(ctx, (size_t)tasks * 2 * reads);
+  w.nodes = get_nodes(ctx, (size_t)tasks * 2 * reads, reinterpret_cast<cudaStream_t>(stream));
   if (!w.nodes) return fail(ctx, AGILE_E_CUDA, "node allocation failed");
   const uint32_t users = (tasks + kCtaThreads - 1) / kCtaThreads;
   const uint32_t cap = resident_ctas<ReadsWork>(ctx);
@@ -1144,7 +1168,7 @@ int agile_run_loop_rw(agile_ctx* ctx, uint32_t conc, uint64_t warmup_ns, uint64_
   w.warmup_ns = warmup_ns;
   w.measure_ns = measure_ns;
   w.max_per_task = max_per_task ? max_per_task : ~0ull;
-  w.nodes = get_nodes(ctx, conc);
+  w.nodes = get_nodes(ctx, conc, reinterpret_cast<cudaStream_t>(stream));
   if (!w.nodes) return fail(ctx, AGILE_E_CUDA, "node allocation failed");
   const uint32_t users = (conc + kCtaThreads - 1) / kCtaThreads;
   return launch(ctx, w, users, reinterpret_cast<cudaStream_t>(stream));

@@ -942,6 +942,17 @@ __device__ __forceinline__ bool wl_push(const DevCtx& c, u32 line, u32 ver, Wait
   }
 }
 
+// AgileApi._fresh_barrier (gpu_api.py:132-137): a buffer whose previous transfer is still pending
+// (issued, barrier not DONE) cannot start another one -> BufferBusy.  WaitNodes start zeroed
+// (t_issue 0: never used) at every run that hands them out.
+__device__ __forceinline__ bool buffer_busy(const DevCtx& c, const WaitNode* node) {
+  if (node->t_issue != 0 && ld_acquire(&node->done) == 0) {
+    set_error(c, E_BUFFER_BUSY, (u64)(uintptr_t)node, node->t_issue);
+    return true;
+  }
+  return false;
+}
+
 __device__ __forceinline__ void copy_page_warp(const uint4* src, uint4* dst) {
   const u32 lane = lane_id();
   uint4 v[8];
@@ -957,6 +968,7 @@ __device__ __forceinline__ void copy_page_warp(const uint4* src, uint4* dst) {
 __device__ void async_read_warp(const DevCtx& c, bool active, u64 key, WaitNode* node, uint4* dst, u32 who,
                                 u32 sq_start, int* outcome = nullptr, u64* victim = nullptr) {
   const u32 lane = lane_id();
+  if (active && buffer_busy(c, node)) active = false;
   bool want = active;
   if (active) { node->dst = (u64)(uintptr_t)dst; node->done = 0; node->t_issue = gtimer(); }
   __syncwarp();
@@ -1059,6 +1071,7 @@ __device__ bool write_block_warp(const DevCtx& c, bool active, u64 key, WaitNode
       active = false;
     }
   }
+  if (active && !once && buffer_busy(c, node)) active = false;
   if (active) { node->dst = 0; node->done = 0; node->t_issue = gtimer(); }
   __syncwarp();
   bool want = active;

@@ -204,10 +204,12 @@ __device__ void release_shared_warp(const DevCtx& c, bool active, u64 key, uint4
 __device__ void async_read_t(const DevCtx& c, bool active, u64 key, WaitNode* node, uint4* dst, u32 who, u32 sq,
                              WaitNode*& eff) {
   eff = node;
+  if (active && buffer_busy(c, node)) active = false;
   bool go = active;
   if (c.st_buckets && active) {
     node->dst = (u64)(uintptr_t)dst;
     node->done = 0;
+    node->t_issue = 0;   // (async_read_warp stamps it; the busy check above already ran)
     bool reg;
     WaitNode* sh = st_lookup_or_register(c, key, node, who, reg);
     if (!reg) { eff = sh; go = false; }
@@ -225,6 +227,7 @@ __device__ void async_write_t(const DevCtx& c, bool active, u64 key, WaitNode* n
     return;
   }
   const u32 lane = lane_id();
+  if (active && buffer_busy(c, node)) active = false;
   bool want = active;
   Spin sp;
   while (__any_sync(FULL, want)) {

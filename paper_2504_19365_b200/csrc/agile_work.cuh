@@ -404,6 +404,24 @@ struct LockCycleWork {
   }
 };
 
+// ------------------------------------------------------------------ BusyWork
+// AgileApi's BufferBusy (gpu_api.py:132-137, 203-204): one lane starts an async_read of a block
+// into its buffer and, without waiting, starts another transfer on the same buffer (read, or
+// write when `write` is set) — the second call must raise BufferBusy.
+struct BusyWork {
+  WaitNode* nodes;   // [1]
+  uint4* buf;        // [256]
+  u32 write;
+  __device__ void run(const DevCtx& c, u32 uidx, u32 nusers) const {
+    if (uidx != 0 || threadIdx.x >= 32) return;
+    const bool act = lane_id() == 0;
+    async_read_warp(c, act, make_key(0, 1), nodes, buf, WHO_USER, 0);
+    if (write) async_write_warp(c, act, make_key(0, 2), nodes, buf, WHO_USER, 0);
+    else async_read_warp(c, act, make_key(0, 2), nodes, buf, WHO_USER, 0);
+    wait_nodes_warp(c, act, nodes);
+  }
+};
+
 // ------------------------------------------------------------------ FlushWork
 // SoftwareCache.flush (software_cache.py:283-298) as an API call: one warp writes every MODIFIED
 // line back and waits for durability.

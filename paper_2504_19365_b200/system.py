@@ -328,6 +328,10 @@ class AgileSystem:
         LockCycle when debug_locks reports the wait-for cycle (lock_chain.py DeadlockDetector)."""
         self._check(self._lib.agile_lock_cycle_demo(self._ctx, n, mode), "lock_cycle_demo")
 
+    def buffer_busy_demo(self, write: bool = False) -> None:
+        """Re-use a buffer whose transfer is pending (raises BufferBusy, gpu_api.py:132-137)."""
+        self._check(self._lib.agile_buffer_busy_demo(self._ctx, int(write)), "buffer_busy_demo")
+
     def share_live(self) -> int:
         """ShareTable.live_entries (share_table.py:198-199); 0 when the table is disabled."""
         n = C.c_uint64(0)

@@ -37,3 +37,14 @@ def test_self_reacquire_is_a_one_cycle():
             s.lock_cycle_demo(1, 1)
         _, _, _, _, det = s.events().by_action("lock", "deadlock")[0]
         assert det[0] == 0 and det[1] == 1 and det[2] == 0   # [L0, L0]
+
+
+@pytest.mark.parametrize("write", [False, True])
+def test_pending_buffer_raises_buffer_busy(write):
+    """AgileApi._fresh_barrier (gpu_api.py:132-137): a second transfer on a buffer whose first is
+    still pending raises BufferBusy (model-mode device: the first read takes ~18 us)."""
+    from paper_2504_19365_b200.errors import BufferBusy
+    cfg = small_config(cache_lines=64, ways=8, blocks=256, emulation="model")
+    with AgileSystem(cfg, device=0) as s:
+        with pytest.raises(BufferBusy):
+            s.buffer_busy_demo(write)
