@@ -38,6 +38,7 @@ def make(cache_gib, table_gib, ew, sw):
     if side:
         cfg.engine.side_warps, cfg.service.side_warps = (int(x) for x in side.split("/"))
     cfg.debug_locks = False
+    cfg.engine.copy = os.environ.get("ENGINE_COPY", "registers")
     s = AgileSystem(cfg, device=0)
     s.fill_store(0, 5, kind="f32")
     dev = torch.device("cuda", 0)
@@ -79,7 +80,7 @@ def main():
         best = min(cos, key=lambda k: mlp_ms[k])
         bat = [gpu_zipf_batch(gen, rows_np, B, L, 1.05, True, dev) for _ in range(n)]
         sync_ms = run_pipeline(s, bat, key0, rows, graphs[best], outs, "sync")["ms"] / n
-        print(json.dumps({"engine_warps": ew, "service_warps": sw, "infra_ctas": infra, "gather_ms": g_ms,
+        print(json.dumps({"engine_copy": s.engine_copy, "side": os.environ.get("SIDE"), "engine_warps": ew, "service_warps": sw, "infra_ctas": infra, "gather_ms": g_ms,
                           "mlp_ms_by_carveout": mlp_ms, "sync_carveout": best, "sync_ms": sync_ms}), flush=True)
         for mode in modes:
             for uc in ucs:
