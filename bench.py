@@ -53,7 +53,7 @@ def _args():
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--engine-warps", type=int, default=128)
     p.add_argument("--service-warps", type=int, default=48)
-    p.add_argument("--side-ctas", type=int, default=24,
+    p.add_argument("--side-ctas", type=int, default=48,
                    help="user CTAs of the side-stream launch in the overlapped DLRM pipelines")
     p.add_argument("--side-engine-warps", type=int, default=64)
     p.add_argument("--side-service-warps", type=int, default=16)

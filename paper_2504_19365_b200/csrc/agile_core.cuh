@@ -460,12 +460,17 @@ __device__ int claim_key_warp(const DevCtx& c, u64 key, u32 pin_n, u32 who, u32&
   }
 }
 
-// Lane-parallel miss path (W <= 32): every lane with `want` claims its own key under its set's
-// lock, so the claims of one warp overlap instead of running one after another.  The loop is
-// convergent — each pass, every waiting lane tries its set lock once and the winners run the
-// O(W) claim — so no lane ever spins inside divergent code; lanes sharing a set are serialised
-// by the lock.  Same semantics as claim_key_warp (re-probe for in-flight dedup, clock victim,
-// CAS to BUSY(key)).  Returns per lane R_HIT / R_FILLING / R_MISS / R_RETRY (R_NONE if !want).
+// Lane-parallel miss path (W <= 32).  Lanes whose keys map to the same set form a group
+// (__match_any_sync on the set index); the group's lowest lane takes the set lock ONCE per pass and
+// every member then scans the set (all loads in flight at once, one round trip) and claims its own
+// victim in lane order: member r replays the policy's picks of the members before it on the same
+// scanned state (ClockPolicy.map called once per miss under the policy lock, software_cache.py:
+// 109-126, 355-371 — so the order and the victims equal the reference's sequential claims) and
+// CASes its victim to BUSY(key) in parallel with the others.  A whole group thus costs one lock
+// round trip instead of one per member.  Same semantics per key as claim_key_warp: re-probe
+// (in-flight dedup), victim by policy, MODIFIED victims written back first (R_WBEVICT).  The loop
+// is convergent; a member whose CAS lost to a hitter retries next pass.  Returns per lane R_HIT /
+// R_FILLING / R_MISS / R_RETRY / R_WBEVICT (R_NONE if !want).
 __device__ int claim_lanes(const DevCtx& c, bool want, u64 key, u32 pin_n, u32 who, u32& line, u64& word,
                            u64& victim_key) {
   const u32 lane = lane_id();
@@ -480,21 +485,23 @@ __device__ int claim_lanes(const DevCtx& c, bool want, u64 key, u32 pin_n, u32 w
   Spin sp;
   while (pending) {
     const bool mine = (pending >> lane) & 1u;
-    bool got = false;
-    bool settled = false;
-    if (mine) {
+    u32 grp = __match_any_sync(FULL, mine ? set : NONE);
+    if (!mine) grp = 0;
+    const u32 leader = grp ? (u32)(__ffs(grp) - 1) : lane;
+    int got = 0;
+    if (mine && lane == leader) {
       got = atom_cas_acquire(&c.set_lock[set], 0u, 1u) == 0u;
       if (got) lk_acquired(c, lk_set_id(c, set));
       else lk_failed(c, lk_set_id(c, set), who);
     }
+    got = __shfl_sync(FULL, got, leader) && mine;
+    bool settled = false;
+    // ---- every member of a locked group scans the set (the same state for all of them)
+    u32 avail = 0, ref1 = 0, hand = 0;
+    int found = -1;
+    u64 fw = 0;
     if (got) {
-      u32 avail = 0, ref1 = 0;
-      int found = -1;
-      u64 fw = 0;
-      // the set's clock hand rides with the scan (no extra round trip after it)
-      const u32 hand = ld_relaxed(&c.hand[set]);
-      // scan the set with every 16 B load in flight at once for W <= 32 (one round trip while
-      // the set lock is held), 8 ways per round trip beyond
+      hand = ld_relaxed(&c.hand[set]);
 #pragma unroll
       for (u32 w0 = 0; w0 < 32; w0 += 8) {
         if (w0 >= W) break;
@@ -520,6 +527,29 @@ __device__ int claim_lanes(const DevCtx& c, bool want, u64 key, u32 pin_n, u32 w
           }
         }
       }
+    }
+    // members that need a victim, in lane order; each replays the picks of the members of its own
+    // group before it (the loop is warp-uniform: every lane walks the same mask and shuffles)
+    const u32 needw = __ballot_sync(FULL, got && found < 0);
+    int v = -1;
+    u32 my_cleared = 0, nh = hand;
+    {
+      u32 av = avail, rf = ref1, hd = hand;
+      bool stop = false;
+      for (u32 m = needw; m; m &= m - 1) {
+        const u32 l = __ffs(m) - 1;
+        const u64 kl = __shfl_sync(FULL, key, l);
+        if (!got || found >= 0 || stop || !((grp >> l) & 1u)) continue;
+        u32 cl = 0, h2 = hd;
+        const int p = c.policy == POL_MODULO ? modulo_pick(c, kl, W, av) : clock_pick_vec(W, hd, av, rf, cl, h2);
+        if (l == lane) { v = p; my_cleared = cl; nh = h2; stop = true; }
+        if (p < 0) { stop = true; continue; }   // nothing left for this member or the ones after it
+        av &= ~(1u << p);                       // the victim turns BUSY
+        rf = (rf & ~cl) | (1u << p);            // swept bits cleared; on_insert sets the victim's
+        hd = h2;
+      }
+    }
+    if (got) {
       if (found >= 0) {
         u64 w2 = fw;
         if (pin_n) w2 = pin_line(c, (u32)(base + found), key, pin_n);
@@ -532,55 +562,58 @@ __device__ int claim_lanes(const DevCtx& c, bool want, u64 key, u32 pin_n, u32 w
           kind = R_RETRY;   // pin count at its cap: come back later
         }
         settled = true;
+      } else if (v < 0) {
+        kind = R_RETRY;     // every way busy/pinned: wait (any_free_wait, software_cache.py:364-365)
+        settled = true;
       } else {
-        u32 cleared = 0, nh = hand;
-        const int v = c.policy == POL_MODULO ? modulo_pick(c, key, W, avail)
-                                             : clock_pick_vec(W, hand, avail, ref1, cleared, nh);
-        if (v < 0) {
-          kind = R_RETRY;   // every way busy/pinned: wait (any_free_wait, software_cache.py:364-365)
-          settled = true;
-        } else {
-          const u64 old = ld_relaxed(&c.tags[base + v]);
-          if (tw_state(old) == ST_MODIFIED && tw_pins(old) == 0) {
-            // MODIFIED victim: write it back first, claim the freed line on the retry
-            const u64 nw = tw_make(ST_BUSY, tw_key(old), tw_ver(old) + 1, false, 0);
-            st_relaxed(&c.wl[base + v], ((u64)((tw_ver(old) + 1) & 0x1FFu)) << 55);
-            if (atom_cas_acqrel(&c.tags[base + v], old, nw) == old) {
-              for (u32 m = cleared; m; m &= m - 1) atomicAnd(&c.tags[base + (__ffs(m) - 1)], ~REF_BIT);
-              st_relaxed(&c.hand[set], nh);
-              victim_key = tw_key(old);
-              log_ev(c, who, M_CACHE, A_EVICT_WB, base + v, key_dev(victim_key), key_blk(victim_key));
-              log_state(c, who, (u32)(base + v), ST_MODIFIED, ST_BUSY, victim_key);
-              kind = R_WBEVICT;
-              line = (u32)(base + v);
-              word = nw;
-              settled = true;
-            }
-          } else if (tw_state(old) != ST_BUSY && tw_pins(old) == 0) {
-            const u64 nw = tw_make(ST_BUSY, key, tw_ver(old) + 1, true, pin_n);
-            st_relaxed(&c.wl[base + v], ((u64)((tw_ver(old) + 1) & 0x1FFu)) << 55);   // open the waiter list
-            if (atom_cas_acqrel(&c.tags[base + v], old, nw) == old) {
-              c.sig[base + v] = (unsigned short)sig16(key);   // probe hint (the tag word decides)
-              for (u32 m = cleared; m; m &= m - 1) atomicAnd(&c.tags[base + (__ffs(m) - 1)], ~REF_BIT);
-              st_relaxed(&c.hand[set], nh);
-              const u32 ost = tw_state(old);
-              if (ost == ST_READY || ost == ST_MODIFIED) {
-                victim_key = tw_key(old);
-                ++resets;
-                log_ev(c, who, M_CACHE, A_EVICT_RESET, base + v, key_dev(victim_key), key_blk(victim_key));
-                log_state(c, who, (u32)(base + v), ost, ST_INVALID, victim_key);
-              }
-              log_state(c, who, (u32)(base + v), ST_INVALID, ST_BUSY, key);
-              ++fills;
-              kind = R_MISS;
-              line = (u32)(base + v);
-              word = nw;
-              settled = true;
-            }
+        const u64 old = ld_relaxed(&c.tags[base + v]);
+        if (tw_state(old) == ST_MODIFIED && tw_pins(old) == 0) {
+          // MODIFIED victim: write it back first, claim the freed line on the retry
+          const u64 nw = tw_make(ST_BUSY, tw_key(old), tw_ver(old) + 1, false, 0);
+          st_relaxed(&c.wl[base + v], ((u64)((tw_ver(old) + 1) & 0x1FFu)) << 55);
+          if (atom_cas_acqrel(&c.tags[base + v], old, nw) == old) {
+            victim_key = tw_key(old);
+            log_ev(c, who, M_CACHE, A_EVICT_WB, base + v, key_dev(victim_key), key_blk(victim_key));
+            log_state(c, who, (u32)(base + v), ST_MODIFIED, ST_BUSY, victim_key);
+            kind = R_WBEVICT;
+            line = (u32)(base + v);
+            word = nw;
+            settled = true;
           }
-          // else: a hitter pinned/touched the victim between scan and CAS: re-evaluate next pass
+        } else if (tw_state(old) != ST_BUSY && tw_pins(old) == 0) {
+          const u64 nw = tw_make(ST_BUSY, key, tw_ver(old) + 1, true, pin_n);
+          st_relaxed(&c.wl[base + v], ((u64)((tw_ver(old) + 1) & 0x1FFu)) << 55);   // open the waiter list
+          if (atom_cas_acqrel(&c.tags[base + v], old, nw) == old) {
+            c.sig[base + v] = (unsigned short)sig16(key);   // probe hint (the tag word decides)
+            const u32 ost = tw_state(old);
+            if (ost == ST_READY || ost == ST_MODIFIED) {
+              victim_key = tw_key(old);
+              ++resets;
+              log_ev(c, who, M_CACHE, A_EVICT_RESET, base + v, key_dev(victim_key), key_blk(victim_key));
+              log_state(c, who, (u32)(base + v), ost, ST_INVALID, victim_key);
+            }
+            log_state(c, who, (u32)(base + v), ST_INVALID, ST_BUSY, key);
+            ++fills;
+            kind = R_MISS;
+            line = (u32)(base + v);
+            word = nw;
+            settled = true;
+          }
         }
+        // else: a hitter pinned/touched the victim between scan and CAS: re-evaluate next pass
+        // the sweep of this member's pick cleared these reference bits (the reference's map)
+        if (settled && c.policy != POL_MODULO)
+          for (u32 m = my_cleared; m; m &= m - 1) atomicAnd(&c.tags[base + (__ffs(m) - 1)], ~REF_BIT);
       }
+    }
+    // the group's hand follows its last settled pick; the leader releases the lock after every
+    // member's CAS (convergent point)
+    const u32 setm = __ballot_sync(FULL, got && settled && v >= 0) & grp;
+    const int lastp = setm ? 31 - __clz(setm) : -1;
+    const u32 fin_hand = __shfl_sync(FULL, nh, lastp < 0 ? lane : (u32)lastp);
+    __syncwarp();
+    if (got && lane == leader) {
+      if (lastp >= 0 && c.policy != POL_MODULO) st_relaxed(&c.hand[set], fin_hand);
       lk_released(c, lk_set_id(c, set));
       st_release(&c.set_lock[set], 0u);
     }
