@@ -1077,6 +1077,7 @@ __device__ __forceinline__ bool wait_ready_lane(const DevCtx& c, u32 line, u64 k
   return tw_state(w) == ST_READY || tw_state(w) == ST_MODIFIED;
 }
 
+template <int kSlice = 4>
 __device__ void deliver_waiters_warp(const DevCtx& c, u64 cur, u32 line);
 
 // Block write (SoftwareCache._try_write / _install_locked / _allocate_locked,
@@ -1227,14 +1228,14 @@ __device__ __forceinline__ void async_write_warp(const DevCtx& c, bool active, u
 
 // ======================================================================= K3: completion service
 
-#ifndef AGILE_SVC_SLICE
-#define AGILE_SVC_SLICE 4
-#endif
-constexpr int kSvcSlice = AGILE_SVC_SLICE;   // uint4 per lane per waiter-copy step (8 or 4)
+// uint4 per lane per waiter-copy step: 8 = every load of both pages in flight at once (the
+// register-engine infra kernel, one CTA per SM), 4 = half the registers in two steps (the bulk-
+// engine infra kernel at 128 registers, and user-side deliveries)
 
 // Waiter delivery (_drain_waiters, software_cache.py:563-570), warp-collective: every lane with a
 // closed waiter list (cur = its first node, 0 = none) of `line` copies the line into each waiting
 // AgileBuf and releases its barrier; two lists are walked per step.
+template <int kSvcSlice>
 __device__ void deliver_waiters_warp(const DevCtx& c, u64 cur, u32 line) {
   const u32 lane = lane_id();
   while (true) {
@@ -1313,6 +1314,7 @@ __device__ __forceinline__ void advance_head(const DevCtx& c, u32 q, u32 who) {
 // BUSY->READY with one release-add (fan-out: waiters poll the tag word), then the SQ head
 // advances over the completed prefix.  Only a full window rings the CQ doorbell.  off/mask is the
 // CQ's poll state, held in the owning lane's registers by service_main.
+template <int kSlice>
 __device__ u32 cq_window_pass(const DevCtx& c, u32 cq, u64& off, u32& mask, u32 who, u64& lat_acc, u32& rings) {
   const u32 lane = lane_id();
   const u32 window = c.cq_window;
@@ -1361,7 +1363,7 @@ __device__ u32 cq_window_pass(const DevCtx& c, u32 cq, u64& off, u32& mask, u32 
   __syncwarp();
   // drain waiters: copy the filled line into every waiting AgileBuf and clear its barrier while
   // the line is still BUSY (not evictable), then flip it READY (software_cache.py:538-541,563-570)
-  deliver_waiters_warp(c, (valid && cache) ? (wlh & WL_PTR_MASK) : 0ull, x.line);
+  deliver_waiters_warp<kSlice>(c, (valid && cache) ? (wlh & WL_PTR_MASK) : 0ull, x.line);
   if (valid && cache && x.kind != K_WB_EVICT) {
     const u64 ot = atom_add_release(&c.tags[x.line], 1ull << ST_SHIFT);   // BUSY -> READY
     if (tw_state(ot) != ST_BUSY) set_error(c, E_ILLEGAL_STATE, x.line, ot);
@@ -1432,6 +1434,7 @@ __device__ void drain_partial_windows(const DevCtx& c, u32 who) {
 // lane per CQ checks the next expected CQE's phase (one round trip for all owned CQs); only ready
 // CQs get a window pass.  Idle passes back off poll_ns -> idle_max_ns.
 constexpr u32 kMaxCqPerLane = 4;
+template <int kSlice = 4>
 __device__ void service_main(const DevCtx& c, const Launch& L, u32 sw) {
   const u32 lane = lane_id();
   const u32 who = WHO_SVC | sw;
@@ -1477,7 +1480,7 @@ __device__ void service_main(const DevCtx& c, const Launch& L, u32 sw) {
         u64 o = __shfl_sync(FULL, off[j], l);
         u32 m = __shfl_sync(FULL, msk[j], l);
         const u32 cq = sw + ((u32)l + 32 * j) * S;
-        got += cq_window_pass(c, cq, o, m, who, lat, rings);
+        got += cq_window_pass<kSlice>(c, cq, o, m, who, lat, rings);
         if (lane == (u32)l) { off[j] = o; msk[j] = m; }
       }
     }
@@ -2061,7 +2064,7 @@ __global__ void __launch_bounds__(kCtaThreads, kBulk ? 2 : 1)
     if (ew < c.engine_warps) engine_main<kEnginePages, kBulk>(c, ew, infra_smem);
   } else {
     const u32 sw = (blockIdx.x - c.n_engine_ctas) * kCtaWarps + warp;
-    if (sw < c.service_warps) service_main(c, L, sw);
+    if (sw < c.service_warps) service_main<kBulk ? 4 : 8>(c, L, sw);
   }
   __syncthreads();
   if (threadIdx.x == 0) {
