@@ -743,6 +743,14 @@ struct EmbBagWork {
     if (lane_id() == 0) b = (u32)atomicAdd(&c.run->work_next, (u64)kGrab);
     return __shfl_sync(FULL, b, 0);
   }
+  // sync mode: kGrab bags per grab while plenty remain, single bags once the previous grab landed
+  // in the last 2 bags per warp of the batch (a warp holding a block while the others ran dry was
+  // the kernel's tail); the grab size comes from the previous grab's index, no extra round trip
+  __device__ __forceinline__ u32 grab_adaptive(const DevCtx& c, u32 g) const {
+    u32 b = 0;
+    if (lane_id() == 0) b = (u32)atomicAdd(&c.run->work_next, (u64)g);
+    return __shfl_sync(FULL, b, 0);
+  }
   // async mode: submit the missing pages of a block's bags (first chunk of each), no waiting
   __device__ __noinline__ void prefetch_block(const DevCtx& c, u32 first, u32 nbags, u32 who, u32 sq) const {
     for (u32 k = 0; k < kGrab && first + k < nbags; ++k) {
@@ -775,6 +783,24 @@ struct EmbBagWork {
     if (prefetch_only) { run_prefetch(c, gw, who); return; }
     const u32 nbags = B * T;
     u32 misses = 0, lookups = 0;
+    if (!pd) {
+      // synchronous mode: grab just in time (no block held ahead), adaptive grab size
+      u32 n = kGrab;
+      while (!aborted(c)) {
+        const u32 first = grab_adaptive(c, n);
+        if (first >= nbags) break;
+        const u32 next_n = first + n + (u64)nwarps_total * 2 < nbags ? kGrab : 1u;
+        bool ok = true;
+        for (u32 k = 0; k < n && first + k < nbags && ok; ++k) ok = pool_bag(c, first + k, who, gw, misses, lookups);
+        if (!ok) break;
+        n = next_n;
+      }
+      if (lane_id() == 0) {
+        atomicAdd(&lookups_miss[0], (u64)lookups);
+        atomicAdd(&lookups_miss[1], (u64)misses);
+      }
+      return;
+    }
     u32 cur = grab_block(c);
     if (pd && cur < nbags) prefetch_block(c, cur, nbags, who, gw);
     u32 pass = 0;
