@@ -966,26 +966,46 @@ struct EmbBagWork {
         line = rs.line;
         word = rs.word;
       }
-      // sum the chunk's rows in lookup order, lane owns dims [4*lane, 4*lane+4): 8 row loads
-      // (16 B/lane, 512 B coalesced each at D = 128) in flight per step
-      const u64 rowaddr = a ? (u64)(uintptr_t)(line_ptr(c, line) + off) : 0ull;
+      // sum the chunk's rows in lookup order, lane owns dims [4*lane, 4*lane+4) (a lane past D/4
+      // reads a copy of its row's first dims and never stores): the active lookups are compacted
+      // to lanes 0..n-1 once (a prefix already is), then rows are loaded 8, then 4, then 1 at a
+      // time, 16 B/lane (512 B coalesced at D = 128) — no zero-padded loads, no per-row lane
+      // search; only the row's 32-bit slot index in the cache's row space is shuffled
+      const u32 rsh = kBlockShift - rows_per_page_shift;   // log2(row bytes)
+      u32 rs = a ? ((line << rows_per_page_shift) | (off >> rsh)) : 0u;
+      const u32 na = __popc(am);
+      if (am & (am + 1u)) rs = __shfl_sync(FULL, rs, lane < na ? __fns(am, 0, lane + 1) : 0u);
+      const uint8_t* rowbase = c.lines + ((lane * 16u) & ((1u << rsh) - 1u));
       u32 dep = 0;
       const u64 pol = row_policy();
-      for (u32 m = am; m; ) {
+      u32 r0 = 0;
+      for (; r0 + 8 <= na; r0 += 8) {
         float4 v[8];
 #pragma unroll
-        for (u32 j = 0; j < 8; ++j) {
-          const int src = m ? __ffs(m) - 1 : 0;
-          const u64 ra = __shfl_sync(FULL, rowaddr, src);
-          v[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (m && dims) v[j] = ld_row(reinterpret_cast<const float4*>(ra) + lane, pol);
-          m &= m - 1;
-        }
+        for (u32 j = 0; j < 8; ++j)
+          v[j] = ld_row(reinterpret_cast<const float4*>(rowbase + ((u64)__shfl_sync(FULL, rs, r0 + j) << rsh)), pol);
 #pragma unroll
         for (u32 j = 0; j < 8; ++j) {
           a0 += (double)v[j].x; a1 += (double)v[j].y; a2 += (double)v[j].z; a3 += (double)v[j].w;
           dep |= __float_as_uint(v[j].x) | __float_as_uint(v[j].w);
         }
+      }
+      if (r0 + 4 <= na) {
+        float4 v[4];
+#pragma unroll
+        for (u32 j = 0; j < 4; ++j)
+          v[j] = ld_row(reinterpret_cast<const float4*>(rowbase + ((u64)__shfl_sync(FULL, rs, r0 + j) << rsh)), pol);
+#pragma unroll
+        for (u32 j = 0; j < 4; ++j) {
+          a0 += (double)v[j].x; a1 += (double)v[j].y; a2 += (double)v[j].z; a3 += (double)v[j].w;
+          dep |= __float_as_uint(v[j].x) | __float_as_uint(v[j].w);
+        }
+        r0 += 4;
+      }
+      for (; r0 < na; ++r0) {
+        const float4 v = ld_row(reinterpret_cast<const float4*>(rowbase + ((u64)__shfl_sync(FULL, rs, r0) << rsh)), pol);
+        a0 += (double)v.x; a1 += (double)v.y; a2 += (double)v.z; a3 += (double)v.w;
+        dep |= __float_as_uint(v.x) | __float_as_uint(v.w);
       }
       // seqlock validation, once per chunk: the tag re-read's address depends on every row value
       // of the warp (redux over the lanes), so it is issued after all of them were loaded

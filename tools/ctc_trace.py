@@ -15,7 +15,7 @@ cfg.epochs = 4
 for mode in (False, True):
     s = AgileSystem(cfg.system, recorder=TraceRecorder(), device=0)
     keys = request_keys(cfg)
-    r = s.run_reads(keys, cfg.tasks, cfg.reads_per_task, cfg.epochs, mode, 200000)
+    r = s.run_reads(keys, cfg.tasks, cfg.reads_per_task, cfg.epochs, mode, int(os.environ.get("COMPUTE_NS", "0")))
     ev = s.events().records
     stages = defaultdict(dict)
     seen = defaultdict(int)
@@ -35,6 +35,21 @@ for mode in (False, True):
         d = [v[b] - v[a] for v in stages.values() if a in v and b in v]
         if d:
             print(f"  {a}->{b}: mean {np.mean(d):.0f} p50 {np.median(d):.0f} max {np.max(d):.0f} n {len(d)}")
+    # per-epoch timeline (commands grouped by enqueue order, 128 per epoch)
+    cmds = sorted((v for v in stages.values() if "enqueue" in v), key=lambda v: v["enqueue"])
+    per = cfg.tasks * cfg.reads_per_task
+    prev_end = None
+    for e in range(len(cmds) // per):
+        g = cmds[e * per:(e + 1) * per]
+        col = lambda k: sorted(v[k] for v in g if k in v)
+        enq, fet, com, post, proc = (col(k) for k in names)
+        row = {"first_enq": enq[0], "last_enq": enq[-1] - enq[0], "first_fetch": fet[0] - enq[0],
+               "16th_fetch": fet[min(15, len(fet) - 1)] - enq[0], "last_complete": com[-1] - enq[0],
+               "last_post": post[-1] - enq[0], "last_process": proc[-1] - enq[0]}
+        if prev_end is not None:
+            row["gap_from_prev_last_process"] = enq[0] - prev_end
+        prev_end = proc[-1]
+        print("  epoch", e, row)
     enq = sorted(v["enqueue"] for v in stages.values() if "enqueue" in v)
     print("  enqueue times (first 5 / per-epoch spans):", enq[:3], [enq[i * 128 + 127] - enq[i * 128] for i in range(len(enq) // 128)])
     s.close()
