@@ -1208,6 +1208,7 @@ static int embbag_launch(agile_ctx* ctx, EmbBagWork& w, const int64_t* idx, cons
   w.out = out;
   w.lookups_miss = reinterpret_cast<u64*>(counters);
   w.B = B; w.T = T; w.L = offsets ? 0 : L; w.D = D;
+  w.t_magic = T > 1 ? ~0ull / T + 1 : 0;
   w.pd = pd;
   uint32_t rpp = kBlockBytes / (D * 4), sh = 0;
   while ((1u << sh) < rpp) ++sh;

@@ -689,6 +689,12 @@ struct EmbBagWork {
   u32 rows_per_page_shift;     // log2(4096 / (D*4))
   u32 nwarps_total;
   u32 prefetch_only;           // 1: pull every page of the batch toward the cache, no pooling
+  u64 t_magic;                 // floor(2^64 / T) + 1: bag / T = umul64hi(bag, t_magic) for T > 1
+
+  // bag -> (sample b, table t) without an integer division (exact for bag < 2^32)
+  __device__ __forceinline__ u32 bag_sample(u32 bag) const {
+    return T == 1 ? bag : (u32)__umul64hi((u64)bag, t_magic);
+  }
 
   __device__ __forceinline__ TabDesc tab(u32 t) const {
     TabDesc d;
@@ -755,7 +761,7 @@ struct EmbBagWork {
   __device__ __noinline__ void prefetch_block(const DevCtx& c, u32 first, u32 nbags, u32 who, u32 sq) const {
     for (u32 k = 0; k < kGrab && first + k < nbags; ++k) {
       const u32 bag = first + k;
-      const u32 t = bag % T;
+      const u32 t = bag - bag_sample(bag) * T;
       const TabDesc td = tab(t);
       u64 start; u32 n;
       bag_span(bag, start, n);
@@ -838,7 +844,7 @@ struct EmbBagWork {
         const u32 first = grab_block(c);
         if (first >= nbags) break;
         for (u32 k = 0; k < kGrab && first + k < nbags; ++k) {
-          const u32 bag = first + k, t = bag % T;
+          const u32 bag = first + k, t = bag - bag_sample(bag) * T;
           const TabDesc td = tab(t);
           u64 start; u32 n;
           bag_span(bag, start, n);
@@ -921,51 +927,31 @@ struct EmbBagWork {
     return res;
   }
 
-  // pool one bag (fp64, 4 dims per lane) and store it; false when the run aborts.  A chunk whose
-  // validation fails restarts the bag (rare: a page was evicted while the warp read it); after 4
-  // failures the bag is pooled row by row, each row validated on its own.
-  __device__ bool pool_bag(const DevCtx& c, u32 bag, u32 who, u32 gw, u32& misses, u32& lookups) const {
+  // One chunk (<= 32 lookups from position c0) of a bag, summed into a0..a3 in lookup order:
+  // probe, miss path, rows, seqlock validation.  Returns 0 ok, 1 validation failed (a page changed
+  // identity while the warp read it: the caller restarts the bag), -1 the run aborts.
+  __device__ __forceinline__ int pool_chunk(const DevCtx& c, const TabDesc& td, u32 t, u64 start, u32 c0, u32 n,
+                                            u32 who, u32 gw, bool first_visit, u32& misses, u32& lookups,
+                                            double& a0, double& a1, double& a2, double& a3) const {
     const u32 lane = lane_id();
-    const u32 b = bag / T, t = bag - b * T;
-    const TabDesc td = tab(t);
-    u64 start; u32 n;
-    bag_span(bag, start, n);
-    const bool dims = lane * 4 < D;
-    double a0, a1, a2, a3;
-    u32 fails = 0;
-    u32 counted = 0;   // chunks below this position were counted (a restart does not count twice)
-    Spin rsp;
-  restart:
-    a0 = a1 = a2 = a3 = 0.0;
-    for (u32 c0 = 0; c0 < n; c0 += 32) {
-      const bool lact = c0 + lane < n;
-      const long long r = lact ? __ldg(idx + start + c0 + lane) : 0ll;
-      u64 key = 0; u32 off = 0;
-      const bool a = lookup_key(c, td, lact, r, t, key, off);
-      const u32 am = __ballot_sync(FULL, a);
-      const bool first_visit = c0 >= counted;
-      if (first_visit) {
-        lookups += __popc(am);
-        counted = c0 + 32;
-      }
-      if (fails >= 4) {
-        const Acc4 r4 = pool_rows_one_by_one(c, am, key, off, who, gw, make_acc4(a0, a1, a2, a3));
-        if (!r4.ok) return false;
-        a0 = r4.v[0]; a1 = r4.v[1]; a2 = r4.v[2]; a3 = r4.v[3];
-        continue;
-      }
-      u32 line = NONE; u64 word = 0;
-      probe_lanes<true>(c, a, key, line, word);
-      const bool ready = a && line != NONE && (tw_state(word) == ST_READY || tw_state(word) == ST_MODIFIED);
-      if (ready && !tw_ref(word)) atomicOr(&c.tags[line], REF_BIT);   // on_hit
-      const u32 need = __ballot_sync(FULL, a && !ready);
-      if (need) {
-        if (first_visit) misses += __popc(need);
-        const Resolved rs = resolve_misses(c, need, key, who, gw, line, word);
-        if (!rs.ok) return false;
-        line = rs.line;
-        word = rs.word;
-      }
+    const bool lact = c0 + lane < n;
+    const long long r = lact ? __ldg(idx + start + c0 + lane) : 0ll;
+    u64 key = 0; u32 off = 0;
+    const bool a = lookup_key(c, td, lact, r, t, key, off);
+    const u32 am = __ballot_sync(FULL, a);
+    if (first_visit) lookups += __popc(am);
+    u32 line = NONE; u64 word = 0;
+    probe_lanes<true>(c, a, key, line, word);
+    const bool ready = a && line != NONE && (tw_state(word) == ST_READY || tw_state(word) == ST_MODIFIED);
+    if (ready && !tw_ref(word)) atomicOr(&c.tags[line], REF_BIT);   // on_hit
+    const u32 need = __ballot_sync(FULL, a && !ready);
+    if (need) {
+      if (first_visit) misses += __popc(need);
+      const Resolved rv = resolve_misses(c, need, key, who, gw, line, word);
+      if (!rv.ok) return -1;
+      line = rv.line;
+      word = rv.word;
+    }
       // sum the chunk's rows in lookup order, lane owns dims [4*lane, 4*lane+4) (a lane past D/4
       // reads a copy of its row's first dims and never stores): the active lookups are compacted
       // to lanes 0..n-1 once (a prefix already is), then rows are loaded 8, then 4, then 1 at a
@@ -975,7 +961,8 @@ struct EmbBagWork {
       u32 rs = a ? ((line << rows_per_page_shift) | (off >> rsh)) : 0u;
       const u32 na = __popc(am);
       if (am & (am + 1u)) rs = __shfl_sync(FULL, rs, lane < na ? __fns(am, 0, lane + 1) : 0u);
-      const uint8_t* rowbase = c.lines + ((lane * 16u) & ((1u << rsh) - 1u));
+      const u32 rb = 1u << rsh;
+      const uint8_t* rowbase = c.lines + ((lane * 16u) & (rb - 1u));
       u32 dep = 0;
       const u64 pol = row_policy();
       u32 r0 = 0;
@@ -983,50 +970,108 @@ struct EmbBagWork {
         float4 v[8];
 #pragma unroll
         for (u32 j = 0; j < 8; ++j)
-          v[j] = ld_row(reinterpret_cast<const float4*>(rowbase + ((u64)__shfl_sync(FULL, rs, r0 + j) << rsh)), pol);
+          v[j] = ld_row(reinterpret_cast<const float4*>(rowbase + (u64)__shfl_sync(FULL, rs, r0 + j) * rb), pol);
 #pragma unroll
         for (u32 j = 0; j < 8; ++j) {
           a0 += (double)v[j].x; a1 += (double)v[j].y; a2 += (double)v[j].z; a3 += (double)v[j].w;
-          dep |= __float_as_uint(v[j].x) | __float_as_uint(v[j].w);
+          dep |= __float_as_uint(v[j].x);   // the 16 B load returns at once
         }
       }
       if (r0 + 4 <= na) {
         float4 v[4];
 #pragma unroll
         for (u32 j = 0; j < 4; ++j)
-          v[j] = ld_row(reinterpret_cast<const float4*>(rowbase + ((u64)__shfl_sync(FULL, rs, r0 + j) << rsh)), pol);
+          v[j] = ld_row(reinterpret_cast<const float4*>(rowbase + (u64)__shfl_sync(FULL, rs, r0 + j) * rb), pol);
 #pragma unroll
         for (u32 j = 0; j < 4; ++j) {
           a0 += (double)v[j].x; a1 += (double)v[j].y; a2 += (double)v[j].z; a3 += (double)v[j].w;
-          dep |= __float_as_uint(v[j].x) | __float_as_uint(v[j].w);
+          dep |= __float_as_uint(v[j].x);   // the 16 B load returns at once
         }
         r0 += 4;
       }
       for (; r0 < na; ++r0) {
-        const float4 v = ld_row(reinterpret_cast<const float4*>(rowbase + ((u64)__shfl_sync(FULL, rs, r0) << rsh)), pol);
+        const float4 v = ld_row(reinterpret_cast<const float4*>(rowbase + (u64)__shfl_sync(FULL, rs, r0) * rb), pol);
         a0 += (double)v.x; a1 += (double)v.y; a2 += (double)v.z; a3 += (double)v.w;
-        dep |= __float_as_uint(v.x) | __float_as_uint(v.w);
+        dep |= __float_as_uint(v.x);
       }
       // seqlock validation, once per chunk: the tag re-read's address depends on every row value
       // of the warp (redux over the lanes), so it is issued after all of them were loaded
       const u64 z = dep_zero(__reduce_or_sync(FULL, dep));
       bool bad = false;
       if (a) bad = ((ld_relaxed(&c.tags[line] + z) ^ word) & IDENT_MASK) != 0;
-      if (__any_sync(FULL, bad)) {
-        ++fails;
-        if (!rsp.again(c, 256, __LINE__ + 100000 * SPIN_FILE_ID)) return false;
-        goto restart;
-      }
-    }
+      return __any_sync(FULL, bad) ? 1 : 0;
+  }
+
+  __device__ __forceinline__ void store_bag(u32 b, const TabDesc& td, double a0, double a1, double a2,
+                                            double a3) const {
+    const u32 lane = lane_id();
+    if (lane * 4 >= D) return;
     uint8_t* o = out + (u64)b * out_row_bytes + td.out_off;
-    if (dims) {
-      if (td.flags & TAB_PARTIAL_F64) {
-        reinterpret_cast<double2*>(o)[2 * lane] = make_double2(a0, a1);
-        reinterpret_cast<double2*>(o)[2 * lane + 1] = make_double2(a2, a3);
-      } else {
-        reinterpret_cast<float4*>(o)[lane] = make_float4((float)a0, (float)a1, (float)a2, (float)a3);
-      }
+    if (td.flags & TAB_PARTIAL_F64) {
+      reinterpret_cast<double2*>(o)[2 * lane] = make_double2(a0, a1);
+      reinterpret_cast<double2*>(o)[2 * lane + 1] = make_double2(a2, a3);
+    } else {
+      reinterpret_cast<float4*>(o)[lane] = make_float4((float)a0, (float)a1, (float)a2, (float)a3);
     }
+  }
+
+  // pool one bag (fp64, 4 dims per lane) and store it; false when the run aborts.  Bags of up to
+  // 32 lookups take one chunk pass with no restart state held (the hot path); a failed validation
+  // or a longer bag goes to pool_bag_slow.
+  __device__ __forceinline__ bool pool_bag(const DevCtx& c, u32 bag, u32 who, u32 gw, u32& misses,
+                                           u32& lookups) const {
+    const u32 b = bag_sample(bag), t = bag - b * T;
+    const TabDesc td = tab(t);
+    u64 start; u32 n;
+    bag_span(bag, start, n);
+    if (n > 32) return pool_bag_slow(c, bag, who, gw, misses, lookups, 0u);
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    const int rc = pool_chunk(c, td, t, start, 0u, n, who, gw, true, misses, lookups, a0, a1, a2, a3);
+    if (rc < 0) return false;
+    if (rc > 0) return pool_bag_slow(c, bag, who, gw, misses, lookups, 32u);
+    store_bag(b, td, a0, a1, a2, a3);
+    return true;
+  }
+
+  // The general bag: chunks of 32 lookups; a chunk whose validation fails restarts the bag (rare: a
+  // page was evicted while the warp read it); after 4 failures the bag is pooled row by row, each
+  // row validated on its own.  `counted`: lookups below this position were already counted.
+  __device__ __noinline__ bool pool_bag_slow(const DevCtx& c, u32 bag, u32 who, u32 gw, u32& misses,
+                                             u32& lookups, u32 counted) const {
+    const u32 b = bag_sample(bag), t = bag - b * T;
+    const TabDesc td = tab(t);
+    u64 start; u32 n;
+    bag_span(bag, start, n);
+    double a0, a1, a2, a3;
+    u32 fails = counted ? 1u : 0u;
+    Spin rsp;
+  restart:
+    a0 = a1 = a2 = a3 = 0.0;
+    for (u32 c0 = 0; c0 < n; c0 += 32) {
+      const bool first_visit = c0 >= counted;
+      if (fails >= 4) {
+        const bool lact = c0 + lane_id() < n;
+        const long long r = lact ? __ldg(idx + start + c0 + lane_id()) : 0ll;
+        u64 key = 0; u32 off = 0;
+        const bool a = lookup_key(c, td, lact, r, t, key, off);
+        const u32 am = __ballot_sync(FULL, a);
+        if (first_visit) lookups += __popc(am);
+        const Acc4 r4 = pool_rows_one_by_one(c, am, key, off, who, gw, make_acc4(a0, a1, a2, a3));
+        if (!r4.ok) return false;
+        a0 = r4.v[0]; a1 = r4.v[1]; a2 = r4.v[2]; a3 = r4.v[3];
+      } else {
+        const int rc = pool_chunk(c, td, t, start, c0, n, who, gw, first_visit, misses, lookups, a0, a1, a2, a3);
+        if (rc < 0) return false;
+        if (rc > 0) {
+          if (first_visit) counted = c0 + 32;
+          ++fails;
+          if (!rsp.again(c, 256, __LINE__ + 100000 * SPIN_FILE_ID)) return false;
+          goto restart;
+        }
+      }
+      if (first_visit) counted = c0 + 32;
+    }
+    store_bag(b, td, a0, a1, a2, a3);
     return true;
   }
 
