@@ -74,16 +74,21 @@ __device__ __forceinline__ bool probe_key_warp(const DevCtx& c, u64 key, u32& li
 // of W (one lane per way) and each group resolves one key per round with a ballot.  Returns per
 // lane the matching (line, word) or line = NONE.  Used for W <= 32; larger W falls back to the
 // per-key probe.
+// bit 15 / bit 31 set where the low / high 16-bit half of w equals pat's (exact: the 15-bit add
+// cannot carry into the next half)
+__device__ __forceinline__ u32 sig_zero2(u32 w, u32 pat) {
+  const u32 x = w ^ pat;
+  return ~(((x & 0x7FFF7FFFu) + 0x7FFF7FFFu) | x) & 0x80008000u;
+}
+// bit 7 of each byte of y (bytes 0 or 0x80) -> a 4-bit mask (the multiply's partial products
+// land on distinct bits, so nothing carries into bits 28..31)
+__device__ __forceinline__ u32 byte_flags4(u32 y) { return (((y >> 7) & 0x01010101u) * 0x10204080u) >> 28; }
 __device__ __forceinline__ u32 sig_match8(uint4 v, u32 pat) {
-  // 8 x 16-bit signatures -> 8-bit match mask
-  u32 m = 0;
-  const u32 w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const u32 r = __vcmpeq2(w[i], pat);
-    m |= ((r & 1u) | ((r >> 15) & 2u)) << (2 * i);
-  }
-  return m;
+  // 8 x 16-bit signatures -> 8-bit match mask (way 2i = low half of word i), SWAR on the integer
+  // pipe: 4 ops per word to flag equal halves, a byte permute to gather the 8 flags, one multiply
+  // per 4 flags to pack them
+  const u32 z0 = sig_zero2(v.x, pat), z1 = sig_zero2(v.y, pat), z2 = sig_zero2(v.z, pat), z3 = sig_zero2(v.w, pat);
+  return byte_flags4(__byte_perm(z0, z1, 0x7531)) | (byte_flags4(__byte_perm(z2, z3, 0x7531)) << 4);
 }
 
 // Probe result of one lane (line = NONE: not resident)
