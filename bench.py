@@ -189,6 +189,42 @@ def _cpu_port(plan, rank, lines, scatter, threads, seconds, max_steps=400, warm_
     return (done / tsum if tsum > 0 else 0.0), desc, cc
 
 
+def _ctc_gpu(device):
+    """configs[0] on the B200: the reference's default CTC sweep (16 tasks x 8 reads x 16 epochs, SSD
+    latency model, 16 channels) through the B200 path (bench/ctc.py); device-timed epochs."""
+    from paper_2504_19365_b200.bench.ctc import run_ctc_sweep
+    from paper_2504_19365_b200.cli import build_config
+    cfg = build_config("ctc_sweep")
+    t0 = time.perf_counter()
+    r = run_ctc_sweep(cfg)
+    return {"what": "reference default ctc_sweep config on the B200 path (device %globaltimer epochs; the "
+                    "reference's criterion 4 asks speedup(0) in [0.95, 1.1] and a peak >= 1.7 at ctc 0.75-1.0)",
+            "rows": [{"ctc": c, "t_sync_ns": ts, "t_async_ns": ta, "speedup": sp} for c, ts, ta, sp, _ in r.rows],
+            "comm_per_epoch_ns": r.info.get("comm_per_epoch_ns"), "wall_s": time.perf_counter() - t0}
+
+
+def _ctc_reference():
+    """configs[0] on the reference simulator from baseline/_ref (its own ctc_sweep, simulated ns, one
+    host core); None when the package is not installed."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "agile_sim")):
+        return None
+    sys.path.insert(0, ref)
+    try:
+        from agile_sim.bench.ctc import run_ctc_sweep
+        from agile_sim.cli import build_config
+        cfg = build_config("ctc_sweep")
+        t0 = time.perf_counter()
+        r = run_ctc_sweep(cfg)
+        return {"what": "reference simulator ctc_sweep, default config (simulated ns), 1 host core",
+                "rows": [{"ctc": c, "t_sync_ns": ts, "t_async_ns": ta, "speedup": sp} for c, ts, ta, sp, _ in r.rows],
+                "wall_s": time.perf_counter() - t0, "cores": 1}
+    except Exception as e:   # the simulator is the reference's; report, do not fail the arm
+        return {"error": repr(e)[:200]}
+    finally:
+        sys.path.remove(ref)
+
+
 def _reference_simulator(seconds=8.0):
     """The reference simulator itself (agile_sim from baseline/_ref, installed from the reference
     package with pip --target; the box has no /root/reference) running the same paged embedding-bag
@@ -291,6 +327,9 @@ def run_reference(args):
     sim = _reference_simulator()
     if sim is not None:
         line["reference_simulator"] = sim
+    ctc = _ctc_reference()
+    if ctc is not None:
+        line["ctc"] = ctc
     print(json.dumps(line), flush=True)
 
 
@@ -632,9 +671,11 @@ def main():
             line["cpu_gpu_max_abs_diff"] = float(np.max(np.abs(o_cpu - o_gpu)))
             line["cpu_baseline"] = {"value": cpu_v, "unit": "lookups/s", "cores": threads, "kind": "port",
                                     "sample": cpu_desc}
+    system.close()
+    if rank == 0 and world == 1 and not args.quick:
+        line["ctc"] = _ctc_gpu(dev)
     if rank == 0:
         print(json.dumps(line), flush=True)
-    system.close()
     if world > 1:
         dist.destroy_process_group()
 

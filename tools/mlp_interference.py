@@ -54,6 +54,10 @@ fresh = [gpu_zipf_batch(gen, rows_np, B, L, 1.05, True, dev) for _ in range(8)]
 res["beside_prefetch_16ctas"] = mlp_beside(lambda: [s.embbag_prefetch(x, key0, rows, D, cnt, 16, stream=side.cuda_stream)
                                                     for x in fresh])
 res["alone_again"] = mlp_beside(lambda: None)
+# the host link loaded by the copy engines only (no SM work beside the MLPs): pinned H2D copies
+pin = torch.empty(64 << 20, dtype=torch.uint8).pin_memory()
+dst = torch.empty(64 << 20, dtype=torch.uint8, device=dev)
+res["beside_h2d_copies"] = mlp_beside(lambda: [dst.copy_(pin, non_blocking=True) for _ in range(12)])
 res["carveout"] = CARVE
 res["side"] = os.environ.get("SIDE")
 # a side launch of idle CTAs only (the infra grid of a run with one user CTA that has no work)
