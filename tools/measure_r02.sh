@@ -44,7 +44,7 @@ fi
 if want sanitizer; then   # profiles/sanitizer_r02.txt
   timeout 1500 compute-sanitizer --tool memcheck --leak-check no --error-exitcode 9 \
     python -m pytest -q -m gpu -x tests/test_gpu_cache.py tests/test_gpu_array_get.py \
-    "tests/test_gpu_queue.py::test_two_level_coalescing" "tests/test_gpu_embbag.py::test_embbag_shapes" \
+    "tests/test_gpu_queue.py::test_two_level_coalescing" tests/test_gpu_embbag.py tests/test_gpu_dlrm_shard.py \
     tests/test_gpu_coherence.py::test_enabled_table_masks_the_hazard_on_every_seed > gpurun_out/sanitizer.txt 2>&1
   echo "memcheck rc=$?"
 fi
