@@ -534,23 +534,34 @@ __device__ int claim_lanes(const DevCtx& c, bool want, u64 key, u32 pin_n, u32 w
       }
     }
     // members that need a victim, in lane order; each replays the picks of the members of its own
-    // group before it (the loop is warp-uniform: every lane walks the same mask and shuffles)
+    // group before it.  All groups replay in parallel, one member rank per step: in step r every
+    // lane of a group computes the pick of its group's r-th member on the group's (replicated)
+    // state, so a pass costs max-group-size picks instead of one per needing lane of the warp.
     const u32 needw = __ballot_sync(FULL, got && found < 0);
     int v = -1;
     u32 my_cleared = 0, nh = hand;
     {
+      const u32 gneed = got ? (needw & grp) : 0u;
+      const u32 myrank = __popc(gneed & lanemask_lt());
+      const u32 gsz = __popc(gneed);
       u32 av = avail, rf = ref1, hd = hand;
       bool stop = false;
-      for (u32 m = needw; m; m &= m - 1) {
-        const u32 l = __ffs(m) - 1;
-        const u64 kl = __shfl_sync(FULL, key, l);
-        if (!got || found >= 0 || stop || !((grp >> l) & 1u)) continue;
+      for (u32 r = 0; __any_sync(FULL, r < gsz); ++r) {
+        u64 kr = 0;
+        if (c.policy == POL_MODULO)   // the key of the group's r-th member (warp-uniform branch)
+          kr = __shfl_sync(FULL, key, r < gsz ? __fns(gneed, 0, (int)r + 1) : lane);
+        if (r >= gsz || stop) continue;
         u32 cl = 0, h2 = hd;
-        const int p = c.policy == POL_MODULO ? modulo_pick(c, kl, W, av) : clock_pick_vec(W, hd, av, rf, cl, h2);
-        if (l == lane) { v = p; my_cleared = cl; nh = h2; stop = true; }
-        if (p < 0) { stop = true; continue; }   // nothing left for this member or the ones after it
-        av &= ~(1u << p);                       // the victim turns BUSY
-        rf = (rf & ~cl) | (1u << p);            // swept bits cleared; on_insert sets the victim's
+        int pk;
+        if (c.policy == POL_MODULO) {
+          pk = modulo_pick(c, kr, W, av);
+        } else {
+          pk = clock_pick_vec(W, hd, av, rf, cl, h2);
+        }
+        if (myrank == r && found < 0) { v = pk; my_cleared = cl; nh = h2; }
+        if (pk < 0) { stop = true; continue; }   // nothing left for this member or the ones after it
+        av &= ~(1u << pk);                       // the victim turns BUSY
+        rf = (rf & ~cl) | (1u << pk);            // swept bits cleared; on_insert sets the victim's
         hd = h2;
       }
     }
@@ -680,22 +691,29 @@ __device__ bool ring_doorbell_until(const DevCtx& c, u32 q, u64 target, u32 who)
       const u64 old = ld_relaxed(&s->db);
       u64 v = old;
       while (true) {
-        const u64 vi = v + lane;
-        const u32 idx = sq_slot_index(c, q, vi);
-        bool upd = false;
-        if (vi < old + D) upd = ld_acquire(&c.sq_state[idx]) == SQ_UPDATED;
-        const u32 b = __ballot_sync(FULL, upd);
-        const u32 prefix = (~b) ? (u32)(__ffs(~b) - 1) : 32u;
-        if (lane < prefix) {
-          // per-lane acq_rel CAS: each lane's flip is itself a release (a relaxed store made
-          // visible only through lane 0's doorbell release is not cumulative in practice — the
-          // engine then saw the doorbell before the ISSUED word)
-          if (atom_cas_acqrel(&c.sq_state[idx], SQ_UPDATED, SQ_ISSUED) != SQ_UPDATED)
-            set_error(c, E_PROTOCOL, q, vi);
-          log_ev(c, who, M_NVME, A_SQE_ISSUED, q, vi & (D - 1), vi & (D - 1));
+        // 64 entries per round trip (two per lane): a full warp's submission (32 UPDATED
+        // entries) is found and bounded in one scan instead of two
+        const u64 vi0 = v + lane, vi1 = v + 32 + lane;
+        const u32 idx0 = sq_slot_index(c, q, vi0), idx1 = sq_slot_index(c, q, vi1);
+        bool upd0 = false, upd1 = false;
+        if (vi0 < old + D) upd0 = ld_acquire(&c.sq_state[idx0]) == SQ_UPDATED;
+        if (vi1 < old + D) upd1 = ld_acquire(&c.sq_state[idx1]) == SQ_UPDATED;
+        const u32 b0 = __ballot_sync(FULL, upd0), b1 = __ballot_sync(FULL, upd1);
+        const u32 prefix = (~b0) ? (u32)(__ffs(~b0) - 1) : ((~b1) ? 32u + (u32)(__ffs(~b1) - 1) : 64u);
+#pragma unroll
+        for (u32 h = 0; h < 2; ++h) {
+          const u64 vi = h ? vi1 : vi0;
+          if (32 * h + lane < prefix) {
+            // per-lane acq_rel CAS: each lane's flip is itself a release (a relaxed store made
+            // visible only through lane 0's doorbell release is not cumulative in practice — the
+            // engine then saw the doorbell before the ISSUED word)
+            if (atom_cas_acqrel(&c.sq_state[h ? idx1 : idx0], SQ_UPDATED, SQ_ISSUED) != SQ_UPDATED)
+              set_error(c, E_PROTOCOL, q, vi);
+            log_ev(c, who, M_NVME, A_SQE_ISSUED, q, vi & (D - 1), vi & (D - 1));
+          }
         }
         v += prefix;
-        if (prefix < 32) break;
+        if (prefix < 64) break;
       }
       __syncwarp();
       if (lane == 0) {
@@ -1068,7 +1086,7 @@ __device__ bool wait_nodes_warp(const DevCtx& c, bool active, const WaitNode* no
   Spin sp;
   while (pending) {
     pending &= ~poll_nodes_warp((pending >> lane_id()) & 1u, node);
-    if (pending && !sp.again(c, 1024, __LINE__ + 100000 * SPIN_FILE_ID)) return false;
+    if (pending && !sp.again(c, 256, __LINE__ + 100000 * SPIN_FILE_ID)) return false;
   }
   return true;
 }
@@ -1239,78 +1257,105 @@ __device__ __forceinline__ void async_write_warp(const DevCtx& c, bool active, u
 
 // Waiter delivery (_drain_waiters, software_cache.py:563-570), warp-collective: every lane with a
 // closed waiter list (cur = its first node, 0 = none) of `line` copies the line into each waiting
-// AgileBuf and releases its barrier; two lists are walked per step.
+// AgileBuf and releases its barrier.  Rounds: every lane loads its current node (destination and
+// link: one round trip for the whole warp), the pages of all lanes' current nodes move kNP at a
+// time (4 pages in flight per step with 8-uint4 slices — 128 registers of data, like the engine's
+// page moves; 2 with 4-uint4 slices), then ONE fence and the barriers of the round are released.
+// A window of single-waiter completions is thus delivered in one node round trip, ceil(n / kNP)
+// page round trips and one fence.
 template <int kSvcSlice>
 __device__ void deliver_waiters_warp(const DevCtx& c, u64 cur, u32 line) {
+  constexpr int kNP = kSvcSlice >= 8 ? 4 : 2;
   const u32 lane = lane_id();
   while (true) {
-    u32 cb = __ballot_sync(FULL, cur != 0);
-    if (!cb) break;
-    const int l0 = __ffs(cb) - 1;
-    cb &= cb - 1;
-    const int l1 = cb ? __ffs(cb) - 1 : -1;
-    const int s1 = l1 < 0 ? l0 : l1;
-    const uint4* src0 = reinterpret_cast<const uint4*>(line_ptr(c, __shfl_sync(FULL, line, l0)));
-    const uint4* src1 = reinterpret_cast<const uint4*>(line_ptr(c, __shfl_sync(FULL, line, s1)));
-    WaitNode* n0 = reinterpret_cast<WaitNode*>(__shfl_sync(FULL, cur, l0) << 4);
-    WaitNode* n1 = reinterpret_cast<WaitNode*>(__shfl_sync(FULL, cur, s1) << 4);
+    const u32 all = __ballot_sync(FULL, cur != 0);
+    if (!all) break;
+    WaitNode* me = reinterpret_cast<WaitNode*>(cur << 4);
     {
       // a waiter list only ever links this run's WaitNodes: anything else is a corrupted list
-      const u64 a0 = (u64)(uintptr_t)n0, a1 = (u64)(uintptr_t)n1;
-      const bool bad = a0 < c.nodes_lo || a0 >= c.nodes_hi || a1 < c.nodes_lo || a1 >= c.nodes_hi;
-      if (bad) {
-        if (lane == 0) set_error(c, E_ILLEGAL_STATE, a0, 0xD0000000ull | (u64)__LINE__);
-        if ((int)lane == l0 || (int)lane == l1) cur = 0;
+      const u64 a = (u64)(uintptr_t)me;
+      const bool bad = cur != 0 && (a < c.nodes_lo || a >= c.nodes_hi);
+      if (__any_sync(FULL, bad)) {
+        if (bad) { set_error(c, E_ILLEGAL_STATE, a, 0xD0000000ull | (u64)__LINE__); cur = 0; }
         continue;
       }
     }
-    // dst == 0: a write's durability handle (async_write) — completion only, no copy
-    uint4* d0 = reinterpret_cast<uint4*>(n0->dst);
-    uint4* d1 = reinterpret_cast<uint4*>(n1->dst);
-    // both pages move in kSvcSlice-uint4 steps per lane (kSvcSlice = 8: one step, every load of
-    // both pages in flight at once; 4: half the registers, two steps)
+    // dst == 0: a write's durability handle (async_write) — completion only, no copy.  The link
+    // is read BEFORE the barrier is released: once DONE, the requester may reuse the node at once
+    // (its next async_read re-links it into another line's list).
+    u64 mydst = 0, mynext = 0;
+    if (cur) { mydst = me->dst; mynext = me->next; }
+    for (u32 rem = all; rem;) {
+      int ln[kNP];
+      const uint4* src[kNP];
+      uint4* dst[kNP];
 #pragma unroll
-    for (int h = 0; h < 8; h += kSvcSlice) {
-      uint4 v0[kSvcSlice], v1[kSvcSlice];
-#pragma unroll
-      for (int k = 0; k < kSvcSlice; ++k) v0[k] = __ldcg(src0 + lane + 32 * (h + k));
-      if (l1 >= 0) {
-#pragma unroll
-        for (int k = 0; k < kSvcSlice; ++k) v1[k] = __ldcg(src1 + lane + 32 * (h + k));
+      for (int p = 0; p < kNP; ++p) {
+        ln[p] = rem ? __ffs(rem) - 1 : -1;
+        if (rem) rem &= rem - 1;
+        const int sl = ln[p] < 0 ? ln[0] : ln[p];
+        src[p] = reinterpret_cast<const uint4*>(line_ptr(c, __shfl_sync(FULL, line, sl)));
+        const u64 d = __shfl_sync(FULL, mydst, sl);
+        dst[p] = ln[p] < 0 ? nullptr : reinterpret_cast<uint4*>(d);
       }
-      if (d0) {
 #pragma unroll
-        for (int k = 0; k < kSvcSlice; ++k) __stcg(d0 + lane + 32 * (h + k), v0[k]);
-      }
-      if (l1 >= 0 && d1) {
+      for (int h = 0; h < 8; h += kSvcSlice) {
+        uint4 v[kNP][kSvcSlice];
 #pragma unroll
-        for (int k = 0; k < kSvcSlice; ++k) __stcg(d1 + lane + 32 * (h + k), v1[k]);
+        for (int p = 0; p < kNP; ++p)
+          if (dst[p]) {
+#pragma unroll
+            for (int k = 0; k < kSvcSlice; ++k) v[p][k] = __ldcg(src[p] + lane + 32 * (h + k));
+          }
+#pragma unroll
+        for (int p = 0; p < kNP; ++p)
+          if (dst[p]) {
+#pragma unroll
+            for (int k = 0; k < kSvcSlice; ++k) __stcg(dst[p] + lane + 32 * (h + k), v[p][k]);
+          }
       }
     }
-    __threadfence();   // every lane's page stores are performed before any barrier is released
+    // every lane's page stores are performed (its own fence) before the warp barrier, after which
+    // the owning lanes publish DONE with plain relaxed stores: fence -> bar.warp.sync -> store is
+    // the cumulative release pattern (one fence per round instead of a release per barrier word)
+    __threadfence();
     __syncwarp();
-    // The owning lane reads its node's link BEFORE releasing the barrier: once DONE, the
-    // requester may reuse the node at once (its next async_read re-links it into another line's
-    // list), so a link read after the release could walk into a foreign list.
-    if ((int)lane == l0) { cur = n0->next; st_release(&n0->done, 1u); }
-    if ((int)lane == l1) { cur = n1->next; st_release(&n1->done, 1u); }
+    if (cur) { st_relaxed(&me->done, 1u); cur = mynext; }
   }
 }
 
 
-__device__ __forceinline__ void advance_head(const DevCtx& c, u32 q, u32 who) {
+// SQ head advance over the completed prefix (_advance_head, nvme_queue.py:213-228), warp-
+// collective for one SQ q (warp-uniform): 32 consecutive entries' completion words are checked in
+// one round trip and the head moves over the whole done prefix with one CAS (a window of k
+// completions costs one pass, not k dependent load + CAS pairs).
+__device__ __forceinline__ void advance_head_warp(const DevCtx& c, u32 q, u32 who) {
   SqWords* s = &c.sqw[q];
   const u32 D = c.sq_depth;
-  u64 h = ld_acquire(&s->head);
+  const u32 lane = lane_id();
+  u64 h = 0;
+  if (lane == 0) h = ld_acquire(&s->head);
+  h = __shfl_sync(FULL, h, 0);
   bool moved = false;
   while (true) {
-    const u64 dv = ld_acquire(&c.sq_done_v[q * D + (u32)(h & (D - 1))]);
-    if (dv != h + 1) break;
-    const u64 prev = atomicCAS(&s->head, h, h + 1);
-    if (prev == h) { h = h + 1; moved = true; }
-    else h = prev;
+    const u64 e = h + lane;
+    // depth < 32: lanes past the ring alias earlier slots whose word cannot equal e + 1
+    const bool ok = ld_acquire(&c.sq_done_v[q * D + (u32)(e & (D - 1))]) == e + 1;
+    const u32 b = __ballot_sync(FULL, ok);
+    const u32 n = b == FULL ? 32u : (u32)(__ffs(~b) - 1);
+    if (n == 0) break;
+    u64 prev = 0;
+    if (lane == 0) prev = atomicCAS(&s->head, h, h + n);
+    prev = __shfl_sync(FULL, prev, 0);
+    if (prev == h) {
+      h += n;
+      moved = true;
+      if (n < 32) break;
+    } else {
+      h = prev;
+    }
   }
-  if (moved) log_ev(c, who, M_NVME, A_HEAD, q, h);
+  if (moved && lane == 0) log_ev(c, who, M_NVME, A_HEAD, q, h);
 }
 
 // One window pass over a CQ owned by the calling warp (cq_polling, agile_service.py:147-171 +
@@ -1393,7 +1438,8 @@ __device__ u32 cq_window_pass(const DevCtx& c, u32 cq, u64& off, u32& mask, u32 
   __syncwarp();
   // head advance: one leader per SQ among completed lanes
   const u32 grp = __match_any_sync(FULL, valid ? sq : 0xffffffffu);
-  if (valid && (grp & lanemask_lt()) == 0) advance_head(c, sq, who);
+  for (u32 lb = __ballot_sync(FULL, valid && (grp & lanemask_lt()) == 0); lb; lb &= lb - 1)
+    advance_head_warp(c, __shfl_sync(FULL, sq, __ffs(lb) - 1), who);
   const u32 vb = __ballot_sync(FULL, valid);
   mask |= vb;
   const u32 fullw = window == 32 ? FULL : ((1u << window) - 1u);

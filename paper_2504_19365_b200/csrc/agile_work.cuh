@@ -16,6 +16,8 @@ namespace agile {
 // grid barrier among user CTAs (the epoch Rendezvous, sim_core.py:139-159). All user CTAs are
 // co-resident by construction (the host sizes the grid from occupancy for these workloads).
 __device__ __forceinline__ bool user_grid_barrier(const DevCtx& c, u32 n_user_ctas) {
+  // one user CTA: the CTA barrier is the rendezvous (the abort check rides on it, uniformly)
+  if (n_user_ctas == 1) return __syncthreads_or(threadIdx.x == 0 && aborted(c)) == 0;
   __syncthreads();
   __shared__ int s_ok;
   if (threadIdx.x == 0) {
