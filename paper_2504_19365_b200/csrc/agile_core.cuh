@@ -1401,9 +1401,10 @@ __device__ u32 cq_window_pass(const DevCtx& c, u32 cq, u64& off, u32& mask, u32 
       atomicExch(&c.sq_done_v[idx], x.vidx + 1);
       cache = x.line != NONE && (x.kind == K_FILL || x.kind == K_WB_KEEP || x.kind == K_WB_EVICT);
       if (cache) {
-        // close the waiter stack of this fill (its version is the BUSY word's)
-        const u64 tw = ld_relaxed(&c.tags[x.line]);
-        wlh = atom_exch_acqrel(&c.wl[x.line], (((u64)tw_ver(tw)) << 55) | (1ull << 54));
+        // close the waiter stack of this fill: setting the closed bit detaches the list (every
+        // later push sees it closed and copies from the line itself; the next claim re-opens the
+        // word for its version), so no tag read is needed to rebuild the word
+        wlh = atom_or_acqrel(&c.wl[x.line], WL_CLOSED);
       }
       if (os != SQ_ISSUED) set_error(c, E_UNKNOWN_CID, sq, slot);
       log_ev(c, who, M_NVME, A_SQE_RELEASE, sq, slot, slot);

@@ -270,6 +270,9 @@ __device__ __forceinline__ u32 atom_cas_acquire(u32* p, u32 cmp, u32 val) {
 __device__ __forceinline__ u64 atom_exch_acqrel(u64* p, u64 val) {
   u64 o; asm volatile("atom.acq_rel.gpu.global.exch.b64 %0, [%1], %2;" : "=l"(o) : "l"(p), "l"(val) : "memory"); return o;
 }
+__device__ __forceinline__ u64 atom_or_acqrel(u64* p, u64 val) {
+  u64 o; asm volatile("atom.acq_rel.gpu.global.or.b64 %0, [%1], %2;" : "=l"(o) : "l"(p), "l"(val) : "memory"); return o;
+}
 __device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 __device__ __forceinline__ void fence_sc() { asm volatile("fence.sc.gpu;" ::: "memory"); }
 __device__ __forceinline__ u64 gtimer() { u64 t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t; }
