@@ -115,9 +115,10 @@ enum : u32 { WHO_USER = 0u << 30, WHO_SVC = 1u << 30, WHO_DEV = 2u << 30, WHO_HO
 struct alignas(64) SqWords {
   u64 tail;      // virtual reservation counter (CAS, capacity depth-1)
   u64 head;      // virtual head (advanced over completed prefix)
-  u64 db;        // published doorbell (virtual), strictly increasing
-  u32 db_lock;   // one publisher at a time (nvme_queue.py:114)
-  u32 pad0;
+  u64 dbl;       // doorbell word: published doorbell (virtual, strictly increasing) << 1 | lock bit
+                 // (one publisher at a time, nvme_queue.py:114): taking the lock returns the
+                 // doorbell, one release store publishes the new doorbell and unlocks
+  u64 pad0;
   u64 db_time;   // %globaltimer of the last publish (device model arrival)
   u64 fetched;   // engine-owned: next virtual index to fetch
   u64 pad1[2];
@@ -269,6 +270,9 @@ __device__ __forceinline__ u32 atom_cas_acquire(u32* p, u32 cmp, u32 val) {
 }
 __device__ __forceinline__ u64 atom_exch_acqrel(u64* p, u64 val) {
   u64 o; asm volatile("atom.acq_rel.gpu.global.exch.b64 %0, [%1], %2;" : "=l"(o) : "l"(p), "l"(val) : "memory"); return o;
+}
+__device__ __forceinline__ u64 atom_or_acquire(u64* p, u64 val) {
+  u64 o; asm volatile("atom.acquire.gpu.global.or.b64 %0, [%1], %2;" : "=l"(o) : "l"(p), "l"(val) : "memory"); return o;
 }
 __device__ __forceinline__ u64 atom_or_acqrel(u64* p, u64 val) {
   u64 o; asm volatile("atom.acq_rel.gpu.global.or.b64 %0, [%1], %2;" : "=l"(o) : "l"(p), "l"(val) : "memory"); return o;
