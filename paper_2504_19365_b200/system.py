@@ -309,7 +309,7 @@ class AgileSystem:
                                                  pages.ctypes.data), "write_blocks")
 
     def evict_blocks(self, dev, blk) -> np.ndarray:
-        """SoftwareCache.evict per block: 0 RESET, 1 DEFERRED, 2 not resident."""
+        """SoftwareCache.evict per block: 0 RESET, 1 DEFERRED, 2 not resident, 3 WRITEBACK_STARTED."""
         dev = np.ascontiguousarray(dev, dtype=np.uint32)
         blk = np.ascontiguousarray(blk, dtype=np.uint64)
         out = np.zeros(len(blk), dtype=np.int8)
