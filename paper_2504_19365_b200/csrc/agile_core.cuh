@@ -665,7 +665,10 @@ __device__ __forceinline__ u32 sq_slot_index(const DevCtx& c, u32 q, u64 v) { re
 // publishes once; everyone loops until the doorbell passed `target`.  Lock and doorbell share one
 // word (doorbell << 1 | lock): the acquiring atomic OR returns the current doorbell and one release
 // store publishes the new doorbell and unlocks (3 round trips fewer than lock word + doorbell word).
-__device__ bool ring_doorbell_until(const DevCtx& c, u32 q, u64 target, u32 who) {
+// `start`: first entry of the caller's own contiguous range [start, target) (all UPDATED by the
+// calling warp before the call); when the published doorbell is exactly `start`, the lock holder
+// flips its own range without scanning (one round trip less) and publishes `target`.
+__device__ bool ring_doorbell_until(const DevCtx& c, u32 q, u64 target, u32 who, u64 start = ~0ull) {
   const u32 lane = lane_id();
   SqWords* s = &c.sqw[q];
   const u32 D = c.sq_depth;
@@ -694,7 +697,19 @@ __device__ bool ring_doorbell_until(const DevCtx& c, u32 q, u64 target, u32 who)
     if (got) {
       const u64 old = __shfl_sync(FULL, ow, 0) >> 1;
       u64 v = old;
-      while (true) {
+      const bool fast = old == start && target > start && target - start <= 32;
+      if (fast) {
+        // fast path: the range right after the doorbell is the caller's own (UPDATED by its
+        // lanes before the warp barrier that precedes this call)
+        const u64 vi = start + lane;
+        if (vi < target) {
+          if (atom_cas_acqrel(&c.sq_state[sq_slot_index(c, q, vi)], SQ_UPDATED, SQ_ISSUED) != SQ_UPDATED)
+            set_error(c, E_PROTOCOL, q, vi);
+          log_ev(c, who, M_NVME, A_SQE_ISSUED, q, vi & (D - 1), vi & (D - 1));
+        }
+        v = target;
+      }
+      while (!fast) {
         // 64 entries per round trip (two per lane): a full warp's submission (32 UPDATED
         // entries) is found and bounded in one scan instead of two
         const u64 vi0 = v + lane, vi1 = v + 32 + lane;
@@ -822,7 +837,7 @@ __device__ bool submit_warp(const DevCtx& c, bool has, u32 dev, u64 blk, u32 lin
       lead_b &= lead_b - 1;
       const u32 qL = __shfl_sync(FULL, q, L);
       const u64 endL = __shfl_sync(FULL, t + m, L);
-      if (!ring_doorbell_until(c, qL, endL, who)) return false;
+      if (!ring_doorbell_until(c, qL, endL, who, __shfl_sync(FULL, t, L))) return false;
     }
     const u32 gb = __ballot_sync(FULL, got);
     if (lane == 0 && gb) atomicAdd(&c.stats[S_ENQUEUES], (u64)__popc(gb));

@@ -174,13 +174,21 @@ struct ReadsWork {
   __device__ __forceinline__ u32 cta_tasks(u32 uidx) const {
     return min(tasks - min(tasks, uidx * kCtaThreads), (u32)kCtaThreads);
   }
-  __device__ void issue(const DevCtx& c, u32 uidx, u32 e, u32 set, u32 who, u32 sq_start) const {
+  // the key of this thread's first request of epoch e (loaded ahead of the epoch's wait, so the
+  // issue after the barrier does not start with a dependent load)
+  __device__ u64 first_key(u32 uidx, u32 e) const {
+    const u32 total = cta_tasks(uidx) * reads;
+    if (e >= epochs || threadIdx.x >= total) return 0ull;
+    const u32 t = uidx * kCtaThreads + threadIdx.x / reads, i = threadIdx.x % reads;
+    return keys[((u64)e * tasks + t) * reads + i];
+  }
+  __device__ void issue(const DevCtx& c, u32 uidx, u32 e, u32 set, u32 who, u32 sq_start, u64 key0) const {
     const u32 total = cta_tasks(uidx) * reads;
     for (u32 k = 0; k * kCtaThreads < total; ++k) {
       const u32 f = k * kCtaThreads + threadIdx.x;
       const bool a = f < total;
       const u32 t = uidx * kCtaThreads + (a ? f / reads : 0), i = a ? f % reads : 0;
-      const u64 key = a ? keys[((u64)e * tasks + t) * reads + i] : 0ull;
+      const u64 key = !a ? 0ull : k == 0 ? key0 : keys[((u64)e * tasks + t) * reads + i];
       const u64 slot = ((u64)t * 2 + set) * reads + i;
       async_read_warp(c, a, key, nodes + (a ? slot : 0), bufs + (a ? slot : 0) * 256, who,
                       sq_start + k + e * reads);
@@ -207,8 +215,10 @@ struct ReadsWork {
     const u32 sq_start = uidx * kCtaWarps + (threadIdx.x >> 5);
     if (uidx == 0 && threadIdx.x == 0) epoch_t[0] = gtimer();
     if (!async_mode) {
+      u64 k0 = first_key(uidx, 0);
       for (u32 e = 0; e < epochs; ++e) {
-        issue(c, uidx, e, 0, who, sq_start);
+        issue(c, uidx, e, 0, who, sq_start, k0);
+        k0 = first_key(uidx, e + 1);
         wait_set(c, uidx, 0);
         // compute starts only after every task's data arrived (bench/ctc.py:80-83)
         if (!user_grid_barrier(c, nusers)) return;
@@ -216,7 +226,7 @@ struct ReadsWork {
         compute_spin(compute_ns);
       }
     } else {
-      issue(c, uidx, 0, 0, who, sq_start);
+      issue(c, uidx, 0, 0, who, sq_start, first_key(uidx, 0));
       // every task's epoch-0 reads are queued before any epoch-1 read: a task that finished its
       // issue early would otherwise interleave epoch-1 commands into the device FIFO ahead of
       // other tasks' epoch-0 commands and delay the first wait by a whole epoch (the reference's
@@ -225,7 +235,7 @@ struct ReadsWork {
       for (u32 e = 0; e < epochs; ++e) {
         const u32 cur = e & 1u;
         // the next epoch's fetches ride under this epoch's compute (bench/ctc.py:47-70)
-        if (e + 1 < epochs) issue(c, uidx, e + 1, cur ^ 1u, who, sq_start);
+        if (e + 1 < epochs) issue(c, uidx, e + 1, cur ^ 1u, who, sq_start, first_key(uidx, e + 1));
         wait_set(c, uidx, cur);
         if (!user_grid_barrier(c, nusers)) return;
         if (uidx == 0 && threadIdx.x == 0) epoch_t[e + 1] = gtimer();
