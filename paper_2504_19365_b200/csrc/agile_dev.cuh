@@ -282,7 +282,10 @@ __device__ __forceinline__ void fence_sc() { asm volatile("fence.sc.gpu;" ::: "m
 __device__ __forceinline__ u64 gtimer() { u64 t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t; }
 __device__ __forceinline__ u32 lane_id() { return threadIdx.x & 31; }
 __device__ __forceinline__ u32 lanemask_lt() { u32 m; asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m)); return m; }
-__device__ __forceinline__ void nap(u32 ns) { __nanosleep(ns); }
+#ifndef AGILE_NAP_MAX_NS
+#define AGILE_NAP_MAX_NS 0xffffffffu   // probe builds cap every backoff nap (tools: nap A/B)
+#endif
+__device__ __forceinline__ void nap(u32 ns) { __nanosleep(ns < AGILE_NAP_MAX_NS ? ns : AGILE_NAP_MAX_NS); }
 
 __device__ __forceinline__ void set_error(const DevCtx& c, u32 code, u64 a, u64 b) {
   if (atomicCAS(&c.pw->error_code, 0u, code) == 0u) {
