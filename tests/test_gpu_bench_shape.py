@@ -75,3 +75,26 @@ def test_cache_sweep_threshold_crossing():
             assert speedup <= 1.02, (lines, speedup)
         elif lines >= 4 * working_set:
             assert speedup > 1.0, (lines, speedup)
+
+
+def test_ctc_sweep_default_shape():
+    # the reference's criterion 4 (tests/test_acceptance.py:142-162) on the default ctc_sweep config:
+    # the GPU curve has the same rise-peak-fall form, but its per-epoch issue/completion chain
+    # (~29 us of dependent L2 round trips) against the reference's modelled ~2 us moves
+    # speedup(0) to ~1.19 (reference band [0.95, 1.1]) and the peak to CTC ~0.5-0.75 at ~1.72x
+    # (reference: >= 1.7 within CTC [0.75, 1.0]); this pins the measured shape against regressions
+    from paper_2504_19365_b200.bench.ctc import run_ctc_sweep
+    from paper_2504_19365_b200.cli import build_config
+
+    rows = run_ctc_sweep(build_config("ctc_sweep")).rows
+    ctcs = [r[0] for r in rows]
+    speedups = [r[3] for r in rows]
+    assert 0.95 <= speedups[0] <= 1.3, speedups
+    peak_i = max(range(len(rows)), key=lambda i: speedups[i])
+    assert speedups[peak_i] >= 1.6, speedups
+    assert 0.4 <= ctcs[peak_i] <= 1.0, (ctcs, speedups)
+    assert speedups[-1] <= speedups[peak_i]
+    for i in range(peak_i):                  # rise and fall are monotone, as in the reference
+        assert speedups[i + 1] >= speedups[i] * 0.95, speedups
+    for i in range(peak_i, len(rows) - 1):
+        assert speedups[i + 1] <= speedups[i] * 1.05, speedups
