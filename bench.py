@@ -170,6 +170,31 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm), "source": "nvidia-smi -lms 100"}
 
 
+def bind_local_numa(gpu: int) -> str:
+    """Pin this process to the CPUs NVML reports as local to the GPU, so the pinned host buffers it
+    allocates afterwards (page store, index uploads, pooled-output downloads) come from the GPU's
+    NUMA node instead of wherever the launcher happened to place the process.  AGILE_NO_BIND=1
+    skips it.  Returns what was done (reported in the JSON line)."""
+    if os.environ.get("AGILE_NO_BIND") == "1":
+        return "off (AGILE_NO_BIND=1)"
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+        idx = int(vis.split(",")[gpu]) if vis and vis.split(",")[0].isdigit() else gpu
+        h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+        ncpu = os.cpu_count() or 1
+        words = pynvml.nvmlDeviceGetCpuAffinity(h, (ncpu + 63) // 64)
+        cpus = {64 * i + b for i, w in enumerate(words) for b in range(64) if (w >> b) & 1 and 64 * i + b < ncpu}
+        cpus &= os.sched_getaffinity(0)
+        if not cpus:
+            return "skipped (no local CPUs in the allowed set)"
+        os.sched_setaffinity(0, cpus)
+        return f"{len(cpus)} GPU-local CPUs"
+    except Exception as e:   # NVML missing or no affinity info: leave the placement alone
+        return f"skipped ({type(e).__name__})"
+
+
 def _plan(args, world):
     """Per-rank sizes (cache bytes, table bytes held by the rank's page store).
     N = 1 (configs[1]): a 16 GiB cache over 4x its size of tables.  N > 1 (configs[4]): 1 TiB of
@@ -390,6 +415,7 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
     assert world == args.gpus or "RANK" not in os.environ, "--gpus must match WORLD_SIZE"
+    numa = bind_local_numa(local)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
@@ -560,7 +586,7 @@ def main():
             "roofline": roofline, "roofline_hbm": roofline_hbm,
             "hit_rate": 1.0 - miss_lookups / max(1, lookups_local),
             # per step: the infra grid + the PDL user grid of one agile_embbag run (1 in fused mode)
-            "gpu_launches": args.steps * (1 if system.launch_mode == "fused" else 2), "launch_mode": system.launch_mode,
+            "gpu_launches": args.steps * (1 if system.launch_mode == "fused" else 2), "launch_mode": system.launch_mode, "host_numa": numa,
             "clocks": clk, "setup_s": setup_s,
             "cache_warm": {"batches": warm, "seconds": warm_s}}
 

@@ -24,6 +24,7 @@ B, T, L, D = bench.B, bench.T, bench.L, bench.D
 
 def main():
     steps = 10
+    print("numa:", bench.bind_local_numa(0), file=sys.stderr)
     dev = torch.device("cuda", 0)
     rows_all = table_rows(64 << 30, D, T)
     plan = plan_shards(rows_all, 1, D)
