@@ -1337,11 +1337,13 @@ __device__ void deliver_waiters_warp(const DevCtx& c, u64 cur, u32 line) {
           }
       }
     }
-    // every lane's page stores are performed (its own fence) before the warp barrier, after which
-    // the owning lanes publish DONE with plain relaxed stores: fence -> bar.warp.sync -> store is
-    // the cumulative release pattern (one fence per round instead of a release per barrier word)
-    __threadfence();
+    // release pattern for the whole round: every lane's page stores happen before the warp barrier
+    // (bar.warp.sync orders memory among its participants), the fence after it is cumulative over
+    // them, and each owning lane's DONE store follows that fence in its own program order — so a
+    // requester whose acquire load sees DONE sees the page (one fence per round instead of an
+    // st.release per barrier word, which serialised across the diverged owning lanes)
     __syncwarp();
+    __threadfence();
     if (cur) { st_relaxed(&me->done, 1u); cur = mynext; }
   }
 }
