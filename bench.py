@@ -81,6 +81,20 @@ def _link_peak():
         return 51.4
 
 
+def _nvml_handle(pynvml, gpu: int):
+    """NVML handle of CUDA device `gpu`, matched by PCI address (CUDA's device order need not be
+    NVML's); falls back to the CUDA_VISIBLE_DEVICES / index mapping."""
+    try:
+        import torch
+        pr = torch.cuda.get_device_properties(gpu)
+        bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+        return pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+    except Exception:
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+        idx = int(vis.split(",")[gpu]) if vis and vis.split(",")[0].isdigit() else gpu
+        return pynvml.nvmlDeviceGetHandleByIndex(idx)
+
+
 class Clocks:
     """SM clocks and clock-event reasons sampled DURING the timed region (the recipe's clocks line):
     NVML from a sampling thread every 2 ms (a timed region of ~50 ms gets ~25 samples); nvidia-smi
@@ -104,9 +118,7 @@ class Clocks:
 
             import pynvml
             pynvml.nvmlInit()
-            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
-            idx = int(vis.split(",")[self.gpu]) if vis and vis.split(",")[0].isdigit() else self.gpu
-            h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            h = _nvml_handle(pynvml, self.gpu)
             bits = {"hw_slowdown": pynvml.nvmlClocksThrottleReasonHwSlowdown,
                     "hw_thermal_slowdown": pynvml.nvmlClocksThrottleReasonHwThermalSlowdown,
                     "sw_thermal_slowdown": pynvml.nvmlClocksThrottleReasonSwThermalSlowdown,
@@ -180,9 +192,7 @@ def bind_local_numa(gpu: int) -> str:
     try:
         import pynvml
         pynvml.nvmlInit()
-        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
-        idx = int(vis.split(",")[gpu]) if vis and vis.split(",")[0].isdigit() else gpu
-        h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+        h = _nvml_handle(pynvml, gpu)
         ncpu = os.cpu_count() or 1
         words = pynvml.nvmlDeviceGetCpuAffinity(h, (ncpu + 63) // 64)
         cpus = {64 * i + b for i, w in enumerate(words) for b in range(64) if (w >> b) & 1 and 64 * i + b < ncpu}
