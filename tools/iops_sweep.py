@@ -1,3 +1,6 @@
+"""Closed-loop 4 KiB IOPS sweep in link mode (GPU-box tool): engine / service warp counts x
+concurrency, completions per second through async_read with service-side waiter delivery
+(profiles/iops_p.txt)."""
 import sys, os, json
 sys.path.insert(0, os.getcwd()); sys.path.insert(0, "tests")
 from conftest import small_config
