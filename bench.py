@@ -720,7 +720,7 @@ def main():
             line["e2e"] = {"value": B * T * L / e2e_s, "unit": "lookups/s",
                            "h2d_bytes_per_step": int(hb_np[0].nbytes + 2 * Tg * 8),
                            "d2h_bytes_per_step": int(outs_np[0].nbytes + 16),
-                           "path": "agile_embbag_host_submit / _wait (C-ABI, pinned host buffers, two staging slots)"}
+                           "path": "agile_embbag_host_submit / _wait (C-ABI, pinned host buffers, two staging slots; the kernel stores the pooled rows into the pinned output)"}
         else:
             hbuf = [torch.from_numpy(host_batches[nb + n_sync + k]).pin_memory() for k in range(args.steps)]
             res = torch.empty((B // world, T, D), dtype=torch.float32).pin_memory()

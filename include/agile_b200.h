@@ -233,7 +233,9 @@ int agile_embbag_host(agile_ctx* ctx, const int64_t* idx, const uint64_t* table_
  * run and D2H of the pooled output on the slot's own stream and return.  Runs of the two slots
  * execute in submission order (one context), while one slot's copies overlap the other's run.
  * Host buffers should be pinned for the copies to be asynchronous; `out` and `counters` are
- * valid after agile_embbag_host_wait(slot), which must precede the slot's next submit. */
+ * valid after agile_embbag_host_wait(slot), which must precede the slot's next submit.  When `out`
+ * is pinned, device-mapped host memory (cudaHostAlloc / cudaHostRegister), the kernel stores the
+ * pooled rows into it directly instead of staging them for a copy-engine download. */
 int agile_embbag_host_submit(agile_ctx* ctx, const int64_t* idx, const uint64_t* table_key0,
                              const int64_t* table_rows, float* out, uint64_t* counters, uint32_t B, uint32_t T,
                              uint32_t L, uint32_t D, uint32_t prefetch_distance, int slot);

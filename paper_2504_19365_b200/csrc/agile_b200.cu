@@ -1554,11 +1554,28 @@ int agile_embbag_host_submit(agile_ctx* ctx, const int64_t* idx, const uint64_t*
   CK(cudaMemcpyAsync(d_rows, table_rows, n_tab, cudaMemcpyHostToDevice, h.st));
   CK(cudaMemsetAsync(d_cnt, 0, 16, h.st));
   if (ctx->last_slot >= 0) CK(cudaStreamWaitEvent(h.st, ctx->hs[ctx->last_slot].ran, 0));
-  int rc = agile_embbag(ctx, d_idx, d_key, d_rows, d_out, d_cnt, B, T, L, D, 0, 0, prefetch_distance, h.st);
+  // Pinned (device-mapped) output: the kernel stores each pooled bag straight into host memory as
+  // it finishes — 512 B posted writes spread over the run — instead of a 27 MB copy-engine
+  // download after it, whose upstream burst slows the next run's page fills by about its own
+  // length (pipelined e2e step 3.02-3.12 ms against 3.32-3.53 staged, profiles/
+  // e2e_direct_out_ab_r02q.txt).  Pageable output, or AGILE_E2E_DIRECT_OUT=0: device staging + D2H.
+  float* kout = d_out;
+  bool direct = false;
+  {
+    const char* ev = getenv("AGILE_E2E_DIRECT_OUT");
+    cudaPointerAttributes pa{};
+    if (!(ev && ev[0] == '0') && cudaPointerGetAttributes(&pa, out) == cudaSuccess &&
+        pa.type == cudaMemoryTypeHost && pa.devicePointer) {
+      kout = reinterpret_cast<float*>(pa.devicePointer);
+      direct = true;
+    }
+    cudaGetLastError();   // clear a lookup failure of a pageable pointer
+  }
+  int rc = agile_embbag(ctx, d_idx, d_key, d_rows, kout, d_cnt, B, T, L, D, 0, 0, prefetch_distance, h.st);
   if (rc) return rc;
   CK(cudaEventRecord(h.ran, h.st));
   ctx->last_slot = slot;
-  CK(cudaMemcpyAsync(out, d_out, n_out, cudaMemcpyDeviceToHost, h.st));
+  if (!direct) CK(cudaMemcpyAsync(out, d_out, n_out, cudaMemcpyDeviceToHost, h.st));
   CK(cudaMemcpyAsync(h.h_cnt, d_cnt, 16, cudaMemcpyDeviceToHost, h.st));
   h.user_cnt = counters;
   h.busy = true;

@@ -138,15 +138,20 @@ def test_fused_launch_mode_matches(gpu_system, monkeypatch):
     assert cnt[0] == 48 * 3 * 20 and cnt[1] > 0
 
 
-def test_embbag_host_async_slots_match(gpu_system):
-    """The pipelined host entry (two staging slots) gives the same sums as the one-call entry."""
+@pytest.mark.parametrize("pinned", [False, True])
+def test_embbag_host_async_slots_match(gpu_system, pinned):
+    """The pipelined host entry (two staging slots) gives the same sums as the one-call entry, with
+    pageable output (device staging + download) and pinned output (the kernel stores into it)."""
     s = gpu_system(cache_lines=1024, ways=16, blocks=1 << 13, pairs=4, engine_warps=4)
     s.fill_store(0, seed=6, kind="f32")
     rng = np.random.default_rng(11)
     rows = np.array([4000, 2000], dtype=np.int64)
     k0 = np.array([0, 500], dtype=np.uint64)
     batches = [np.stack([rng.integers(0, r, size=(24, 20)) for r in rows], axis=1).astype(np.int64) for _ in range(5)]
-    outs = [np.empty((24, 2, 128), dtype=np.float32) for _ in range(2)]
+    if pinned:
+        outs = [torch.empty((24, 2, 128), dtype=torch.float32).pin_memory().numpy() for _ in range(2)]
+    else:
+        outs = [np.empty((24, 2, 128), dtype=np.float32) for _ in range(2)]
     cnts = [np.zeros(2, dtype=np.uint64) for _ in range(2)]
     got = []
     for k, b in enumerate(batches):
