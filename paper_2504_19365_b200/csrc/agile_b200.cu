@@ -1522,6 +1522,23 @@ int agile_bfs_level(agile_ctx* ctx, const int64_t* row_ptr, uint32_t v0, const i
   return launch(ctx, w, users, st);
 }
 
+}  // extern "C"
+
+// Device alias of a pinned, device-mapped host output buffer (nullptr: pageable, or
+// AGILE_E2E_DIRECT_OUT=0): the host-buffer entries then let K5 store the pooled rows into it.
+static float* mapped_host_out(float* out) {
+  const char* ev = getenv("AGILE_E2E_DIRECT_OUT");
+  if (ev && ev[0] == '0') return nullptr;
+  cudaPointerAttributes pa{};
+  float* r = nullptr;
+  if (cudaPointerGetAttributes(&pa, out) == cudaSuccess && pa.type == cudaMemoryTypeHost && pa.devicePointer)
+    r = reinterpret_cast<float*>(pa.devicePointer);
+  cudaGetLastError();   // clear a lookup failure of a pageable pointer
+  return r;
+}
+
+extern "C" {
+
 int agile_embbag_host_submit(agile_ctx* ctx, const int64_t* idx, const uint64_t* table_key0,
                              const int64_t* table_rows, float* out, uint64_t* counters, uint32_t B, uint32_t T,
                              uint32_t L, uint32_t D, uint32_t prefetch_distance, int slot) {
@@ -1559,18 +1576,9 @@ int agile_embbag_host_submit(agile_ctx* ctx, const int64_t* idx, const uint64_t*
   // download after it, whose upstream burst slows the next run's page fills by about its own
   // length (pipelined e2e step 3.02-3.12 ms against 3.32-3.53 staged, profiles/
   // e2e_direct_out_ab_r02q.txt).  Pageable output, or AGILE_E2E_DIRECT_OUT=0: device staging + D2H.
-  float* kout = d_out;
-  bool direct = false;
-  {
-    const char* ev = getenv("AGILE_E2E_DIRECT_OUT");
-    cudaPointerAttributes pa{};
-    if (!(ev && ev[0] == '0') && cudaPointerGetAttributes(&pa, out) == cudaSuccess &&
-        pa.type == cudaMemoryTypeHost && pa.devicePointer) {
-      kout = reinterpret_cast<float*>(pa.devicePointer);
-      direct = true;
-    }
-    cudaGetLastError();   // clear a lookup failure of a pageable pointer
-  }
+  float* kout = mapped_host_out(out);
+  const bool direct = kout != nullptr;
+  if (!direct) kout = d_out;
   int rc = agile_embbag(ctx, d_idx, d_key, d_rows, kout, d_cnt, B, T, L, D, 0, 0, prefetch_distance, h.st);
   if (rc) return rc;
   CK(cudaEventRecord(h.ran, h.st));
@@ -1615,9 +1623,10 @@ int agile_embbag_host(agile_ctx* ctx, const int64_t* idx, const uint64_t* table_
   CK(cudaMemcpyAsync(d_key, table_key0, n_tab, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(d_rows, table_rows, n_tab, cudaMemcpyHostToDevice, st));
   CK(cudaMemsetAsync(d_cnt, 0, 16, st));
-  int rc = agile_embbag(ctx, d_idx, d_key, d_rows, d_out, d_cnt, B, T, L, D, 0, 0, prefetch_distance, st);
+  float* kout = mapped_host_out(out);   // pinned output: the kernel stores into it directly
+  int rc = agile_embbag(ctx, d_idx, d_key, d_rows, kout ? kout : d_out, d_cnt, B, T, L, D, 0, 0, prefetch_distance, st);
   if (rc) return rc;
-  CK(cudaMemcpyAsync(out, d_out, n_out, cudaMemcpyDeviceToHost, st));
+  if (!kout) CK(cudaMemcpyAsync(out, d_out, n_out, cudaMemcpyDeviceToHost, st));
   uint64_t cnt[2] = {0, 0};
   CK(cudaMemcpyAsync(cnt, d_cnt, 16, cudaMemcpyDeviceToHost, st));
   rc = agile_sync(ctx, st);

@@ -64,14 +64,17 @@ def test_embbag_shapes(gpu_system, D, L):
     assert err < 1e-5
 
 
-def test_embbag_host_entry_matches_device_entry(gpu_system):
+@pytest.mark.parametrize("pinned", [False, True])
+def test_embbag_host_entry_matches_device_entry(gpu_system, pinned):
+    # pageable output: staged + downloaded; pinned output: the kernel stores into it directly
     s = gpu_system(cache_lines=1024, ways=16, blocks=1 << 13, pairs=4, engine_warps=4)
     s.fill_store(0, seed=4, kind="f32")
     rng = np.random.default_rng(1)
     rows = np.array([4000, 4000], dtype=np.int64)
     idx = rng.integers(0, 4000, size=(16, 2, 20)).astype(np.int64)
     k0 = np.array([0, 500], dtype=np.uint64)
-    out, cnt = s.embbag_host(idx, k0, rows, 128, prefetch_distance=1)
+    o = torch.full((16, 2, 128), float("nan")).pin_memory().numpy() if pinned else None
+    out, cnt = s.embbag_host(idx, k0, rows, 128, prefetch_distance=1, out=o)
     ref = embbag_reference(4, 0, k0, idx, 128)
     assert np.max(np.abs(out - ref) / np.maximum(np.abs(ref), 1)) < 1e-5
     assert int(cnt[0]) == 16 * 2 * 20
