@@ -463,7 +463,8 @@ def main():
     scatter = not args.no_scatter
     nb = args.warmup + args.steps
     n_sync = max(2, args.steps // 2)
-    n_e2e = args.steps
+    E2E_PASSES = 3
+    n_e2e = E2E_PASSES * args.steps
     host_batches = [make_batch(SEED, s, rows_all, B, L, ALPHA, scatter, my_tables)
                     for s in range(nb + n_sync + n_e2e + 1)]
     dbat = [torch.from_numpy(x).to(dev) for x in host_batches[:nb + n_sync]]
@@ -700,24 +701,31 @@ def main():
         if world == 1:
             # fresh batches (never seen by the cache in this run), like the timed region
             # host buffers in pinned memory, as a serving frontend would hold them
-            hb_np = [torch.from_numpy(host_batches[nb + n_sync + k]).pin_memory().numpy() for k in range(args.steps)]
-            outs_np = [torch.empty((B, Tg, D), dtype=torch.float32).pin_memory().numpy() for _ in range(2)]
+            # Three passes, each with freshly pinned host buffers and fresh batches; the median
+            # pass is the value (the box's host side has multi-ms slow phases that can hold a whole
+            # pass; every pass is listed)
             keyh = torch.from_numpy(descs["key0"].view(np.int64).copy()).pin_memory().numpy().view(np.uint64)
             rowsh = torch.from_numpy(my_rows.copy()).pin_memory().numpy()
-            cnts = [np.zeros(2, dtype=np.uint64) for _ in range(2)]
-            # pipelined through the C-ABI: step k's pooled output leaves (D2H) and step k+1's
-            # indices arrive (H2D) while a run is on the device; every copy is inside the region
-            t_e = time.perf_counter()
-            for k in range(args.steps):
-                slot = k % 2
-                if k >= 2:
+            passes = []
+            for ps in range(E2E_PASSES):
+                b0 = nb + n_sync + ps * args.steps
+                hb_np = [torch.from_numpy(host_batches[b0 + k]).pin_memory().numpy() for k in range(args.steps)]
+                outs_np = [torch.empty((B, Tg, D), dtype=torch.float32).pin_memory().numpy() for _ in range(2)]
+                cnts = [np.zeros(2, dtype=np.uint64) for _ in range(2)]
+                # pipelined through the C-ABI: step k's pooled output leaves and step k+1's indices
+                # arrive while a run is on the device; every copy is inside the region
+                t_e = time.perf_counter()
+                for k in range(args.steps):
+                    slot = k % 2
+                    if k >= 2:
+                        system.embbag_host_wait(slot)
+                    system.embbag_host_submit(hb_np[k], keyh, rowsh, D, outs_np[slot], cnts[slot], slot,
+                                              prefetch_distance=args.prefetch)
+                for slot in (0, 1):
                     system.embbag_host_wait(slot)
-                system.embbag_host_submit(hb_np[k], keyh, rowsh, D, outs_np[slot], cnts[slot], slot,
-                                          prefetch_distance=args.prefetch)
-            for slot in (0, 1):
-                system.embbag_host_wait(slot)
-            e2e_s = (time.perf_counter() - t_e) / args.steps
-            line["e2e"] = {"value": B * T * L / e2e_s, "unit": "lookups/s",
+                passes.append(B * T * L * args.steps / (time.perf_counter() - t_e))
+            line["e2e"] = {"value": statistics.median(passes), "unit": "lookups/s",
+                           "passes": passes, "method": f"median of {E2E_PASSES} passes of {args.steps} steps",
                            "h2d_bytes_per_step": int(hb_np[0].nbytes + 2 * Tg * 8),
                            "d2h_bytes_per_step": int(outs_np[0].nbytes + 16),
                            "path": "agile_embbag_host_submit / _wait (C-ABI, pinned host buffers, two staging slots; the kernel stores the pooled rows into the pinned output)"}
